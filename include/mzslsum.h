@@ -1,0 +1,208 @@
+/*
+ * mzslsum.h -- C ABI of the B200 (sm_100a) implementation of the hot path of
+ * arxiv 1811.10074, "Parallel sliding window sums".
+ *
+ * The library (paper_1811_10074_b200/libmzslsum.so) computes:
+ *   - sliding window sums y_i = x_i (+) ... (+) x_{i+w-1}        (Eq. 2)
+ *     by the block suffix/prefix decomposition of Algorithm 2    (L122-152)
+ *     or by O(log w) doubling for commutative operators          (abstract L8, L150, L229);
+ *   - 2-bit packing of DNA                                        (Sec. 2.4);
+ *   - minimizers: rolling k-mer code + invertible hash + sliding window minimum
+ *     (the "faster version of the vector input algorithm", L152) + compaction of the
+ *     distinct (seed, position) pairs                             (Sec. 2.4, Fig. 2);
+ *   - a seed table: pointer table + position table                (Sec. 2.4, Fig. 1),
+ *     bucketed on the top bits of the hash, with the phase functions of the
+ *     multi-GPU build (count / partition / finalize; NCCL runs between them).
+ *
+ * CONVENTIONS (all entry points)
+ *   - Every array argument is a DEVICE pointer owned by the caller, unless the
+ *     parameter name starts with h_ (host).  The library never frees caller memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     *_ex and phase functions are asynchronous and stream-ordered; the plain
+ *     convenience calls (slsum_run, mz_extract, seedtable_build with h_m) synchronize.
+ *   - Scratch memory comes from the caller's workspace `ws` of `ws_bytes` bytes,
+ *     sized by the matching *_workspace_bytes call; passing ws = NULL makes the call
+ *     allocate (cudaMallocAsync) and free its own scratch on `stream`.
+ *   - Return value 0 = success; negative = error code below (see slsum_strerror).
+ *     Degenerate sizes are NOT errors: n < w gives 0 sums, a sequence shorter
+ *     than k + w - 1 gives 0 minimizers, m = 0 gives an all-zero pointer table.
+ *   - Integer results are bit-identical for any stream, tile size or GPU count.
+ *   - Thread safety: stateless; concurrent calls are safe with distinct workspaces.
+ */
+#ifndef MZSLSUM_H
+#define MZSLSUM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ errors */
+#define SLSUM_OK            0
+#define SLSUM_EINVAL       (-1)  /* NULL pointer, w = 0, k not in [1,31], bad op/kind/bits */
+#define SLSUM_EUNSUPPORTED (-2)  /* non-commutative op on the COMMUTATIVE path          */
+#define SLSUM_ECAPACITY    (-3)  /* more records than `capacity` (sync calls only)      */
+#define SLSUM_ECUDA        (-4)  /* CUDA launch / runtime error                         */
+#define SLSUM_ENOMEM       (-5)  /* workspace too small / allocation failed            */
+
+const char* slsum_strerror(int rc);
+/* library version, e.g. 0x000100 */
+int slsum_version(void);
+
+/* ------------------------------------------------------------------ sliding sums
+ * Eq. 2: y_i = x_i (+) x_{i+1} (+) ... (+) x_{i+w-1}, exactly w
+ * addends, for i in [0, n-w]; y receives max(0, n-w+1) elements.
+ *
+ * op (element type of x and y):
+ *   SLSUM_MIN_U32       uint32 min
+ *   SLSUM_MAX_U32       uint32 max
+ *   SLSUM_ADD_U32       uint32 add modulo 2^32
+ *   SLSUM_ADD_F32       float32 add (result within 1e-5 |ref| + 1e-6 w of the strict
+ *                       left fold; the decomposition regroups the w terms)
+ *   SLSUM_AFFINE_U32X2  pairs (a, b) of uint32 (8 bytes per element), the affine map
+ *                       t -> a t + b over Z/2^32 composed left-after-right:
+ *                       (a,b) (+) (c,d) = (a c, a d + b).  Associative and NOT
+ *                       commutative: proves that a path preserves operand order.
+ *   SLSUM_MIN_U64       uint64 min (e.g. (key << 32 | pos) argmin keys)
+ * path:
+ *   SLSUM_PATH_GENERIC      Algorithm 2's decomposition with blocks of length w:
+ *                           y_i = S[i] (+) P[i+w-1] (S = suffix fold to the end of i's
+ *                           block, P = prefix fold from the start of its block), 3 (+)
+ *                           per output, any associative op, operand order preserved.
+ *   SLSUM_PATH_COMMUTATIVE  ceil(log2 w) doubling rounds (abstract L8: O(P/log w) "for a
+ *                           sum with commutative operator"); rejects AFFINE with
+ *                           SLSUM_EUNSUPPORTED.
+ *   SLSUM_PATH_AUTO         GENERIC (the faster path on B200 for every w).
+ * x, y: device arrays of n and max(0, n-w+1) elements; x and y must not overlap.
+ */
+enum {
+  SLSUM_MIN_U32 = 0,
+  SLSUM_MAX_U32 = 1,
+  SLSUM_ADD_U32 = 2,
+  SLSUM_ADD_F32 = 3,
+  SLSUM_AFFINE_U32X2 = 4,
+  SLSUM_MIN_U64 = 5
+};
+enum { SLSUM_PATH_GENERIC = 0, SLSUM_PATH_COMMUTATIVE = 1, SLSUM_PATH_AUTO = 2 };
+
+/* GENERIC path on the default stream; returns after completion. */
+int slsum_run(int op, uint32_t w, const void* x, void* y, uint64_t n);
+/* asynchronous on `stream`; no workspace needed. */
+int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n, int path, void* stream);
+
+/* ------------------------------------------------------------------ 2-bit packing
+ * Sec. 2.4 (L67) sequence R = r_0 r_1 ...; encoding per DESIGN.md R6/R7:
+ * A/a -> 0, C/c -> 1, G/g -> 2, T/t -> 3; every other byte is invalid (code 0).
+ * words[t] (uint64, ceil(n/32) of them) holds bases 32t..32t+31, MSB-first: base 32t+j
+ * at bits (63-2j, 62-2j).  invalid[t] (uint32, ceil(n/32)) has bit j set iff base
+ * 32t+j is invalid.  Bits past n are 0.  seq: n device bytes.
+ */
+int mz_encode(const uint8_t* seq, uint64_t n, uint64_t* words, uint32_t* invalid, void* stream);
+
+/* ------------------------------------------------------------------ minimizers
+ * PAPER.md L85 (Sec. 2.4, Fig. 2) with the readings of DESIGN.md:
+ *   k-mer q       code_q = sum_{t<k} b_{q+t} 4^(k-1-t) (2k bits, MSB-first, R6)
+ *   key_q         H_2k(code_q) (MZ_KEY_HASH; the masked Wang/minimap2 mix, R5)
+ *                 or code_q (MZ_KEY_RAW, Fig. 2's lexicographic order, R4)
+ *   window i      the w k-mers q = i .. i+w-1 = bases [i, i+k+w-2] (R1); valid iff all
+ *                 those bases are A/C/G/T and no segment (read) starts in (i, i+k+w-2] (R8)
+ *   p_i           the leftmost position of the minimum key in window i (R2)
+ *   output        every distinct (key[p], pos_base + p) selected by a valid window,
+ *                 ascending by position (L85 "stored only once"), each pair emitted by
+ *                 the first valid window selecting it (change rule, R3).
+ * Input kinds:
+ *   MZ_IN_ASCII    seq = n bytes
+ *   MZ_IN_PACKED2  seq = ceil(n/32) uint64 words as written by mz_encode; invalid =
+ *                  ceil(n/32) uint32 bitmap words, or NULL if every base is valid
+ * read_off: NULL, or nreads + 1 ascending LOCAL base offsets, read_off[0] = 0,
+ *   read_off[nreads] = n; windows never span two reads (C4 segmented windows).
+ * pos_base: added to every emitted position (global offset of seq[0]).
+ * [win_lo, win_hi): LOCAL window range whose first-selections are emitted (a shard
+ *   owning global windows [a,b) passes bases [a-1, b+k+w-2) with win_lo = 1 when a > 0,
+ *   R25); win_hi = UINT64_MAX means "all".
+ * out: hash[capacity], pos[capacity] (uint64 each; hash = key), d_count (1 uint64,
+ *   device) receives the total number of records even if it exceeds capacity; only the
+ *   first min(count, capacity) records are written, in order.
+ * Supported: k in [1, 31], w >= 1, 2k >= 1.  Records per window <= 1, so capacity =
+ *   number of windows always suffices.
+ */
+enum { MZ_IN_ASCII = 0, MZ_IN_PACKED2 = 1 };
+enum { MZ_KEY_HASH = 0, MZ_KEY_RAW = 1 };
+
+typedef struct mz_in {
+  int kind;                  /* MZ_IN_ASCII or MZ_IN_PACKED2                    */
+  const void* seq;           /* device: bytes or packed words                   */
+  const uint32_t* invalid;   /* device: invalid bitmap for PACKED2, or NULL     */
+  uint64_t n;                /* number of bases                                 */
+  const uint64_t* read_off;  /* device: nreads+1 read starts, or NULL           */
+  uint64_t nreads;
+  uint64_t pos_base;
+  uint64_t win_lo;
+  uint64_t win_hi;
+} mz_in_t;
+
+typedef struct mz_out {
+  uint64_t* hash;            /* device, capacity entries */
+  uint64_t* pos;             /* device, capacity entries */
+  uint64_t capacity;
+  uint64_t* d_count;         /* device, 1 entry          */
+} mz_out_t;
+
+/* scratch for mz_extract_ex on n bases (tile descriptors + packed copy for ASCII) */
+size_t mz_workspace_bytes(uint64_t n, int k, int w, int kind);
+/* asynchronous extraction on `stream`. */
+int mz_extract_ex(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out,
+                  void* ws, size_t ws_bytes, void* stream);
+/* BASELINE shape: ASCII input, hashed keys, one segment, pos_base 0, default stream.
+ * Synchronous; returns SLSUM_ECAPACITY if the count exceeds out->capacity
+ * (*out->d_count then holds the required count). */
+int mz_extract(const uint8_t* seq, uint64_t n, int k, int w, mz_out_t* out);
+
+/* ------------------------------------------------------------------ seed table
+ * Fig. 1 (L63-65): a pointer table over seeds + a position table.  Seeds are bucketed
+ * on the top `bucket_bits` bits of the 2k-bit key (R21):
+ *   fp(key)     = key >> (2k-32) if 2k >= 32, else key << (32-2k)   (top-aligned 32 bits)
+ *   bucket(key) = fp(key) >> (32 - bucket_bits)
+ * offsets[2^bucket_bits + 1] (uint64): offsets[b] = number of records with bucket < b.
+ * pos_out[m] (uint64): positions grouped by bucket, ascending position inside a bucket.
+ * fp_out[m] (uint32, may be NULL): the fingerprints in the same order.
+ * m: number of records; if d_m != NULL the count is read on the device from *d_m and m is
+ *   only its upper bound (lets the table follow mz_extract_ex without a host sync).
+ * Requires 1 <= bucket_bits <= min(2k, 30).
+ */
+size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits);
+int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
+                    int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* Multi-GPU phases (owner(bucket) = bucket >> (bucket_bits - log2 nranks); nranks a
+ * power of two; NCCL all_reduce / all_to_all run between these calls):
+ *  seedtable_count      counts[2^bits] (uint32) = per-bucket record counts (overwritten).
+ *  seedtable_partition  stable partition of the records by owner rank: send_fp/send_pos
+ *                       (m entries) grouped by owner, ascending position inside a group;
+ *                       send_counts[nranks] (uint64, device) entries per owner.
+ *  seedtable_finalize   from the received entries (concatenated in sender-rank order) and
+ *                       the all-reduced counts, build this rank's slice of the table:
+ *                       offsets_local[2^bits/nranks + 1] starting at 0, pos_out/fp_out
+ *                       (m_recv entries).  Concatenating the ranks' slices (offsets
+ *                       shifted by the preceding ranks' totals) gives seedtable_build's
+ *                       output on the union of the records.
+ */
+int seedtable_count(const uint64_t* hash, uint64_t m, const uint64_t* d_m, int k, int bucket_bits,
+                    uint32_t* counts, void* stream);
+size_t seedtable_partition_workspace_bytes(uint64_t m, int nranks);
+int seedtable_partition(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
+                        int k, int bucket_bits, int nranks, uint32_t* send_fp, uint64_t* send_pos,
+                        uint64_t* send_counts, void* ws, size_t ws_bytes, void* stream);
+size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bits, int nranks);
+int seedtable_finalize(const uint32_t* recv_fp, const uint64_t* recv_pos, uint64_t m_recv,
+                       const uint32_t* global_counts, int bucket_bits, int rank, int nranks,
+                       uint64_t* offsets_local, uint64_t* pos_out, uint32_t* fp_out,
+                       void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MZSLSUM_H */

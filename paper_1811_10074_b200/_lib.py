@@ -1,0 +1,252 @@
+"""ctypes binding of libmzslsum.so (include/mzslsum.h).  Argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; this module only turns torch
+tensors into device pointers and the current CUDA stream into a cudaStream_t.  There is
+no CPU fallback: if the shared library is missing, importing the module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmzslsum.so")
+
+# ---------------------------------------------------------------- constants (mzslsum.h)
+SLSUM_OK, SLSUM_EINVAL, SLSUM_EUNSUPPORTED, SLSUM_ECAPACITY, SLSUM_ECUDA, SLSUM_ENOMEM = 0, -1, -2, -3, -4, -5
+SLSUM_MIN_U32, SLSUM_MAX_U32, SLSUM_ADD_U32, SLSUM_ADD_F32, SLSUM_AFFINE_U32X2, SLSUM_MIN_U64 = range(6)
+SLSUM_PATH_GENERIC, SLSUM_PATH_COMMUTATIVE, SLSUM_PATH_AUTO = range(3)
+MZ_IN_ASCII, MZ_IN_PACKED2 = 0, 1
+MZ_KEY_HASH, MZ_KEY_RAW = 0, 1
+U64_MAX = 2 ** 64 - 1
+
+OP_DTYPE = {SLSUM_MIN_U32: torch.uint32, SLSUM_MAX_U32: torch.uint32, SLSUM_ADD_U32: torch.uint32,
+            SLSUM_ADD_F32: torch.float32, SLSUM_AFFINE_U32X2: torch.uint32, SLSUM_MIN_U64: torch.uint64}
+
+
+class SlsumError(RuntimeError):
+    def __init__(self, rc: int, what: str):
+        self.rc = rc
+        super().__init__(f"{what}: {strerror(rc)} ({rc})")
+
+
+class MzIn(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("seq", ctypes.c_void_p), ("invalid", ctypes.c_void_p),
+                ("n", ctypes.c_uint64), ("read_off", ctypes.c_void_p), ("nreads", ctypes.c_uint64),
+                ("pos_base", ctypes.c_uint64), ("win_lo", ctypes.c_uint64), ("win_hi", ctypes.c_uint64)]
+
+
+class MzOut(ctypes.Structure):
+    _fields_ = [("hash", ctypes.c_void_p), ("pos", ctypes.c_void_p), ("capacity", ctypes.c_uint64),
+                ("d_count", ctypes.c_void_p)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1811_10074_b200/build.py` "
+                      "(there is no CPU fallback)")
+
+_L = ctypes.CDLL(LIB_PATH)
+_u64, _i32, _u32, _vp, _sz = ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
+
+
+def _sig(name, res, *args):
+    f = getattr(_L, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_strerror = _sig("slsum_strerror", ctypes.c_char_p, _i32)
+_version = _sig("slsum_version", _i32)
+_slsum_run = _sig("slsum_run", _i32, _i32, _u32, _vp, _vp, _u64)
+_slsum_run_ex = _sig("slsum_run_ex", _i32, _i32, _u32, _vp, _vp, _u64, _i32, _vp)
+_mz_encode = _sig("mz_encode", _i32, _vp, _u64, _vp, _vp, _vp)
+_mz_ws = _sig("mz_workspace_bytes", _sz, _u64, _i32, _i32, _i32)
+_mz_extract_ex = _sig("mz_extract_ex", _i32, ctypes.POINTER(MzIn), _i32, _i32, _i32, ctypes.POINTER(MzOut), _vp, _sz, _vp)
+_mz_extract_path = _sig("mz_extract_path", _i32, ctypes.POINTER(MzIn), _i32, _i32, _i32, ctypes.POINTER(MzOut), _vp,
+                        _sz, _vp, _i32)
+_mz_extract = _sig("mz_extract", _i32, _vp, _u64, _i32, _i32, ctypes.POINTER(MzOut))
+_st_ws = _sig("seedtable_workspace_bytes", _sz, _u64, _i32)
+_st_build = _sig("seedtable_build", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+_st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
+_st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
+_st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+_st_fin_ws = _sig("seedtable_finalize_workspace_bytes", _sz, _u64, _i32, _i32)
+_st_fin = _sig("seedtable_finalize", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+
+EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_encode", "mz_workspace_bytes",
+           "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_count",
+           "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
+           "seedtable_finalize"]
+
+
+def strerror(rc: int) -> str:
+    return _strerror(rc).decode()
+
+
+def version() -> int:
+    return _version()
+
+
+def _check(rc: int, what: str) -> int:
+    if rc != SLSUM_OK:
+        raise SlsumError(rc, what)
+    return rc
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensor required (the library takes device pointers)")
+    if not t.is_contiguous():
+        raise ValueError("contiguous tensor required")
+    return t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(1, int(nbytes)), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------- sliding sums (Eq. 2)
+def slsum_run(op: int, w: int, x: torch.Tensor, y: torch.Tensor | None = None, path: int = SLSUM_PATH_GENERIC,
+              stream=None) -> torch.Tensor:
+    """y_i = x_i (+) ... (+) x_{i+w-1} on the device.  AFFINE_U32X2 takes x of shape (n, 2)."""
+    n = x.shape[0]
+    nout = max(0, n - w + 1)
+    if y is None:
+        y = torch.empty((nout,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    _check(_slsum_run_ex(op, w, _ptr(x), _ptr(y), n, path, _stream(stream)), "slsum_run_ex")
+    return y
+
+
+# ---------------------------------------------------------------- 2-bit packing
+def mz_encode(seq: torch.Tensor, words: torch.Tensor | None = None, invalid: torch.Tensor | None = None,
+              stream=None):
+    n = seq.numel()
+    nw = (n + 31) // 32
+    if words is None:
+        words = torch.empty(nw, dtype=torch.uint64, device=seq.device)
+    if invalid is None:
+        invalid = torch.empty(nw, dtype=torch.uint32, device=seq.device)
+    _check(_mz_encode(_ptr(seq), n, _ptr(words), _ptr(invalid), _stream(stream)), "mz_encode")
+    return words, invalid
+
+
+# ---------------------------------------------------------------- minimizers
+def mz_workspace_bytes(n: int, k: int, w: int, kind: int = MZ_IN_ASCII) -> int:
+    return int(_mz_ws(n, k, w, kind))
+
+
+def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, kind: int = MZ_IN_ASCII,
+                  invalid: torch.Tensor | None = None, read_off: torch.Tensor | None = None, pos_base: int = 0,
+                  win_lo: int = 0, win_hi: int = U64_MAX, keymode: int = MZ_KEY_HASH,
+                  capacity: int | None = None, out_hash: torch.Tensor | None = None,
+                  out_pos: torch.Tensor | None = None, d_count: torch.Tensor | None = None,
+                  ws: torch.Tensor | None = None, stream=None, path: int = 0):
+    """Asynchronous minimizer extraction; returns (hash, pos, d_count) device tensors (count on device)."""
+    if n is None:
+        n = seq.numel() if kind == MZ_IN_ASCII else seq.numel() * 32
+    span = k + w - 1
+    nwin = max(0, n - span + 1)
+    if capacity is None:
+        capacity = out_hash.numel() if out_hash is not None else nwin
+    dev = seq.device
+    if out_hash is None:
+        out_hash = torch.empty(max(1, capacity), dtype=torch.uint64, device=dev)
+    if out_pos is None:
+        out_pos = torch.empty(max(1, capacity), dtype=torch.uint64, device=dev)
+    if d_count is None:
+        d_count = torch.zeros(1, dtype=torch.uint64, device=dev)
+    if ws is None:
+        ws = _ws(mz_workspace_bytes(n, k, w, kind), dev)
+    nreads = 0 if read_off is None else read_off.numel() - 1
+    mi = MzIn(kind, _ptr(seq), _ptr(invalid), n, _ptr(read_off), nreads, pos_base, win_lo, win_hi)
+    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count))
+    _check(_mz_extract_path(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
+                            _stream(stream), path), "mz_extract_ex")
+    return out_hash, out_pos, d_count
+
+
+def mz_extract(seq: torch.Tensor, k: int, w: int, **kw):
+    """Synchronous convenience: returns (hash, pos) trimmed to the record count."""
+    h, p, c = mz_extract_ex(seq, k, w, **kw)
+    cnt = int(c.item())
+    cap = kw.get("capacity", h.numel())
+    if cnt > h.numel():
+        raise SlsumError(SLSUM_ECAPACITY, f"mz_extract: {cnt} records > capacity {cap}")
+    return h[:cnt], p[:cnt]
+
+
+# ---------------------------------------------------------------- seed table (Fig. 1)
+def seedtable_workspace_bytes(m: int, bits: int) -> int:
+    return int(_st_ws(m, bits))
+
+
+def seedtable_build(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *, m: int | None = None,
+                    d_m: torch.Tensor | None = None, with_fp: bool = True, offsets: torch.Tensor | None = None,
+                    pos_out: torch.Tensor | None = None, fp_out: torch.Tensor | None = None,
+                    ws: torch.Tensor | None = None, stream=None):
+    """Returns (offsets[2^bits+1], pos_out[m], fp_out[m] or None)."""
+    if m is None:
+        m = hash_.numel()
+    dev = hash_.device
+    if offsets is None:
+        offsets = torch.empty((1 << bits) + 1, dtype=torch.uint64, device=dev)
+    if pos_out is None:
+        pos_out = torch.empty(max(1, m), dtype=torch.uint64, device=dev)
+    if fp_out is None and with_fp:
+        fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    if ws is None:
+        ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _check(_st_build(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out), _ptr(pos_out),
+                     _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build")
+    return offsets, pos_out, fp_out
+
+
+def seedtable_count(hash_: torch.Tensor, k: int, bits: int, *, m: int | None = None, d_m=None, counts=None,
+                    stream=None) -> torch.Tensor:
+    if m is None:
+        m = hash_.numel()
+    if counts is None:
+        counts = torch.empty(1 << bits, dtype=torch.uint32, device=hash_.device)
+    _check(_st_count(_ptr(hash_), m, _ptr(d_m), k, bits, _ptr(counts), _stream(stream)), "seedtable_count")
+    return counts
+
+
+def seedtable_partition(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, nranks: int, *,
+                        m: int | None = None, d_m=None, ws=None, stream=None):
+    """Returns (send_fp[m], send_pos[m], send_counts[nranks]) grouped by owner rank."""
+    if m is None:
+        m = hash_.numel()
+    dev = hash_.device
+    send_fp = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    send_pos = torch.empty(max(1, m), dtype=torch.uint64, device=dev)
+    send_counts = torch.empty(nranks, dtype=torch.uint64, device=dev)
+    if ws is None:
+        ws = _ws(_st_part_ws(max(1, m), nranks), dev)
+    _check(_st_part(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, nranks, _ptr(send_fp), _ptr(send_pos),
+                    _ptr(send_counts), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_partition")
+    return send_fp, send_pos, send_counts
+
+
+def seedtable_finalize(recv_fp: torch.Tensor, recv_pos: torch.Tensor, m_recv: int, global_counts, bits: int,
+                       rank: int, nranks: int, *, with_fp: bool = True, ws=None, stream=None):
+    """Returns (offsets_local[2^bits/nranks + 1], pos_out[m_recv], fp_out or None)."""
+    dev = recv_pos.device
+    nbl = (1 << bits) // nranks
+    offsets = torch.empty(nbl + 1, dtype=torch.uint64, device=dev)
+    pos_out = torch.empty(max(1, m_recv), dtype=torch.uint64, device=dev)
+    fp_out = torch.empty(max(1, m_recv), dtype=torch.uint32, device=dev) if with_fp else None
+    if ws is None:
+        ws = _ws(_st_fin_ws(max(1, m_recv), bits, nranks), dev)
+    _check(_st_fin(_ptr(recv_fp), _ptr(recv_pos), m_recv, _ptr(global_counts), bits, rank, nranks, _ptr(offsets),
+                   _ptr(pos_out), _ptr(fp_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_finalize")
+    return offsets, pos_out, fp_out

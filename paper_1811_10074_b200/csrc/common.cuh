@@ -1,0 +1,160 @@
+// common.cuh -- shared device/host helpers of libmzslsum (sm_100a).
+//
+// Nothing in here is part of the oracle (oracle/ shares no code with csrc/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/mzslsum.h"
+
+#define MZS_API extern "C" __attribute__((visibility("default")))
+
+namespace mzs {
+
+// ---------------------------------------------------------------- host helpers
+void set_cuda_error(cudaError_t e);
+
+#define MZS_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) {                             \
+      ::mzs::set_cuda_error(e_);                         \
+      return SLSUM_ECUDA;                                \
+    }                                                    \
+  } while (0)
+
+#define MZS_LAUNCHED() MZS_CUDA(cudaPeekAtLastError())
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x, size_t a = kAlign) { return (x + a - 1) / a * a; }
+
+// Carves typed sub-buffers out of a caller-provided workspace.
+struct Carve {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  bool ok = true;
+  Carve(void* p, size_t c) : base(static_cast<char*>(p)), cap(c) {}
+  template <class T>
+  T* take(size_t n) {
+    size_t bytes = align_up(n * sizeof(T));
+    if (used + bytes > cap) { ok = false; return nullptr; }
+    T* r = reinterpret_cast<T*>(base + used);
+    used += bytes;
+    return r;
+  }
+};
+
+// Sizes a workspace the same way Carve consumes it.
+struct Sizer {
+  size_t used = 0;
+  template <class T>
+  void take(size_t n) { used += align_up(n * sizeof(T)); }
+};
+
+// Owns a temporary workspace when the caller passed ws == NULL.
+struct TempWs {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~TempWs() { if (p) cudaFreeAsync(p, s); }
+};
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+  return *reinterpret_cast<const volatile uint64_t*>(p);
+}
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+  *reinterpret_cast<volatile uint64_t*>(p) = v;
+}
+
+// Decoupled look-back tile status words: (flag << 62) | value.
+constexpr uint64_t kLbAgg = 1ull << 62;      // tile aggregate published
+constexpr uint64_t kLbInc = 2ull << 62;      // inclusive prefix published
+constexpr uint64_t kLbVal = (1ull << 62) - 1;
+
+// Called by ALL 32 lanes of ONE warp.  Publishes `agg` for tile `tile`, walks back over
+// predecessors 32 at a time and returns the exclusive prefix (sum of all earlier tiles'
+// aggregates).  Tiles must be numbered in launch order (dynamic tile ids), so every
+// predecessor is resident or finished: no deadlock.
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_t tile, uint64_t agg) {
+  const unsigned lane = lane_id();
+  if (tile == 0) {
+    if (lane == 0) st_volatile_u64(&status[0], kLbInc | agg);
+    return 0;
+  }
+  if (lane == 0) st_volatile_u64(&status[tile], kLbAgg | agg);
+  uint64_t excl = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (true) {
+    int64_t idx = base - (int64_t)lane;
+    uint64_t v = idx >= 0 ? ld_volatile_u64(&status[idx]) : (kLbInc | 0);
+    while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+      if ((v >> 62) == 0) v = ld_volatile_u64(&status[idx]);
+    }
+    unsigned inc_mask = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    uint64_t val = v & kLbVal;
+    if (inc_mask) {
+      int first = __ffs(inc_mask) - 1;  // closest predecessor with an inclusive prefix
+      uint64_t part = lane <= (unsigned)first ? val : 0;
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      excl += part;
+      break;
+    }
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    excl += val;
+    base -= 32;
+  }
+  if (lane == 0) st_volatile_u64(&status[tile], kLbInc | (excl + agg));
+  return excl;
+}
+
+// Block-wide exclusive sum of one value per thread (TPB threads, multiple of 32).
+// `warp_sums` must hold TPB/32 entries of shared memory.  Returns the exclusive prefix
+// of this thread; *total receives the block total (valid in every thread).
+template <int TPB, class T>
+__device__ __forceinline__ T block_exclusive_sum(T v, T* warp_sums, T* total) {
+  constexpr int NW = TPB / 32;
+  const unsigned lane = lane_id(), wid = warp_id();
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= (unsigned)o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T s = lane < (unsigned)NW ? warp_sums[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= (unsigned)o) s += y;
+    }
+    if (lane < (unsigned)NW) warp_sums[lane] = s;  // inclusive warp prefix
+  }
+  __syncthreads();
+  T wpre = wid ? warp_sums[wid - 1] : T(0);
+  *total = warp_sums[NW - 1];
+  __syncthreads();
+  return wpre + x - v;
+}
+
+}  // namespace mzs

@@ -1,0 +1,615 @@
+// mz.cu -- minimizer extraction (Sec. 2.4, Fig. 2) on B200.
+//
+// One fused kernel per tile of TW consecutive windows (a window = w consecutive k-mers):
+//   phase 1  rolling 2-bit k-mer codes from the packed words (L67: k-mers are a sliding
+//            sum under string concatenation, realised as a shift register) and the
+//            invertible hash H_2k (R5) -> packed keys (hash << 14 | slot) in
+//            shared memory; hashes never round-trip HBM.
+//   phase 2  the sliding window minimum with the paper's decomposition (Alg. 2):
+//            blocks of w keys, suffix minima S (Y1) and prefix minima P (X1), window
+//            argmin = S[i] (+) P[i+w-1]; keys compare as (hash, position) so the minimum
+//            is the leftmost one (R2).  A window emits its argmin iff it is valid and its
+//            predecessor is invalid or had a different argmin (change rule, R3); emitted
+//            slots are marked in a shared bitmask.
+//   phase 3  ordered compaction: popcounts -> block scan -> decoupled look-back over
+//            tiles (single pass, deterministic) -> (hash, pos) records.
+// Fast path: w in [1,16] as a compile-time block length (S/P in registers), k <= 25.
+// Generic path: any w <= 1024 and any k <= 31, S/P by block-wide segmented scans.
+#include "ops.cuh"
+
+namespace mzs {
+namespace {
+
+constexpr int kSlotBits = 14;  // slot index inside a tile (< 16384)
+constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1;
+
+// H_b (R5): the masked Wang/minimap2 integer mix, all arithmetic mod 2^b.
+__device__ __forceinline__ uint32_t hash_b32(uint32_t x, uint32_t m) {
+  x = (x * 0x1FFFFFu - 1u) & m;  // (2^21-1) x - 1
+  x ^= x >> 24;
+  x = (x * 265u) & m;
+  x ^= x >> 14;
+  x = (x * 21u) & m;
+  x ^= x >> 28;
+  x = (x * 0x80000001u) & m;     // (2^31+1) x
+  return x;
+}
+__device__ __forceinline__ uint64_t hash_b64(uint64_t x, uint64_t m) {
+  x = (x * 0x1FFFFFull - 1ull) & m;
+  x ^= x >> 24;
+  x = (x * 265ull) & m;
+  x ^= x >> 14;
+  x = (x * 21ull) & m;
+  x ^= x >> 28;
+  x = (x * 0x80000001ull) & m;
+  return x;
+}
+
+struct MzArgs {
+  const uint64_t* words;     // packed bases (MSB-first, 32 per word)
+  const uint32_t* invalid;   // invalid bitmap or nullptr
+  uint64_t nwords;
+  uint64_t n;                // bases
+  uint64_t nwin;             // windows = n - (k+w-1) + 1
+  const uint64_t* read_off;  // nreads+1 or nullptr
+  uint64_t nreads;
+  uint64_t pos_base, win_lo, win_hi;
+  int k, w, raw;
+  uint64_t* out_hash;
+  uint64_t* out_pos;
+  uint64_t capacity;
+  uint64_t* d_count;
+  uint64_t* status;          // look-back tile status [ntiles]
+  uint32_t* tile_counter;
+  uint64_t ntiles;
+  uint32_t tw;               // windows per tile
+};
+
+__device__ __forceinline__ uint64_t ldw(const MzArgs& a, int64_t i) {
+  return (i >= 0 && (uint64_t)i < a.nwords) ? __ldg(a.words + i) : 0ull;
+}
+__device__ __forceinline__ uint32_t ldi(const MzArgs& a, int64_t i) {
+  return (a.invalid && i >= 0 && (uint64_t)i < a.nwords) ? __ldg(a.invalid + i) : 0u;
+}
+// bits for bases [lo, lo+64): bit j <-> base lo+j is invalid
+__device__ __forceinline__ uint64_t inv_window64(const MzArgs& a, int64_t lo) {
+  const int64_t wi = lo >> 5;
+  const uint32_t sh = (uint32_t)(lo & 31);
+  const uint64_t ab = (uint64_t)ldi(a, wi) | ((uint64_t)ldi(a, wi + 1) << 32);
+  const uint64_t c = ldi(a, wi + 2);
+  return sh ? (ab >> sh) | (c << (64 - sh)) : ab;
+}
+// first index r in [0, nreads] with read_off[r] > x  (read_off[nreads] = n)
+__device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
+  uint64_t lo = 0, hi = a.nreads + 1;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) >> 1;
+    if ((int64_t)__ldg(a.read_off + mid) > x) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------ phase 1
+// Keys of k-mers q0 .. q0+Q-1 into slots s0 .. s0+Q-1.  If CHECK, wv[slot] = 1 iff the
+// window whose LAST k-mer is that slot's k-mer is valid (run of valid same-read bases
+// ending at the k-mer's last base >= k + w - 1).
+template <class Key, int Q, bool H64, bool CHECK>
+__device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint8_t* wv) {
+  const int k = a.k;
+  const int64_t wi = q0 >> 5;
+  const uint32_t off = (uint32_t)(q0 & 31) * 2;
+  const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1), C = ldw(a, wi + 2);
+  const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
+  const uint64_t Y = off ? (B << off) | (C >> (64 - off)) : B;
+  // stream of the bases entering after the first k-mer: q0+k, q0+k+1, ...
+  uint64_t Z = (X << (2 * k)) | (Y >> (64 - 2 * k));
+  uint32_t run = 0;
+  uint64_t iv = 0;
+  int64_t next_rs = INT64_MAX;
+  uint64_t ri = 0;
+  const int span = k + a.w - 1;
+  if (CHECK) {
+    // run length at base x0 = q0 + k - 2 (capped at span), then walk base by base
+    const int64_t x0 = q0 + k - 2;
+    const uint64_t bits = inv_window64(a, x0 - span + 1) & ((span >= 64) ? ~0ull : ((1ull << span) - 1));
+    int64_t start = bits ? (x0 - span + 1) + (63 - __clzll(bits)) + 1 : x0 - span + 1;
+    if (a.read_off) {
+      ri = upper_read(a, x0);                 // first read start > x0
+      const int64_t rs = ri ? (int64_t)__ldg(a.read_off + ri - 1) : 0;
+      if (rs > start) start = rs;
+      next_rs = ri <= a.nreads ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
+    }
+    run = (uint32_t)max((int64_t)0, x0 - start + 1);
+    iv = inv_window64(a, x0 + 1);  // bit s <-> base x0+1+s = last base of k-mer q0+s
+  }
+  const int kk = 2 * k;
+  if (H64) {
+    const uint64_t km = (kk == 64) ? ~0ull : ((1ull << kk) - 1);
+    uint64_t code = X >> (64 - kk);
+#pragma unroll
+    for (int s = 0; s < Q; ++s) {
+      if (s > 0) {
+        code = ((code << 2) | (Z >> 62)) & km;
+        Z <<= 2;
+      }
+      if (CHECK) {
+        const int64_t x = q0 + s + k - 1;
+        const uint32_t inv = (uint32_t)(iv >> s) & 1u;
+        if (x == next_rs) {
+          run = 0;
+          next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
+          while (next_rs <= x) next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
+        }
+        run = inv ? 0u : run + 1u;
+        wv[s0 + s] = run >= (uint32_t)span;
+      }
+      const uint64_t h = a.raw ? code : hash_b64(code, km);
+      keys[s0 + s] = Key::make(h, s0 + s);
+    }
+  } else {
+    const uint32_t km = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
+    uint32_t code = (uint32_t)(X >> (64 - kk));
+#pragma unroll
+    for (int s = 0; s < Q; ++s) {
+      if (s > 0) {
+        code = ((code << 2) | (uint32_t)(Z >> 62)) & km;
+        Z <<= 2;
+      }
+      if (CHECK) {
+        const int64_t x = q0 + s + k - 1;
+        const uint32_t inv = (uint32_t)(iv >> s) & 1u;
+        if (x == next_rs) {
+          run = 0;
+          next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
+          while (next_rs <= x) next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
+        }
+        run = inv ? 0u : run + 1u;
+        wv[s0 + s] = run >= (uint32_t)span;
+      }
+      const uint32_t h = a.raw ? code : hash_b32(code, km);
+      keys[s0 + s] = Key::make(h, s0 + s);
+    }
+  }
+}
+
+// Packed key: (hash << 14) | slot -- lexicographic (hash, position) order in one u64.
+struct PackedKey {
+  unsigned long long v;
+  __device__ __forceinline__ static PackedKey make(uint64_t h, uint32_t slot) {
+    return PackedKey{(h << kSlotBits) | slot};
+  }
+  __device__ __forceinline__ uint32_t slot() const { return (uint32_t)(v & kSlotMask); }
+  __device__ __forceinline__ uint64_t hash() const { return v >> kSlotBits; }
+  __device__ __forceinline__ bool operator!=(const PackedKey& o) const { return v != o.v; }
+};
+__device__ __forceinline__ PackedKey kmin(PackedKey a, PackedKey b) { return a.v <= b.v ? a : b; }
+
+// Wide key for 2k > 50: hash and slot kept apart (ties broken by the slot).
+struct WideKey {
+  unsigned long long h;
+  uint32_t s;
+  uint32_t pad;
+  __device__ __forceinline__ static WideKey make(uint64_t h, uint32_t slot) { return WideKey{h, slot, 0}; }
+  __device__ __forceinline__ uint32_t slot() const { return s; }
+  __device__ __forceinline__ uint64_t hash() const { return h; }
+  __device__ __forceinline__ bool operator!=(const WideKey& o) const { return h != o.h || s != o.s; }
+};
+__device__ __forceinline__ WideKey kmin(WideKey a, WideKey b) {
+  return (a.h < b.h || (a.h == b.h && a.s <= b.s)) ? a : b;
+}
+
+template <class Key>
+struct OpKeyMin {
+  using T = Key;
+  static constexpr bool kCommutative = true, kIdempotent = true;
+  __device__ __forceinline__ static T id() { return T::make(~0ull >> kSlotBits, (uint32_t)kSlotMask); }
+  __device__ __forceinline__ static T op(T a, T b) { return kmin(a, b); }
+};
+template <>
+__device__ __forceinline__ WideKey OpKeyMin<WideKey>::id() { return WideKey{~0ull, 0xffffffffu, 0}; }
+
+// shuffles of the key types (used by the generic path's segmented scans)
+__device__ __forceinline__ PackedKey shfl_up(PackedKey v, int o) { return PackedKey{__shfl_up_sync(0xffffffffu, v.v, o)}; }
+__device__ __forceinline__ PackedKey shfl_down(PackedKey v, int o) { return PackedKey{__shfl_down_sync(0xffffffffu, v.v, o)}; }
+__device__ __forceinline__ WideKey shfl_up(WideKey v, int o) {
+  return WideKey{__shfl_up_sync(0xffffffffu, v.h, o), __shfl_up_sync(0xffffffffu, v.s, o), 0};
+}
+__device__ __forceinline__ WideKey shfl_down(WideKey v, int o) {
+  return WideKey{__shfl_down_sync(0xffffffffu, v.h, o), __shfl_down_sync(0xffffffffu, v.s, o), 0};
+}
+
+}  // namespace
+// make the key shuffles visible to the segmented-scan templates in ops.cuh (ADL)
+}  // namespace mzs
+
+namespace mzs {
+namespace {
+
+// Tile cleanliness: no invalid base and no read start strictly inside the tile's bases.
+template <int TPB>
+__device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int64_t b_hi) {
+  int dirty = 0;
+  if (a.invalid) {
+    const int64_t w0 = max((int64_t)0, b_lo >> 5), w1 = min((int64_t)a.nwords - 1, (b_hi - 1) >> 5);
+    for (int64_t wi = w0 + threadIdx.x; wi <= w1; wi += TPB) {
+      uint32_t m = __ldg(a.invalid + wi);
+      // restrict to [b_lo, b_hi)
+      const int64_t base = wi << 5;
+      if (base < b_lo) m &= 0xffffffffu << (uint32_t)(b_lo - base);
+      if (base + 32 > b_hi) m &= (b_hi - base >= 32) ? 0xffffffffu : ((1u << (uint32_t)(b_hi - base)) - 1u);
+      dirty |= (m != 0);
+    }
+  }
+  if (a.read_off && threadIdx.x == 0) {
+    const uint64_t r = upper_read(a, b_lo);  // first read start > b_lo
+    if (r <= a.nreads && (int64_t)__ldg(a.read_off + r) < b_hi) dirty = 1;
+  }
+  return !__syncthreads_or(dirty);
+}
+
+// Phase 3: ordered output of the emitted slots of this tile.
+template <int TPB, class Key>
+__device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, int64_t tile_lo, const Key* keys,
+                                              const uint32_t* emit, uint32_t nsw, uint64_t* warp_sums,
+                                              uint64_t* bcast) {
+  const uint32_t wpt = (nsw + TPB - 1) / TPB;
+  const uint32_t u0 = threadIdx.x * wpt;
+  uint64_t cnt = 0;
+  for (uint32_t u = u0; u < u0 + wpt && u < nsw; ++u) cnt += __popc(emit[u]);
+  uint64_t total;
+  const uint64_t excl = block_exclusive_sum<TPB, uint64_t>(cnt, warp_sums, &total);
+  if (warp_id() == 0) {
+    const uint64_t off = lookback_exclusive(a.status, tile, total);
+    if (lane_id() == 0) {
+      *bcast = off;
+      if (tile == a.ntiles - 1) *a.d_count = off + total;
+    }
+  }
+  __syncthreads();
+  uint64_t o = *bcast + excl;
+  for (uint32_t u = u0; u < u0 + wpt && u < nsw; ++u) {
+    uint32_t bits = emit[u];
+    while (bits) {
+      const uint32_t b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const uint32_t slot = u * 32 + b;
+      if (o < a.capacity) {
+        a.out_hash[o] = keys[slot].hash();
+        a.out_pos[o] = a.pos_base + (uint64_t)(tile_lo - 1 + (int64_t)slot);
+      }
+      ++o;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ fast path kernel
+template <int W>
+struct FastGeom {
+  static constexpr int TPB = 256;
+  static constexpr int M0 = (32 / W) > 0 ? (32 / W) : 1;
+  // R = M*W even so that Q = R + 1 is odd (conflict-free strided key stores), Q <= 33
+  static constexpr int M = ((M0 * W) % 2 == 0) ? M0 : (M0 > 1 ? M0 - 1 : 2);
+  static constexpr int R = M * W;
+  static constexpr int Q = R + 1;
+  static constexpr int TW = TPB * R;
+  static constexpr int NS = TPB * Q;
+  static constexpr int NSW = NS / 32;
+  static_assert(Q <= 33, "phase-1 rolling window holds 32 bases");
+  static_assert(NS < (1 << kSlotBits), "slot bits");
+  static_assert(TPB >= W + 1, "halo slots");
+};
+
+template <int W, bool H64, bool CHECK>
+__device__ __forceinline__ void fast_tile(const MzArgs& a, uint64_t tile, int64_t tile_lo, PackedKey* keys,
+                                          uint8_t* wv, uint32_t* emit) {
+  using G = FastGeom<W>;
+  const int t = threadIdx.x;
+  // ---- phase 1: slots t*Q .. t*Q+Q-1 <-> k-mers tile_lo-1+t*Q ...
+  phase1_keys<PackedKey, G::Q, H64, CHECK>(a, tile_lo - 1 + (int64_t)t * G::Q, (uint32_t)(t * G::Q), keys, wv);
+  __syncthreads();
+  // ---- phase 2: windows j = t*R .. t*R+R-1 (tile-relative); window j = slots j+1 .. j+W
+  const int jb = t * G::R;
+  const int64_t i_base = tile_lo + jb;  // sequence-local window index of j = jb
+  PackedKey S[W], kb[W];
+  PackedKey yprev;
+  bool vprev;
+  auto valid_of = [&](int j) -> bool {
+    const int64_t i = tile_lo + j;
+    if (i < 0 || (uint64_t)i >= a.nwin) return false;
+    return CHECK ? (wv[j + W] != 0) : true;
+  };
+  auto visit = [&](int j, PackedKey y) {
+    const bool v = valid_of(j);
+    const int64_t i = tile_lo + j;
+    if (v && (!vprev || y != yprev) && (uint64_t)i >= a.win_lo && (uint64_t)i < a.win_hi) {
+      const uint32_t s = y.slot();
+      atomicOr(&emit[s >> 5], 1u << (s & 31));
+    }
+    vprev = v;
+    yprev = y;
+  };
+  // block 0 keys and the window before the strip (j = jb - 1 = slots jb .. jb+W-1)
+  {
+    const PackedKey k0 = keys[jb];
+#pragma unroll
+    for (int q = 0; q < W; ++q) kb[q] = keys[jb + 1 + q];
+    PackedKey p = kb[0];
+#pragma unroll
+    for (int q = 1; q < W - 1; ++q) p = kmin(p, kb[q]);
+    yprev = (W == 1) ? k0 : kmin(k0, p);
+    vprev = valid_of(jb - 1);
+    S[W - 1] = kb[W - 1];
+#pragma unroll
+    for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
+  }
+  (void)i_base;
+#pragma unroll 1
+  for (int b = 1; b <= G::M; ++b) {
+    const int jblk = jb + (b - 1) * W;  // first window of block b-1
+    visit(jblk, S[0]);
+    const int sb = jb + 1 + b * W;      // first slot of block b
+#pragma unroll
+    for (int q = 0; q < W; ++q) kb[q] = keys[sb + q];
+    PackedKey p = kb[0];
+#pragma unroll
+    for (int q = 0; q < W - 1; ++q) {
+      if (q > 0) p = kmin(p, kb[q]);
+      visit(jblk + q + 1, kmin(S[q + 1], p));
+    }
+    S[W - 1] = kb[W - 1];
+#pragma unroll
+    for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
+  }
+}
+
+template <int W, bool H64>
+__global__ void __launch_bounds__(256) mz_fast_kernel(MzArgs a) {
+  using G = FastGeom<W>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PackedKey* keys = reinterpret_cast<PackedKey*>(smem_raw);
+  __shared__ uint32_t emit[G::NSW];
+  __shared__ uint8_t wv[G::NS];
+  __shared__ uint64_t warp_sums[G::TPB / 32];
+  __shared__ uint64_t bcast;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  for (int u = threadIdx.x; u < G::NSW; u += G::TPB) emit[u] = 0;
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const int64_t tile_lo = (int64_t)tile * G::TW;
+  const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + G::NS + a.k;  // bases touched
+  const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi);
+  if (clean) fast_tile<W, H64, false>(a, tile, tile_lo, keys, wv, emit);
+  else fast_tile<W, H64, true>(a, tile, tile_lo, keys, wv, emit);
+  __syncthreads();
+  phase3_output<G::TPB, PackedKey>(a, tile, tile_lo, keys, emit, G::NSW, warp_sums, &bcast);
+}
+
+// ------------------------------------------------------------------ generic path kernel
+constexpr int kGenTPB = 256;
+constexpr int kGenE = 16;                 // slots per thread
+constexpr int kGenNS = kGenTPB * kGenE;   // 4096 slots per tile
+
+template <class Key, bool H64>
+__global__ void __launch_bounds__(kGenTPB) mz_generic_kernel(MzArgs a) {
+  using Op = OpKeyMin<Key>;
+  constexpr int NSW = kGenNS / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Key* keys = reinterpret_cast<Key*>(smem_raw);
+  Key* sP = keys + kGenNS;
+  Key* sS = sP + kGenNS;
+  __shared__ uint32_t emit[NSW];
+  __shared__ uint8_t wv[kGenNS];
+  __shared__ uint64_t warp_sums[kGenTPB / 32];
+  __shared__ uint64_t bcast;
+  __shared__ uint32_t s_tile;
+  __shared__ SegScratch<Op, kGenTPB> sh;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  for (int u = threadIdx.x; u < NSW; u += kGenTPB) emit[u] = 0;
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint32_t W = (uint32_t)a.w;
+  const int64_t tile_lo = (int64_t)tile * a.tw;
+  const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + kGenNS + a.k;
+  const bool clean = tile_is_clean<kGenTPB>(a, b_lo, b_hi);
+  const int t = threadIdx.x;
+  if (clean) phase1_keys<Key, kGenE, H64, false>(a, tile_lo - 1 + (int64_t)t * kGenE, t * kGenE, keys, wv);
+  else phase1_keys<Key, kGenE, H64, true>(a, tile_lo - 1 + (int64_t)t * kGenE, t * kGenE, keys, wv);
+  __syncthreads();
+  // phase 2: block S/P over slots, blocks of W starting at slot 1 (slot s <-> k-mer tile_lo-1+s)
+  {
+    Key v[kGenE], P[kGenE], S[kGenE];
+#pragma unroll
+    for (int j = 0; j < kGenE; ++j) v[j] = keys[t * kGenE + j];
+    block_prefix_suffix<Op, kGenTPB, kGenE>(v, P, S, W, 1u, sh);
+#pragma unroll
+    for (int j = 0; j < kGenE; ++j) {
+      sP[t * kGenE + j] = P[j];
+      sS[t * kGenE + j] = S[j];
+    }
+  }
+  __syncthreads();
+  {
+    // windows j in [0, tw): window j = slots j+1 .. j+W; thread t takes a contiguous range
+    const uint32_t per = (a.tw + kGenTPB - 1) / kGenTPB;
+    const int j0 = t * per;
+    const int j1 = min((int)a.tw, j0 + (int)per);
+    auto wmin = [&](int j) -> Key {
+      // j == -1 (window before the tile) spans slot 0 and the first W-1 slots of block 0
+      if (j < 0) return W == 1 ? keys[0] : kmin(keys[0], sP[W - 1]);
+      return (j % W == 0) ? sS[j + 1] : kmin(sS[j + 1], sP[j + W]);
+    };
+    auto valid_of = [&](int j) -> bool {
+      const int64_t i = tile_lo + j;
+      if (i < 0 || (uint64_t)i >= a.nwin) return false;
+      return clean ? true : (wv[j + W] != 0);
+    };
+    if (j0 < j1) {
+      Key yprev = wmin(j0 - 1);
+      bool vprev = valid_of(j0 - 1);
+      for (int j = j0; j < j1; ++j) {
+        const Key y = wmin(j);
+        const bool v = valid_of(j);
+        const int64_t i = tile_lo + j;
+        if (v && (!vprev || y != yprev) && (uint64_t)i >= a.win_lo && (uint64_t)i < a.win_hi) {
+          const uint32_t s = y.slot();
+          atomicOr(&emit[s >> 5], 1u << (s & 31));
+        }
+        vprev = v;
+        yprev = y;
+      }
+    }
+  }
+  __syncthreads();
+  phase3_output<kGenTPB, Key>(a, tile, tile_lo, keys, emit, NSW, warp_sums, &bcast);
+}
+
+// ------------------------------------------------------------------ host side
+int launch_mz(MzArgs a, int path, cudaStream_t st) {
+  const int k = a.k, w = a.w;
+  const bool h64 = 2 * k > 32;
+  const bool packed_ok = 2 * k + kSlotBits <= 64;
+  // 0 = auto, 1 = force generic
+  const bool fast = path == 0 && packed_ok && w >= 1 && w <= 16;
+  if (fast) {
+#define MZS_FAST(WW)                                                                                   \
+  case WW: {                                                                                           \
+    using G = FastGeom<WW>;                                                                            \
+    a.tw = G::TW;                                                                                      \
+    a.ntiles = (a.nwin + G::TW - 1) / G::TW;                                                           \
+    const size_t smem = sizeof(PackedKey) * G::NS;                                                     \
+    auto kern = h64 ? mz_fast_kernel<WW, true> : mz_fast_kernel<WW, false>;                            \
+    MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
+    MZS_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), st));                                \
+    MZS_CUDA(cudaMemsetAsync(a.status, 0, sizeof(uint64_t) * a.ntiles, st));                           \
+    kern<<<(unsigned)a.ntiles, G::TPB, smem, st>>>(a);                                                 \
+    MZS_LAUNCHED();                                                                                    \
+    return SLSUM_OK;                                                                                   \
+  }
+    switch (w) {
+      MZS_FAST(1) MZS_FAST(2) MZS_FAST(3) MZS_FAST(4) MZS_FAST(5) MZS_FAST(6) MZS_FAST(7) MZS_FAST(8)
+      MZS_FAST(9) MZS_FAST(10) MZS_FAST(11) MZS_FAST(12) MZS_FAST(13) MZS_FAST(14) MZS_FAST(15) MZS_FAST(16)
+      default: break;
+    }
+#undef MZS_FAST
+  }
+  if (w > 1024) return SLSUM_EUNSUPPORTED;
+  a.tw = (uint32_t)(kGenNS - w - 1);
+  a.ntiles = (a.nwin + a.tw - 1) / a.tw;
+  MZS_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), st));
+  MZS_CUDA(cudaMemsetAsync(a.status, 0, sizeof(uint64_t) * a.ntiles, st));
+  if (packed_ok) {
+    const size_t smem = 3 * sizeof(PackedKey) * kGenNS;
+    auto kern = h64 ? mz_generic_kernel<PackedKey, true> : mz_generic_kernel<PackedKey, false>;
+    MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)a.ntiles, kGenTPB, smem, st>>>(a);
+  } else {
+    const size_t smem = 3 * sizeof(WideKey) * kGenNS;
+    auto kern = mz_generic_kernel<WideKey, true>;
+    MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)a.ntiles, kGenTPB, smem, st>>>(a);
+  }
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+// max tiles for n bases (the generic path has the smallest tiles: >= 4096-1025 windows)
+uint64_t max_tiles(uint64_t n) { return n / 3000 + 2; }
+
+}  // namespace
+
+int encode_launch(const uint8_t* seq, uint64_t n, uint64_t* words, uint32_t* invalid, cudaStream_t st);
+
+}  // namespace mzs
+
+using namespace mzs;
+
+MZS_API size_t mz_workspace_bytes(uint64_t n, int k, int w, int kind) {
+  (void)k; (void)w;
+  Sizer z;
+  z.take<uint32_t>(1);                  // tile counter
+  z.take<uint64_t>(max_tiles(n));       // look-back status
+  if (kind == MZ_IN_ASCII) {
+    z.take<uint64_t>((n + 31) / 32 + 1);
+    z.take<uint32_t>((n + 31) / 32 + 1);
+  }
+  return z.used;
+}
+
+// internal entry with a path selector (0 auto, 1 generic) for tests
+MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out, void* ws,
+                            size_t ws_bytes, void* stream, int path) {
+  if (!in || !out || !out->d_count || k < 1 || k > 31 || w < 1) return SLSUM_EINVAL;
+  if (in->kind != MZ_IN_ASCII && in->kind != MZ_IN_PACKED2) return SLSUM_EINVAL;
+  if (keymode != MZ_KEY_HASH && keymode != MZ_KEY_RAW) return SLSUM_EINVAL;
+  if (in->read_off && in->nreads == 0) return SLSUM_EINVAL;
+  if (out->capacity && (!out->hash || !out->pos)) return SLSUM_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  const uint64_t n = in->n;
+  const uint64_t span = (uint64_t)k + (uint64_t)w - 1;
+  if (n < span || in->win_lo >= in->win_hi) {
+    MZS_CUDA(cudaMemsetAsync(out->d_count, 0, sizeof(uint64_t), st));
+    return SLSUM_OK;
+  }
+  if (!in->seq) return SLSUM_EINVAL;
+  TempWs tmp;
+  const size_t need = mz_workspace_bytes(n, k, w, in->kind);
+  if (!ws) {
+    MZS_CUDA(cudaMallocAsync(&tmp.p, need, st));
+    tmp.s = st;
+    ws = tmp.p;
+    ws_bytes = need;
+  }
+  if (ws_bytes < need) return SLSUM_ENOMEM;
+  Carve c(ws, ws_bytes);
+  MzArgs a{};
+  a.tile_counter = c.take<uint32_t>(1);
+  a.status = c.take<uint64_t>(max_tiles(n));
+  a.nwords = (n + 31) / 32;
+  if (in->kind == MZ_IN_ASCII) {
+    uint64_t* words = c.take<uint64_t>(a.nwords + 1);
+    uint32_t* inval = c.take<uint32_t>(a.nwords + 1);
+    int rc = encode_launch(static_cast<const uint8_t*>(in->seq), n, words, inval, st);
+    if (rc) return rc;
+    a.words = words;
+    a.invalid = inval;
+  } else {
+    a.words = static_cast<const uint64_t*>(in->seq);
+    a.invalid = in->invalid;
+  }
+  a.n = n;
+  a.nwin = n - span + 1;
+  a.read_off = in->read_off;
+  a.nreads = in->read_off ? in->nreads : 0;
+  a.pos_base = in->pos_base;
+  a.win_lo = in->win_lo;
+  a.win_hi = in->win_hi;
+  a.k = k;
+  a.w = w;
+  a.raw = keymode == MZ_KEY_RAW;
+  a.out_hash = out->hash;
+  a.out_pos = out->pos;
+  a.capacity = out->capacity;
+  a.d_count = out->d_count;
+  return launch_mz(a, path, st);
+}
+
+MZS_API int mz_extract_ex(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out, void* ws, size_t ws_bytes,
+                          void* stream) {
+  return mz_extract_path(in, k, w, keymode, out, ws, ws_bytes, stream, 0);
+}
+
+MZS_API int mz_extract(const uint8_t* seq, uint64_t n, int k, int w, mz_out_t* out) {
+  if (!out) return SLSUM_EINVAL;
+  mz_in_t in{};
+  in.kind = MZ_IN_ASCII;
+  in.seq = seq;
+  in.n = n;
+  in.win_lo = 0;
+  in.win_hi = UINT64_MAX;
+  int rc = mz_extract_ex(&in, k, w, MZ_KEY_HASH, out, nullptr, 0, nullptr);
+  if (rc) return rc;
+  uint64_t cnt = 0;
+  MZS_CUDA(cudaMemcpy(&cnt, out->d_count, sizeof(cnt), cudaMemcpyDeviceToHost));
+  return cnt > out->capacity ? SLSUM_ECAPACITY : SLSUM_OK;
+}

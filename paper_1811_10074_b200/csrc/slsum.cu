@@ -1,0 +1,212 @@
+// slsum.cu -- sliding window sums, Eq. 2:
+//   y_i = x_i (+) x_{i+1} (+) ... (+) x_{i+w-1}
+//
+// GENERIC path: Algorithm 2 "VectorInput" (L123-150) re-planned for a CTA instead of a
+// P-lane SIMD register.  A CTA tile of L = TPB*E inputs is split into blocks of length w;
+// per block the prefix folds (Alg. 2's X1) and suffix folds (Alg. 2's Y1, the carry) are
+// computed by a serial register strip per thread plus order-preserving segmented
+// warp-shuffle scans across threads (Blelloch-style parallel scan, L150).  Then
+//   y_i = S[i]                 if i starts a block
+//   y_i = S[i] (+) P[i+w-1]    otherwise
+// i.e. 3 (+) per output independent of w (L150: "for any operator (+)"; associativity
+// only).  Consecutive tiles overlap by w-1 inputs (the carry of Alg. 2 becomes a halo).
+//
+// COMMUTATIVE path: ceil(log2 w) doubling rounds t_{r+1}[i] = t_r[i] (+) t_r[i+2^r] in
+// shared memory (L44: "every sum ... is a prefix sum ... O(log(w))"; abstract L8), finished
+// by the overlap t_m[i] (+) t_m[i+w-2^m] for idempotent ops or by the binary digits of w.
+#include "ops.cuh"
+
+namespace mzs {
+namespace {
+
+template <class Op, int TPB, int E>
+__global__ void __launch_bounds__(TPB) slsum_generic_kernel(const typename Op::T* __restrict__ x,
+                                                           typename Op::T* __restrict__ y, uint64_t n,
+                                                           uint32_t w, uint64_t nout, uint32_t tout) {
+  using T = typename Op::T;
+  constexpr uint32_t L = TPB * E;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sP = reinterpret_cast<T*>(smem_raw);
+  T* sS = sP + padded_len<T>(L);
+  __shared__ SegScratch<Op, TPB> sh;
+
+  const uint64_t g0 = (uint64_t)blockIdx.x * tout;
+  const uint32_t t = threadIdx.x;
+  T v[E], P[E], S[E];
+  {
+    const uint64_t g = g0 + (uint64_t)t * E;
+    if (g + E <= n && (sizeof(T) * E) % 16 == 0 && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+      const uint4* src = reinterpret_cast<const uint4*>(x + g);
+#pragma unroll
+      for (int q = 0; q < (int)(sizeof(T) * E / 16); ++q) {
+        uint4 u = __ldg(src + q);
+        *reinterpret_cast<uint4*>(reinterpret_cast<char*>(v) + 16 * q) = u;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+    }
+  }
+  block_prefix_suffix<Op, TPB, E>(v, P, S, w, 0u, sh);
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    sP[pad_idx<T>(t * E + j)] = P[j];
+    sS[pad_idx<T>(t * E + j)] = S[j];
+  }
+  __syncthreads();
+  for (uint32_t e = t; e < tout; e += TPB) {
+    const uint64_t i = g0 + e;
+    if (i >= nout) break;
+    T s = sS[pad_idx<T>(e)];
+    y[i] = (e % w == 0) ? s : Op::op(s, sP[pad_idx<T>(e + w - 1)]);
+  }
+}
+
+template <class Op, int TPB>
+__global__ void __launch_bounds__(TPB) slsum_doubling_kernel(const typename Op::T* __restrict__ x,
+                                                            typename Op::T* __restrict__ y, uint64_t n,
+                                                            uint32_t w, uint64_t nout, uint32_t L,
+                                                            uint32_t tout) {
+  using T = typename Op::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* B = A + L;
+  const uint64_t g0 = (uint64_t)blockIdx.x * tout;
+  for (uint32_t e = threadIdx.x; e < L; e += TPB) A[e] = (g0 + e < n) ? x[g0 + e] : Op::id();
+  __syncthreads();
+  // m = floor(log2 w)
+  const int m = 31 - __clz(w);
+  if (Op::kIdempotent) {
+    for (int r = 0; r < m; ++r) {
+      const uint32_t d = 1u << r;
+      for (uint32_t e = threadIdx.x; e + d < L; e += TPB) B[e] = Op::op(A[e], A[e + d]);
+      __syncthreads();
+      T* tmp = A; A = B; B = tmp;
+    }
+    const uint32_t d = w - (1u << m);
+    for (uint32_t e = threadIdx.x; e < tout; e += TPB) {
+      if (g0 + e >= nout) break;
+      y[g0 + e] = d ? Op::op(A[e], A[e + d]) : A[e];
+    }
+  } else {
+    // binary digits of w, smallest piece leftmost: y_i = t_c0[i] (+) t_c1[i+2^c0] (+) ...
+    constexpr int NACC = 8;  // outputs per thread held in registers (tout <= 8*TPB, host-enforced)
+    T acc[NACC];
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) acc[j] = Op::id();
+    uint32_t off = 0;
+    for (int r = 0; r <= m; ++r) {
+      if ((w >> r) & 1u) {
+#pragma unroll
+        for (int j = 0; j < NACC; ++j) {
+          const uint32_t e = threadIdx.x + j * TPB;
+          if (e < tout) acc[j] = Op::op(acc[j], A[e + off]);
+        }
+        off += 1u << r;
+      }
+      if (r < m) {
+        const uint32_t d = 1u << r;
+        for (uint32_t e = threadIdx.x; e + d < L; e += TPB) B[e] = Op::op(A[e], A[e + d]);
+        __syncthreads();
+        T* tmp = A; A = B; B = tmp;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NACC; ++j) {
+      const uint32_t e = threadIdx.x + j * TPB;
+      if (e < tout && g0 + e < nout) y[g0 + e] = acc[j];
+    }
+  }
+}
+
+template <class Op>
+int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  const uint64_t nout = n - w + 1;
+  // smallest CTA whose tile keeps the halo (w-1) under 1/8 of it; 1024 threads max
+  int tpb = 256;
+  while (tpb < 1024 && (uint64_t)(w - 1) * 8 > (uint64_t)tpb * E) tpb *= 2;
+  const uint32_t L = tpb * E;
+  if (w - 1 >= L / 2) return SLSUM_EUNSUPPORTED;  // w > ~8192 (4-byte) / ~4096 (8-byte)
+  uint32_t tout = (L - (w - 1)) & ~31u;
+  if (tout == 0) tout = L - (w - 1);
+  const uint64_t grid = (nout + tout - 1) / tout;
+  const size_t smem = 2 * sizeof(T) * padded_len<T>(L);
+  const T* x = static_cast<const T*>(xv);
+  T* y = static_cast<T*>(yv);
+#define MZS_GEN(TPB_)                                                                          \
+  do {                                                                                         \
+    auto k = slsum_generic_kernel<Op, TPB_, E>;                                                \
+    MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<(unsigned)grid, TPB_, smem, st>>>(x, y, n, w, nout, tout);                            \
+  } while (0)
+  if (tpb == 256) MZS_GEN(256);
+  else if (tpb == 512) MZS_GEN(512);
+  else MZS_GEN(1024);
+#undef MZS_GEN
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+template <class Op>
+int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int TPB = 512;
+  const uint64_t nout = n - w + 1;
+  // tile: tout = 8*TPB outputs (register accumulators) from L = tout + w - 1 inputs held in
+  // two ping-pong shared-memory buffers (<= 200 KB)
+  const uint32_t tout = 8 * TPB;
+  const uint64_t Lw = ((uint64_t)tout + w - 1 + 31) & ~31ull;
+  if (2 * sizeof(T) * Lw > 200 * 1024) return SLSUM_EUNSUPPORTED;  // w > ~21500 (4-byte)
+  const uint32_t L = (uint32_t)Lw;
+  const uint64_t grid = (nout + tout - 1) / tout;
+  const size_t smem = 2 * sizeof(T) * (size_t)L;
+  auto k = slsum_doubling_kernel<Op, TPB>;
+  MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const typename Op::T*>(xv), static_cast<typename Op::T*>(yv),
+                                       n, w, nout, L, tout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+}  // namespace
+}  // namespace mzs
+
+using namespace mzs;
+
+MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n, int path, void* stream) {
+  if (w == 0 || op < SLSUM_MIN_U32 || op > SLSUM_MIN_U64) return SLSUM_EINVAL;
+  if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_AUTO) return SLSUM_EINVAL;
+  if (n < w) return SLSUM_OK;  // zero outputs (not an error)
+  if (!x || !y) return SLSUM_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  if (path == SLSUM_PATH_AUTO) path = SLSUM_PATH_GENERIC;
+  if (path == SLSUM_PATH_GENERIC) {
+    switch (op) {
+      case SLSUM_MIN_U32: return launch_generic<OpMinU32>(x, y, n, w, st);
+      case SLSUM_MAX_U32: return launch_generic<OpMaxU32>(x, y, n, w, st);
+      case SLSUM_ADD_U32: return launch_generic<OpAddU32>(x, y, n, w, st);
+      case SLSUM_ADD_F32: return launch_generic<OpAddF32>(x, y, n, w, st);
+      case SLSUM_AFFINE_U32X2: return launch_generic<OpAffine>(x, y, n, w, st);
+      case SLSUM_MIN_U64: return launch_generic<OpMinU64>(x, y, n, w, st);
+    }
+  } else {
+    switch (op) {
+      case SLSUM_MIN_U32: return launch_doubling<OpMinU32>(x, y, n, w, st);
+      case SLSUM_MAX_U32: return launch_doubling<OpMaxU32>(x, y, n, w, st);
+      case SLSUM_ADD_U32: return launch_doubling<OpAddU32>(x, y, n, w, st);
+      case SLSUM_ADD_F32: return launch_doubling<OpAddF32>(x, y, n, w, st);
+      case SLSUM_AFFINE_U32X2: return SLSUM_EUNSUPPORTED;  // not commutative (abstract L8, D15)
+      case SLSUM_MIN_U64: return launch_doubling<OpMinU64>(x, y, n, w, st);
+    }
+  }
+  return SLSUM_EINVAL;
+}
+
+MZS_API int slsum_run(int op, uint32_t w, const void* x, void* y, uint64_t n) {
+  int rc = slsum_run_ex(op, w, x, y, n, SLSUM_PATH_GENERIC, nullptr);
+  if (rc != SLSUM_OK) return rc;
+  MZS_CUDA(cudaStreamSynchronize(nullptr));
+  return SLSUM_OK;
+}

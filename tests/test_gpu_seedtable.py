@@ -1,0 +1,114 @@
+"""GPU parity: seedtable_build and the multi-GPU phases (count / partition / finalize) vs
+the oracle's seed table (Fig. 1; bucketing DESIGN.md R21).  Bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synthgen import host as G
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_1811_10074_b200")
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_table(key, pos, k, bits, use_dm=False):
+    kt, pt = _dev(key.astype(np.uint64)), _dev(pos.astype(np.uint64))
+    m = len(key)
+    if use_dm:
+        dm = torch.tensor([m], dtype=torch.int64, device="cuda").view(torch.uint64)
+        # capacity larger than the count: the device count must win
+        kt = _dev(np.concatenate([key.astype(np.uint64), np.zeros(17, np.uint64)]))
+        pt = _dev(np.concatenate([pos.astype(np.uint64), np.zeros(17, np.uint64)]))
+        off, po, fp = P.seedtable_build(kt, pt, k, bits, m=kt.numel(), d_m=dm)
+    else:
+        off, po, fp = P.seedtable_build(kt, pt, k, bits)
+    torch.cuda.synchronize()
+    return off.cpu().numpy(), po[:m].cpu().numpy(), fp[:m].cpu().numpy()
+
+
+def _cmp(key, pos, k, bits, **kw):
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    go, gp, gf = gpu_table(key, pos, k, bits, **kw)
+    assert np.array_equal(go, wo)
+    assert np.array_equal(gp, wp)
+    assert np.array_equal(gf, wf)
+
+
+@pytest.mark.parametrize("k,bits", [(15, 24), (19, 24), (15, 16), (19, 8), (15, 1), (4, 8), (12, 20), (31, 30)])
+def test_random_keys(k, bits):
+    rng = np.random.default_rng(k * 31 + bits)
+    for m in (1, 7, 4095, 4096, 4097, 100_003):
+        key = rng.integers(0, 1 << (2 * k), size=m, dtype=np.uint64)
+        pos = np.sort(rng.choice(10 ** 10, size=m, replace=False)).astype(np.uint64)
+        _cmp(key, pos, k, bits)
+
+
+def test_heavy_buckets_and_device_count():
+    rng = np.random.default_rng(1)
+    m = 300_000
+    key = np.where(rng.random(m) < 0.6, np.uint64(12345), rng.integers(0, 1 << 30, size=m, dtype=np.uint64))
+    pos = np.arange(m, dtype=np.uint64) * 3
+    _cmp(key, pos, 15, 24)
+    _cmp(key, pos, 15, 24, use_dm=True)
+    _cmp(np.full(10_000, 7, np.uint64), np.arange(10_000, dtype=np.uint64), 15, 24)
+
+
+def test_empty():
+    off, po, fp = P.seedtable_build(torch.zeros(1, dtype=torch.uint64, device="cuda"),
+                                    torch.zeros(1, dtype=torch.uint64, device="cuda"), 15, 12, m=0)
+    assert int(off.view(torch.int64).abs().sum().item()) == 0
+
+
+def test_c1_minimizers_table():
+    s = G.c1_ascii(1_000_000)
+    key, pos = O.mz(s, 15, 10)
+    _cmp(key, pos, 15, 24)
+    _cmp(key, pos, 15, 16)
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4, 8])
+def test_multi_rank_phases_emulated(nranks):
+    """The C5 exchange with the NCCL collectives replaced by in-process slicing: ranks own
+    contiguous shards of the minimizer list; count -> (sum) -> partition -> (all_to_all)
+    -> finalize; the concatenated slices must equal the single-table oracle."""
+    k, bits = 19, 24
+    c3 = G.C3(n=3_000_000)
+    key, pos = O.mz(c3.ascii(), k, 19 - 9)
+    m = len(key)
+    cuts = [m * g // nranks for g in range(nranks + 1)]
+    counts = None
+    sends = []
+    for g in range(nranks):
+        kt, pt = _dev(key[cuts[g]:cuts[g + 1]]), _dev(pos[cuts[g]:cuts[g + 1]])
+        c = P.seedtable_count(kt, k, bits).view(torch.int32).to(torch.int64)
+        counts = c if counts is None else counts + c
+        sends.append(P.seedtable_partition(kt, pt, k, bits, nranks))
+    gcounts = counts.to(torch.int32).view(torch.uint32)
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    nbl = (1 << bits) // nranks
+    all_off, all_pos, all_fp, base = [], [], [], 0
+    for r in range(nranks):
+        fps, poss = [], []
+        for g in range(nranks):
+            sf, sp, sc = sends[g]
+            sc = sc.cpu().numpy().astype(np.int64)
+            o = int(sc[:r].sum())
+            fps.append(sf[o:o + sc[r]])
+            poss.append(sp[o:o + sc[r]])
+        rf = torch.cat([f.view(torch.int32) for f in fps]).view(torch.uint32)
+        rp = torch.cat([q.view(torch.int64) for q in poss]).view(torch.uint64)
+        mr = rf.numel()
+        for gc in (gcounts, None):
+            off, po, fp = P.seedtable_finalize(rf, rp, mr, gc, bits, r, nranks)
+            offn = off.cpu().numpy()
+            assert np.array_equal(offn + np.uint64(base), wo[r * nbl: (r + 1) * nbl + 1])
+        all_pos.append(po[:mr].cpu().numpy())
+        all_fp.append(fp[:mr].cpu().numpy())
+        base += mr
+    assert np.array_equal(np.concatenate(all_pos), wp)
+    assert np.array_equal(np.concatenate(all_fp), wf)

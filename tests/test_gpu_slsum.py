@@ -1,0 +1,122 @@
+"""GPU parity: slsum_run_ex (GENERIC and COMMUTATIVE paths) vs the oracle's strict left
+fold (Eq. 2).  Integer ops bit-exact; f32 add within the BASELINE
+tolerance |g - o| <= 1e-5 |o| + 1e-6 w."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synthgen import host as G
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_1811_10074_b200")
+
+OPS = [(P.SLSUM_MIN_U32, O.MIN_U32), (P.SLSUM_MAX_U32, O.MAX_U32), (P.SLSUM_ADD_U32, O.ADD_U32),
+       (P.SLSUM_ADD_F32, O.ADD_F32), (P.SLSUM_AFFINE_U32X2, O.AFFINE_U32X2), (P.SLSUM_MIN_U64, O.MIN_U64)]
+WS = [1, 2, 3, 4, 5, 7, 10, 16, 17, 31, 32, 33, 64, 100, 255, 256, 1000, 1024]
+
+
+def _input(op, n, rng):
+    if op == P.SLSUM_ADD_F32:
+        return rng.standard_normal(n).astype(np.float32)
+    if op == P.SLSUM_AFFINE_U32X2:
+        return rng.integers(0, 2 ** 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    if op == P.SLSUM_MIN_U64:
+        return rng.integers(0, 2 ** 63, size=n, dtype=np.uint64)
+    hi = 2 ** 32 if rng.random() < 0.7 else 5  # small alphabets force ties
+    return rng.integers(0, hi, size=n, dtype=np.uint64).astype(np.uint32)
+
+
+def _check(op, w, x, got):
+    want = O.slsum(dict(OPS)[op], w, x)
+    assert got.shape == want.shape
+    if op == P.SLSUM_ADD_F32:
+        tol = 1e-5 * np.abs(want.astype(np.float64)) + 1e-6 * w
+        err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+        assert np.all(err <= tol), (w, float((err / tol).max()))
+    else:
+        assert np.array_equal(got, want), (op, w)
+
+
+def _run(op, w, x, path):
+    xt = torch.from_numpy(x).cuda()
+    y = P.slsum_run(op, w, xt, path=path)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()  # uint32/uint64 tensors only move bytes here (no torch arithmetic)
+
+
+@pytest.mark.parametrize("op", [o for o, _ in OPS])
+@pytest.mark.parametrize("w", WS)
+def test_generic_vs_oracle(op, w):
+    rng = np.random.default_rng(op * 10000 + w)
+    for n in sorted({w, w + 1, 2 * w + 3, 5000, 70_001}):
+        x = _input(op, n, rng)
+        _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_GENERIC))
+
+
+@pytest.mark.parametrize("op", [o for o, _ in OPS if o != P.SLSUM_AFFINE_U32X2])
+@pytest.mark.parametrize("w", WS)
+def test_commutative_vs_oracle(op, w):
+    rng = np.random.default_rng(op * 777 + w)
+    for n in sorted({w, w + 5, 9000, 50_003}):
+        x = _input(op, n, rng)
+        _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_COMMUTATIVE))
+
+
+def test_affine_rejected_by_commutative_path():
+    x = torch.zeros((100, 2), dtype=torch.uint32, device="cuda")
+    with pytest.raises(P.SlsumError) as e:
+        P.slsum_run(P.SLSUM_AFFINE_U32X2, 4, x, path=P.SLSUM_PATH_COMMUTATIVE)
+    assert e.value.rc == P.SLSUM_EUNSUPPORTED
+
+
+def test_degenerate():
+    x = torch.from_numpy(np.arange(10, dtype=np.uint32)).cuda()
+    assert P.slsum_run(P.SLSUM_ADD_U32, 11, x).numel() == 0
+    y = P.slsum_run(P.SLSUM_ADD_U32, 10, x)
+    assert y.cpu().numpy().tolist() == [45]
+    assert np.array_equal(P.slsum_run(P.SLSUM_MIN_U32, 1, x).cpu().numpy(), np.arange(10, dtype=np.uint32))
+    with pytest.raises(P.SlsumError):
+        P.slsum_run(P.SLSUM_ADD_U32, 0, x)
+    e = torch.zeros(0, dtype=torch.uint32, device="cuda")
+    assert P.slsum_run(P.SLSUM_MIN_U32, 3, e).numel() == 0
+
+
+@pytest.mark.parametrize("w", [4, 16, 64, 256, 1024])
+def test_c2_full_size_sampled(w):
+    """C2 at full size (2^28 elements) in bench.py's launch configuration: sampled outputs vs
+    the oracle computed one by one, plus the exact u32-add closed form at every position."""
+    n = 1 << 28
+    from synthgen import device as D
+    xu = D.c2_u32(n)
+    rng = np.random.default_rng(w)
+    idx = np.concatenate([[0, n - w], rng.integers(0, n - w + 1, size=200)])
+    it = torch.from_numpy(idx).cuda()
+    for op in (P.SLSUM_MIN_U32, P.SLSUM_ADD_U32):
+        for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE):
+            y = P.slsum_run(op, w, xu, path=path)
+            ys = y.view(torch.int32)[it].cpu().numpy().view(np.uint32)
+            for j, i in enumerate(idx):
+                xs = G.c2_u32(w, lo=int(i))
+                assert ys[j] == O.slsum(dict(OPS)[op], w, xs)[0], (op, path, i)
+            if op == P.SLSUM_ADD_U32:
+                # exact closed form at every position: prefix differences mod 2^32 (torch.cumsum)
+                x64 = xu.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+                ps = torch.cumsum(x64, 0)  # < 2^60, exact
+                del x64
+                ref = ps[w - 1:].clone()
+                ref[1:] -= ps[: n - w]
+                del ps
+                got = y.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+                assert torch.equal(ref & 0xFFFFFFFF, got)
+                del ref, got
+            del y
+    xf = D.c2_f32(n)
+    for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE):
+        y = P.slsum_run(P.SLSUM_ADD_F32, w, xf, path=path)
+        ys = y[it].cpu().numpy()
+        for j, i in enumerate(idx):
+            o = O.slsum(O.ADD_F32, w, G.c2_f32(w, lo=int(i)))[0]
+            assert abs(float(ys[j]) - float(o)) <= 1e-5 * abs(float(o)) + 1e-6 * w
+        del y
