@@ -111,8 +111,17 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   if (CHECK) {
     // run length at base x0 = q0 + k - 2 (capped at span), then walk base by base
     const int64_t x0 = q0 + k - 2;
-    const uint64_t bits = inv_window64(a, x0 - span + 1) & ((span >= 64) ? ~0ull : ((1ull << span) - 1));
-    int64_t start = bits ? (x0 - span + 1) + (63 - __clzll(bits)) + 1 : x0 - span + 1;
+    // last invalid base in [x0-span+1, x0], scanning back 64 bases at a time (span may exceed 64)
+    int64_t start = x0 - span + 1;
+    for (int64_t hi = x0; hi >= x0 - span + 1; hi -= 64) {
+      const int64_t lo = max(hi - 63, x0 - span + 1);
+      const int cnt = (int)(hi - lo + 1);
+      const uint64_t bits = inv_window64(a, lo) & (cnt >= 64 ? ~0ull : ((1ull << cnt) - 1));
+      if (bits) {
+        start = lo + (63 - __clzll(bits)) + 1;
+        break;
+      }
+    }
     if (a.read_off) {
       ri = upper_read(a, x0);                 // first read start > x0
       const int64_t rs = ri ? (int64_t)__ldg(a.read_off + ri - 1) : 0;

@@ -1,0 +1,126 @@
+"""CPU multi-process tests of the multi-GPU path (world_size 2 and 4, gloo backend).
+
+The planner (paper_1811_10074_b200.dist.plan_shards) and the C5 exchange logic
+(exchange_seedtable: all_reduce of counts, all_to_all of split sizes and entries,
+per-rank base offsets) run exactly as on the GPUs; only the local phases are replaced by
+oracle-backed ones (test-only), so no GPU is needed.  Every rank's slice must equal the
+matching slice of the single-process oracle table, and the shard outputs must
+concatenate to the single-process minimizer list (R25)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from synthgen import host as H
+
+K, W, BITS = 16, 10, 12   # 2k = 32: the fingerprint is the key itself (oracle helpers stay exact)
+N = 400_000
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OraclePhases:
+    """Test-only local phases built from the oracle + numpy (never used by the product)."""
+
+    def count(self, hash_, m, k, bits):
+        key = hash_[:m].numpy().view(np.uint64)
+        off, _, _ = O.seedtable(key, np.zeros(m, np.uint64), k, bits)
+        return torch.from_numpy(np.diff(off.astype(np.int64)).astype(np.int32))
+
+    def partition(self, hash_, pos, m, k, bits, nranks):
+        key = hash_[:m].numpy().view(np.uint64)
+        fp = np.array([O.fingerprint(int(x), k) for x in key], dtype=np.uint32)
+        g = nranks.bit_length() - 1
+        owner = (fp >> (32 - g)) if g else np.zeros(m, np.uint32)
+        order = np.argsort(owner, kind="stable")
+        counts = np.bincount(owner, minlength=nranks).tolist()
+        return (torch.from_numpy(fp[order].view(np.int32).copy()),
+                torch.from_numpy(pos[:m].numpy()[order].copy()), counts)
+
+    def finalize(self, recv_fp, recv_pos, m_recv, global_counts, bits, rank, nranks):
+        fp = recv_fp[:m_recv].numpy().view(np.uint32).astype(np.uint64)
+        ps = recv_pos[:m_recv].numpy().view(np.uint64)
+        off, fpo, po = O.seedtable(fp, ps, 16, bits)          # 2k = 32: key = fingerprint
+        nbl = (1 << bits) // nranks
+        loc = off[rank * nbl: (rank + 1) * nbl + 1].astype(np.int64)
+        return (torch.from_numpy(loc - loc[0]), torch.from_numpy(po.view(np.int64).copy()),
+                torch.from_numpy(fpo.view(np.int32).copy()))
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1811_10074_b200 import dist as D
+        c3 = H.C3(n=N)
+        seq = c3.ascii()
+        sh = D.plan_shards(N, K, W, world)[rank]
+        sub = seq[sh.base_lo: sh.base_hi]
+        key, pos = O.mz(sub, K, W, pos_base=sh.base_lo, win_lo=sh.win_lo, win_hi=sh.win_hi)
+        m = len(key)
+        off, pl, fl, base = D.exchange_seedtable(torch.from_numpy(key.view(np.int64).copy()),
+                                                 torch.from_numpy(pos.view(np.int64).copy()), m, K, BITS,
+                                                 OraclePhases())
+        q.put((rank, key, pos, off.numpy(), pl.numpy(), fl.numpy(), base))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_extraction_and_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    seq = H.C3(n=N).ascii()
+    wk, wp = O.mz(seq, K, W)
+    # shard outputs concatenate to the single-process list
+    assert np.array_equal(np.concatenate([r[1] for r in res]), wk)
+    assert np.array_equal(np.concatenate([r[2] for r in res]), wp)
+    # the ranks' table slices concatenate to the single-process table
+    wo, wf, wpos = O.seedtable(wk, wp, K, BITS)
+    nbl = (1 << BITS) // world
+    for rank, _, _, off, pl, fl, base in res:
+        assert np.array_equal(off.astype(np.uint64) + np.uint64(base), wo[rank * nbl: (rank + 1) * nbl + 1])
+    assert np.array_equal(np.concatenate([r[4] for r in res]).view(np.uint64), wpos)
+    assert np.array_equal(np.concatenate([r[5] for r in res]).view(np.uint32), wf)
+
+
+def test_plan_shards_covers_windows():
+    from paper_1811_10074_b200 import dist as D
+    for n, k, w, G in [(10_000, 19, 10, 8), (100, 15, 10, 4), (24, 15, 10, 2), (3_100_000_000, 19, 10, 8)]:
+        sh = D.plan_shards(n, k, w, G)
+        nwin = max(0, n - (k + w - 1) + 1)
+        assert sh[0].win_a == 0 and sh[-1].win_b == nwin
+        for a, b in zip(sh, sh[1:]):
+            assert a.win_b == b.win_a
+        for s in sh:
+            if s.win_b > s.win_a:
+                assert s.base_lo == max(0, s.win_a - 1) and s.base_hi == s.win_b + k + w - 2
+                assert s.win_hi - s.win_lo == s.win_b - s.win_a
+
+
+def test_plan_reads_balanced():
+    from paper_1811_10074_b200 import dist as D
+    c4 = H.C4(nreads=10_000)
+    parts = D.plan_reads(c4.read_off, 8)
+    assert parts[0][0] == 0 and parts[-1][1] == 10_000
+    sizes = [int(c4.read_off[b] - c4.read_off[a]) for a, b in parts]
+    assert max(sizes) < 1.2 * (c4.n / 8)
