@@ -90,17 +90,19 @@ constexpr uint64_t kLbAgg = 1ull << 62;      // tile aggregate published
 constexpr uint64_t kLbInc = 2ull << 62;      // inclusive prefix published
 constexpr uint64_t kLbVal = (1ull << 62) - 1;
 
-// Called by ALL 32 lanes of ONE warp.  Publishes `agg` for tile `tile`, walks back over
-// predecessors 32 at a time and returns the exclusive prefix (sum of all earlier tiles'
-// aggregates).  Tiles must be numbered in launch order (dynamic tile ids), so every
-// predecessor is resident or finished: no deadlock.
-__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_t tile, uint64_t agg) {
+// Decoupled look-back, split in two so a tile can publish its aggregate as soon as it is
+// known and resolve its prefix later (after doing other work).
+// publish: one thread.  Tile 0's aggregate is its inclusive prefix.
+__device__ __forceinline__ void lookback_publish(uint64_t* status, uint64_t tile, uint64_t agg) {
+  st_volatile_u64(&status[tile], (tile == 0 ? kLbInc : kLbAgg) | agg);
+}
+// resolve: ALL 32 lanes of ONE warp.  Walks back over predecessors 32 at a time, returns
+// the exclusive prefix and publishes this tile's inclusive prefix.  Tiles are numbered in
+// claim order and every claimed tile publishes its aggregate without waiting, so the walk
+// always terminates.
+__device__ __forceinline__ uint64_t lookback_resolve(uint64_t* status, uint64_t tile, uint64_t agg) {
   const unsigned lane = lane_id();
-  if (tile == 0) {
-    if (lane == 0) st_volatile_u64(&status[0], kLbInc | agg);
-    return 0;
-  }
-  if (lane == 0) st_volatile_u64(&status[tile], kLbAgg | agg);
+  if (tile == 0) return 0;
   uint64_t excl = 0;
   int64_t base = (int64_t)tile - 1;
   while (true) {
@@ -124,6 +126,13 @@ __device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_
   }
   if (lane == 0) st_volatile_u64(&status[tile], kLbInc | (excl + agg));
   return excl;
+}
+
+// Both steps at once (ALL 32 lanes of ONE warp).
+__device__ __forceinline__ uint64_t lookback_exclusive(uint64_t* status, uint64_t tile, uint64_t agg) {
+  if (lane_id() == 0) lookback_publish(status, tile, agg);
+  __syncwarp();
+  return lookback_resolve(status, tile, agg);
 }
 
 // Block-wide exclusive sum of one value per thread (TPB threads, multiple of 32).

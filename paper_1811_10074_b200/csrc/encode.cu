@@ -8,17 +8,26 @@
 namespace mzs {
 namespace {
 
-// 4 ASCII bytes (little-endian in v) -> 4 codes (byte lanes) and a 4-bit invalid mask
-__device__ __forceinline__ void enc4(uint32_t v, uint32_t& codes, uint32_t& inv) {
-  const uint32_t u = v & 0xDFDFDFDFu;  // upper case
-  // code = ((c >> 1) & 3) ^ ((c >> 2) & 1): A 0x41 -> 0, C 0x43 -> 1, G 0x47 -> 2, T 0x54 -> 3
-  codes = ((u >> 1) & 0x03030303u) ^ ((u >> 2) & 0x01010101u);
-  const uint32_t ok = __vcmpeq4(u, 0x41414141u) | __vcmpeq4(u, 0x43434343u) | __vcmpeq4(u, 0x47474747u) |
-                      __vcmpeq4(u, 0x54545454u);
-  // ok has 0xFF in every valid byte lane
-  const uint32_t bad = ~ok;
-  inv = ((bad >> 7) & 1u) | ((bad >> 14) & 2u) | ((bad >> 21) & 4u) | ((bad >> 28) & 8u);
-  codes &= ok;  // invalid bases carry code 0
+// 4 ASCII bytes (little-endian in v) -> one byte of 4 MSB-first 2-bit codes and a 4-bit
+// invalid mask (bit j <-> byte j).  SWAR, no per-byte branches:
+//   u    = v & 0xDF..              upper case
+//   c_j  = ((u>>1)&3) ^ ((u>>2)&1) A 0x41 -> 0, C 0x43 -> 1, G 0x47 -> 2, T 0x54 -> 3
+//   e_j  = 0x41 + {0,2,6,19}[c_j]  the letter that code would come from
+//   valid_j <=> u_j == e_j          exact per-byte zero test of u ^ e
+__device__ __forceinline__ void enc4(uint32_t v, uint32_t& packed_byte, uint32_t& inv4) {
+  const uint32_t u = v & 0xDFDFDFDFu;
+  const uint32_t c = ((u >> 1) & 0x03030303u) ^ ((u >> 2) & 0x01010101u);
+  const uint32_t c1 = (c >> 1) & 0x01010101u;                 // c >= 2
+  const uint32_t c3 = c & c1;                                  // c == 3
+  const uint32_t e = 0x41414141u + 2u * c + 2u * c1 + 11u * c3;
+  const uint32_t x = u ^ e;
+  // per byte: 0x80 iff the byte of x is zero (valid), exact (no borrow across bytes)
+  const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+  const uint32_t cm = c & ((z >> 7) * 0xFFu);                 // invalid bases carry code 0
+  // gather c_j (bits 8j) to bits 30-2j of the low word: byte = c0<<6|c1<<4|c2<<2|c3
+  packed_byte = (cm * 0x40100401u) >> 24;
+  // gather the invalid flags (bits 8j after >> 7) to bits 21..24
+  inv4 = ((((~z & 0x80808080u) >> 7) * 0x00204081u) >> 21) & 0xFu;
 }
 
 __global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__ seq, uint64_t n,
@@ -48,11 +57,10 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__
   uint32_t inv = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    uint32_t c, m;
-    enc4(v[i], c, m);
-    // bases 4i..4i+3 (byte lanes 0..3) -> bits (63-2j, 62-2j), j = 4i + lane
-    const uint32_t packed = ((c & 0xFFu) << 6) | (((c >> 8) & 0xFFu) << 4) | (((c >> 16) & 0xFFu) << 2) | (c >> 24);
-    word |= (uint64_t)packed << (56 - 8 * i);
+    uint32_t pb, m;
+    enc4(v[i], pb, m);
+    // bases 4i..4i+3 -> bits (63-8i .. 56-8i)
+    word |= (uint64_t)pb << (56 - 8 * i);
     inv |= m << (4 * i);
   }
   if (b0 + 32 > n) {  // bits past n are 0

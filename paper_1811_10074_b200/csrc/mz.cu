@@ -15,6 +15,8 @@
 //            tiles (single pass, deterministic) -> (hash, pos) records.
 // Fast path: w in [1,16] as a compile-time block length (S/P in registers), k <= 25.
 // Generic path: any w <= 1024 and any k <= 31, S/P by block-wide segmented scans.
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace mzs {
@@ -90,12 +92,16 @@ __device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
 }
 
 // ------------------------------------------------------------------ phase 1
-// Keys of k-mers q0 .. q0+Q-1 into slots s0 .. s0+Q-1.  If CHECK, wv[slot] = 1 iff the
-// window whose LAST k-mer is that slot's k-mer is valid (run of valid same-read bases
-// ending at the k-mer's last base >= k + w - 1).
-template <class Key, int Q, bool H64, bool CHECK>
-__device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint8_t* wv) {
-  const int k = a.k;
+// Keys of k-mers q0 .. q0+Q-1 into slots s0 .. s0+Q-1.  If CHECK, bit `slot` of the shared
+// bitmask wvb (zeroed by the caller) is set iff the window whose LAST k-mer is that slot's
+// k-mer is valid (run of valid same-read bases ending at the k-mer's last base >= k+w-1).
+// KK != 0: k is the compile-time constant KK (lets the compiler drop the masking and the
+// xor-shift work on the always-zero high bits); RAW: keys are the codes themselves.
+template <class Key, int Q, bool H64, bool CHECK, int KK = 0, bool RAW = false>
+__device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint32_t* wvb) {
+  static_assert(Q <= 33, "validity bits of one strip fit in a u64 shifted by < 32");
+  uint64_t vbits = 0;
+  const int k = KK ? KK : a.k;
   const int64_t wi = q0 >> 5;
   const uint32_t off = (uint32_t)(q0 & 31) * 2;
   const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1), C = ldw(a, wi + 2);
@@ -133,7 +139,8 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   }
   const int kk = 2 * k;
   if (H64) {
-    const uint64_t km = (kk == 64) ? ~0ull : ((1ull << kk) - 1);
+    // 2k > 32: the low word of the mask is all ones (lets the compiler mask the high word only)
+    const uint64_t km = ((uint64_t)((1u << (kk - 32)) - 1u) << 32) | 0xffffffffull;
     uint64_t code = X >> (64 - kk);
 #pragma unroll
     for (int s = 0; s < Q; ++s) {
@@ -150,9 +157,9 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
           while (next_rs <= x) next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
         }
         run = inv ? 0u : run + 1u;
-        wv[s0 + s] = run >= (uint32_t)span;
+        vbits |= (uint64_t)(run >= (uint32_t)span) << s;
       }
-      const uint64_t h = a.raw ? code : hash_b64(code, km);
+      const uint64_t h = RAW ? code : hash_b64(code, km);
       keys[s0 + s] = Key::make(h, s0 + s);
     }
   } else {
@@ -173,13 +180,23 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
           while (next_rs <= x) next_rs = (++ri <= a.nreads) ? (int64_t)__ldg(a.read_off + ri) : INT64_MAX;
         }
         run = inv ? 0u : run + 1u;
-        wv[s0 + s] = run >= (uint32_t)span;
+        vbits |= (uint64_t)(run >= (uint32_t)span) << s;
       }
-      const uint32_t h = a.raw ? code : hash_b32(code, km);
+      const uint32_t h = RAW ? code : hash_b32(code, km);
       keys[s0 + s] = Key::make(h, s0 + s);
     }
   }
+  if (CHECK && vbits) {
+    const uint32_t w0 = s0 >> 5, sh = s0 & 31;
+    const uint32_t lo = (uint32_t)(vbits << sh), mid = (uint32_t)(vbits >> (32 - sh));
+    const uint32_t hi = sh ? (uint32_t)(vbits >> (64 - sh)) : 0u;
+    if (lo) atomicOr(&wvb[w0], lo);
+    if (mid) atomicOr(&wvb[w0 + 1], mid);
+    if (hi) atomicOr(&wvb[w0 + 2], hi);
+  }
 }
+
+__device__ __forceinline__ bool wv_bit(const uint32_t* wvb, int s) { return (wvb[s >> 5] >> (s & 31)) & 1u; }
 
 // Packed key: (hash << 14) | slot -- lexicographic (hash, position) order in one u64.
 struct PackedKey {
@@ -256,17 +273,50 @@ __device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int
   return !__syncthreads_or(dirty);
 }
 
-// Phase 3: ordered output of the emitted slots of this tile.
-template <int TPB, class Key>
-__device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, int64_t tile_lo, const Key* keys,
-                                              const uint32_t* emit, uint32_t nsw, uint64_t* warp_sums,
+// Code + key of the k-mer at local position q, from scratch (phase 3 re-derives the hash
+// of every emitted position instead of keeping all keys of a super-tile resident).
+template <bool H64, int KK = 0>
+__device__ __forceinline__ uint64_t key_at(const MzArgs& a, int64_t q) {
+  const int64_t wi = q >> 5;
+  const uint32_t off = (uint32_t)(q & 31) * 2;
+  const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1);
+  const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
+  const int kk = 2 * (KK ? KK : a.k);
+  if (H64) {
+    const uint64_t code = X >> (64 - kk);
+    const uint64_t km = ((uint64_t)((1u << (kk - 32)) - 1u) << 32) | 0xffffffffull;
+    return a.raw ? code : hash_b64(code, km);
+  } else {
+    const uint32_t code = (uint32_t)(X >> (64 - kk));
+    const uint32_t km = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
+    return a.raw ? code : hash_b32(code, km);
+  }
+}
+
+// Phase 3: ordered output of the slots marked in `emit` (S sub-tiles x NS slots each; slot s
+// of sub-tile u is the k-mer sub_lo(u) - 1 + s).  The set bits are first compacted, in order,
+// into a shared list of super-tile slot indices (the keys' smem, no longer needed); one
+// look-back per super-tile; then one thread per record re-derives the hash and writes.
+template <int TPB, bool H64>
+__device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, int64_t super_lo, int NS, int nsub,
+                                              const uint32_t* emit, uint16_t* list, uint64_t* warp_sums,
                                               uint64_t* bcast) {
-  const uint32_t wpt = (nsw + TPB - 1) / TPB;
-  const uint32_t u0 = threadIdx.x * wpt;
-  uint64_t cnt = 0;
-  for (uint32_t u = u0; u < u0 + wpt && u < nsw; ++u) cnt += __popc(emit[u]);
+  const int nsw = nsub * (NS / 32);
+  const int wpt = (nsw + TPB - 1) / TPB;
+  const int u0 = threadIdx.x * wpt;
+  const int u1 = min(nsw, u0 + wpt);
+  uint32_t cnt = 0;
+  for (int u = u0; u < u1; ++u) cnt += __popc(emit[u]);
   uint64_t total;
-  const uint64_t excl = block_exclusive_sum<TPB, uint64_t>(cnt, warp_sums, &total);
+  uint32_t o = (uint32_t)block_exclusive_sum<TPB, uint64_t>(cnt, warp_sums, &total);
+  for (int u = u0; u < u1; ++u) {
+    uint32_t bits = emit[u];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      list[o++] = (uint16_t)(u * 32 + b);
+    }
+  }
   if (warp_id() == 0) {
     const uint64_t off = lookback_exclusive(a.status, tile, total);
     if (lane_id() == 0) {
@@ -275,19 +325,16 @@ __device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, in
     }
   }
   __syncthreads();
-  uint64_t o = *bcast + excl;
-  for (uint32_t u = u0; u < u0 + wpt && u < nsw; ++u) {
-    uint32_t bits = emit[u];
-    while (bits) {
-      const uint32_t b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const uint32_t slot = u * 32 + b;
-      if (o < a.capacity) {
-        a.out_hash[o] = keys[slot].hash();
-        a.out_pos[o] = a.pos_base + (uint64_t)(tile_lo - 1 + (int64_t)slot);
-      }
-      ++o;
-    }
+  const uint64_t base = *bcast;
+  const uint32_t nrec = (uint32_t)total;
+  for (uint32_t i = threadIdx.x; i < nrec; i += TPB) {
+    const uint64_t oo = base + i;
+    if (oo >= a.capacity) break;
+    const int slot_all = list[i];
+    const int sub = slot_all / NS, slot = slot_all - sub * NS;
+    const int64_t q = super_lo + (int64_t)sub * a.tw - 1 + slot;
+    a.out_hash[oo] = key_at<H64>(a, q);
+    a.out_pos[oo] = a.pos_base + (uint64_t)q;
   }
 }
 
@@ -300,44 +347,47 @@ struct FastGeom {
   static constexpr int M = ((M0 * W) % 2 == 0) ? M0 : (M0 > 1 ? M0 - 1 : 2);
   static constexpr int R = M * W;
   static constexpr int Q = R + 1;
-  static constexpr int TW = TPB * R;
-  static constexpr int NS = TPB * Q;
+  static constexpr int TW = TPB * R;     // windows per sub-tile
+  static constexpr int NS = TPB * Q;     // key slots per sub-tile
   static constexpr int NSW = NS / 32;
+  static constexpr int SUBS = 4;         // sub-tiles per super-tile (one look-back each)
   static_assert(Q <= 33, "phase-1 rolling window holds 32 bases");
+  static_assert(R + W <= 64, "per-thread emission mask");
   static_assert(NS < (1 << kSlotBits), "slot bits");
+  static_assert(SUBS * NS * 2 <= NS * 8 && SUBS * NS < 65536, "phase-3 slot list fits in the keys smem");
   static_assert(TPB >= W + 1, "halo slots");
 };
 
-template <int W, bool H64, bool CHECK>
-__device__ __forceinline__ void fast_tile(const MzArgs& a, uint64_t tile, int64_t tile_lo, PackedKey* keys,
-                                          uint8_t* wv, uint32_t* emit) {
+// Phase 2 for one sub-tile: thread t owns windows jb .. jb+R-1 (window j = slots j+1 .. j+W).
+// [vlo, vhi): windows that exist; [elo, ehi): windows allowed to emit (shard range).
+// FULL: every window of the strip (and the one before it) is valid and may emit -- the
+// common case -- so the per-window work is the 3 minima plus the change test.
+template <int W, bool CHECK, bool FULL>
+__device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_t* wvb, int vlo, int vhi, int elo,
+                                            int ehi, uint32_t* emit) {
   using G = FastGeom<W>;
-  const int t = threadIdx.x;
-  // ---- phase 1: slots t*Q .. t*Q+Q-1 <-> k-mers tile_lo-1+t*Q ...
-  phase1_keys<PackedKey, G::Q, H64, CHECK>(a, tile_lo - 1 + (int64_t)t * G::Q, (uint32_t)(t * G::Q), keys, wv);
-  __syncthreads();
-  // ---- phase 2: windows j = t*R .. t*R+R-1 (tile-relative); window j = slots j+1 .. j+W
-  const int jb = t * G::R;
-  const int64_t i_base = tile_lo + jb;  // sequence-local window index of j = jb
+  const int jb = threadIdx.x * G::R;
   PackedKey S[W], kb[W];
-  PackedKey yprev;
+  uint32_t sprev;  // slot of the previous window's argmin
   bool vprev;
+  uint64_t em = 0;  // bit i <-> slot jb + 1 + i
   auto valid_of = [&](int j) -> bool {
-    const int64_t i = tile_lo + j;
-    if (i < 0 || (uint64_t)i >= a.nwin) return false;
-    return CHECK ? (wv[j + W] != 0) : true;
+    if (FULL) return true;
+    const bool in = (unsigned)(j - vlo) < (unsigned)(vhi - vlo);
+    return CHECK ? (in && wv_bit(wvb, j + W)) : in;
   };
   auto visit = [&](int j, PackedKey y) {
-    const bool v = valid_of(j);
-    const int64_t i = tile_lo + j;
-    if (v && (!vprev || y != yprev) && (uint64_t)i >= a.win_lo && (uint64_t)i < a.win_hi) {
-      const uint32_t s = y.slot();
-      atomicOr(&emit[s >> 5], 1u << (s & 31));
+    const uint32_t s = y.slot();
+    if (FULL) {
+      em |= (uint64_t)(s != sprev) << (s - (uint32_t)(jb + 1));
+    } else {
+      const bool v = valid_of(j);
+      const bool e = v && (!vprev || s != sprev) && ((unsigned)(j - elo) < (unsigned)(ehi - elo));
+      em |= (uint64_t)e << (s - (uint32_t)(jb + 1));
+      vprev = v;
     }
-    vprev = v;
-    yprev = y;
+    sprev = s;
   };
-  // block 0 keys and the window before the strip (j = jb - 1 = slots jb .. jb+W-1)
   {
     const PackedKey k0 = keys[jb];
 #pragma unroll
@@ -345,18 +395,17 @@ __device__ __forceinline__ void fast_tile(const MzArgs& a, uint64_t tile, int64_
     PackedKey p = kb[0];
 #pragma unroll
     for (int q = 1; q < W - 1; ++q) p = kmin(p, kb[q]);
-    yprev = (W == 1) ? k0 : kmin(k0, p);
+    sprev = ((W == 1) ? k0 : kmin(k0, p)).slot();
     vprev = valid_of(jb - 1);
     S[W - 1] = kb[W - 1];
 #pragma unroll
     for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
   }
-  (void)i_base;
 #pragma unroll 1
   for (int b = 1; b <= G::M; ++b) {
-    const int jblk = jb + (b - 1) * W;  // first window of block b-1
+    const int jblk = jb + (b - 1) * W;
     visit(jblk, S[0]);
-    const int sb = jb + 1 + b * W;      // first slot of block b
+    const int sb = jb + 1 + b * W;
 #pragma unroll
     for (int q = 0; q < W; ++q) kb[q] = keys[sb + q];
     PackedKey p = kb[0];
@@ -369,35 +418,150 @@ __device__ __forceinline__ void fast_tile(const MzArgs& a, uint64_t tile, int64_
 #pragma unroll
     for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
   }
+  // OR the strip's mask into the shared bitmask (slots jb+1 .. jb+R+W)
+  if (em) {
+    const int s0 = jb + 1;
+    const int w0 = s0 >> 5, sh = s0 & 31;
+    const uint32_t lo = (uint32_t)(em << sh);
+    const uint32_t mid = (uint32_t)(em >> (32 - sh));
+    const uint32_t hi = sh ? (uint32_t)(em >> (64 - sh)) : 0u;
+    if (lo) atomicOr(&emit[w0], lo);
+    if (mid) atomicOr(&emit[w0 + 1], mid);
+    if (hi) atomicOr(&emit[w0 + 2], hi);
+  }
 }
 
-template <int W, bool H64>
-__global__ void __launch_bounds__(256) mz_fast_kernel(MzArgs a) {
+// Output of one finished super-tile (fast path): its emit bitmask -> ordered slot list in
+// `list` -> prefix via look-back -> records.  Called one super-tile LATE (see the kernel), so
+// the look-back finds its predecessors' aggregates already published.
+template <int W, bool H64, int KK>
+__device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, const uint32_t* emit, uint32_t excl,
+                                            uint32_t total, uint16_t* list, uint64_t* bcast) {
   using G = FastGeom<W>;
+  constexpr int NSWT = G::SUBS * G::NSW;
+  constexpr int WPT = (NSWT + G::TPB - 1) / G::TPB;
+  const int u0 = threadIdx.x * WPT;
+  uint32_t o = excl;
+#pragma unroll
+  for (int uu = 0; uu < WPT; ++uu) {
+    const int u = u0 + uu;
+    if (u >= NSWT) break;
+    uint32_t bits = emit[u];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      list[o++] = (uint16_t)(u * 32 + b);
+    }
+  }
+  if (warp_id() == 0) {
+    const uint64_t off = lookback_resolve(a.status, tile, total);
+    if (lane_id() == 0) {
+      *bcast = off;
+      if (tile == a.ntiles - 1) *a.d_count = off + total;
+    }
+  }
+  __syncthreads();
+  const uint64_t base = *bcast;
+  const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
+  for (uint32_t i = threadIdx.x; i < total; i += G::TPB) {
+    const uint64_t oo = base + i;
+    if (oo >= a.capacity) break;
+    const uint32_t slot_all = list[i];
+    const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
+    const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
+    const int64_t q = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
+    a.out_hash[oo] = key_at<H64, KK>(a, q);
+    a.out_pos[oo] = a.pos_base + (uint64_t)q;
+  }
+  __syncthreads();  // `list` and `emit` are reused next
+}
+
+// Persistent: every CTA claims super-tiles in order (atomic counter), computes phases 1-2 of
+// all SUBS sub-tiles into one of two emit bitmasks, publishes the super-tile's record count,
+// and only then outputs its PREVIOUS super-tile -- one super-tile of slack for the
+// predecessors' counts to arrive.
+template <int W, bool H64, int KK>
+__global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
+  using G = FastGeom<W>;
+  constexpr int NSWT = G::SUBS * G::NSW;
+  constexpr int WPT = (NSWT + G::TPB - 1) / G::TPB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PackedKey* keys = reinterpret_cast<PackedKey*>(smem_raw);
-  __shared__ uint32_t emit[G::NSW];
-  __shared__ uint8_t wv[G::NS];
+  __shared__ uint32_t emit[2][NSWT + 2];
+  __shared__ uint32_t wvb[G::NSW + 3];
   __shared__ uint64_t warp_sums[G::TPB / 32];
   __shared__ uint64_t bcast;
   __shared__ uint32_t s_tile;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  for (int u = threadIdx.x; u < G::NSW; u += G::TPB) emit[u] = 0;
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const int64_t tile_lo = (int64_t)tile * G::TW;
-  const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + G::NS + a.k;  // bases touched
-  const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi);
-  if (clean) fast_tile<W, H64, false>(a, tile, tile_lo, keys, wv, emit);
-  else fast_tile<W, H64, true>(a, tile, tile_lo, keys, wv, emit);
-  __syncthreads();
-  phase3_output<G::TPB, PackedKey>(a, tile, tile_lo, keys, emit, G::NSW, warp_sums, &bcast);
+  const int t = threadIdx.x;
+  int64_t pend = -1;           // previous super-tile awaiting output
+  uint32_t pend_excl = 0, pend_total = 0;
+  int cur = 0;
+  while (true) {
+    if (t == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+    for (int u = t; u < NSWT + 2; u += G::TPB) emit[cur][u] = 0;
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    if (tile >= a.ntiles) break;
+    const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
+    for (int sub = 0; sub < G::SUBS; ++sub) {
+      const int64_t tile_lo = super_lo + (int64_t)sub * G::TW;
+      if (tile_lo >= (int64_t)a.nwin) break;
+      const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + G::NS + a.k;  // bases touched
+      for (int u = t; u < G::NSW + 3; u += G::TPB) wvb[u] = 0;
+      const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi);  // (also the barrier for wvb)
+      const int64_t q0 = tile_lo - 1 + (int64_t)t * G::Q;
+      if (a.raw) {
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, true>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, true>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+      } else {
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, false>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, false>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+      }
+      __syncthreads();
+      // window ranges relative to the sub-tile
+      const int vlo = (int)max((int64_t)-1, -tile_lo);
+      const int vhi = (int)min((int64_t)G::TW, (int64_t)a.nwin - tile_lo);
+      // emitting windows: [win_lo, win_hi) and [0, vhi), clamped into [0, TW] with elo <= ehi
+      const int64_t wl = min(max((int64_t)a.win_lo - tile_lo, (int64_t)0), (int64_t)G::TW);
+      const int64_t wh = min((int64_t)min(a.win_hi, (uint64_t)INT64_MAX) - tile_lo, (int64_t)vhi);
+      const int elo = (int)wl, ehi = (int)max(wh, wl);
+      // vlo may be -1: the window before the sub-tile exists and feeds the change rule
+      const int jb = t * G::R;
+      const bool full = clean && vlo <= jb - 1 && jb + G::R <= vhi && elo <= jb && jb + G::R <= ehi;
+      uint32_t* em = emit[cur] + sub * G::NSW;
+      if (full) fast_phase2<W, false, true>(keys, wvb, vlo, vhi, elo, ehi, em);
+      else if (clean) fast_phase2<W, false, false>(keys, wvb, vlo, vhi, elo, ehi, em);
+      else fast_phase2<W, true, false>(keys, wvb, vlo, vhi, elo, ehi, em);
+      __syncthreads();
+    }
+    // count this super-tile's records and publish the count right away
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int uu = 0; uu < WPT; ++uu) {
+      const int u = t * WPT + uu;
+      if (u < NSWT) cnt += __popc(emit[cur][u]);
+    }
+    uint64_t total;
+    const uint32_t excl = (uint32_t)block_exclusive_sum<G::TPB, uint64_t>(cnt, warp_sums, &total);
+    if (t == 0) lookback_publish(a.status, tile, total);
+    if (pend >= 0)
+      fast_output<W, H64, KK>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
+                              reinterpret_cast<uint16_t*>(keys), &bcast);
+    pend = (int64_t)tile;
+    pend_excl = excl;
+    pend_total = (uint32_t)total;
+    cur ^= 1;
+  }
+  if (pend >= 0)
+    fast_output<W, H64, KK>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
+                            reinterpret_cast<uint16_t*>(keys), &bcast);
 }
 
 // ------------------------------------------------------------------ generic path kernel
 constexpr int kGenTPB = 256;
 constexpr int kGenE = 16;                 // slots per thread
-constexpr int kGenNS = kGenTPB * kGenE;   // 4096 slots per tile
+constexpr int kGenNS = kGenTPB * kGenE;   // 4096 slots per sub-tile
+constexpr int kGenSubs = 4;
 
 template <class Key, bool H64>
 __global__ void __launch_bounds__(kGenTPB) mz_generic_kernel(MzArgs a) {
@@ -407,70 +571,83 @@ __global__ void __launch_bounds__(kGenTPB) mz_generic_kernel(MzArgs a) {
   Key* keys = reinterpret_cast<Key*>(smem_raw);
   Key* sP = keys + kGenNS;
   Key* sS = sP + kGenNS;
-  __shared__ uint32_t emit[NSW];
-  __shared__ uint8_t wv[kGenNS];
+  __shared__ uint32_t emit[kGenSubs * NSW];
+  __shared__ uint32_t wvb[NSW + 3];
   __shared__ uint64_t warp_sums[kGenTPB / 32];
   __shared__ uint64_t bcast;
   __shared__ uint32_t s_tile;
   __shared__ SegScratch<Op, kGenTPB> sh;
   if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_counter, 1u);
-  for (int u = threadIdx.x; u < NSW; u += kGenTPB) emit[u] = 0;
+  for (int u = threadIdx.x; u < kGenSubs * NSW; u += kGenTPB) emit[u] = 0;
   __syncthreads();
   const uint64_t tile = s_tile;
   const uint32_t W = (uint32_t)a.w;
-  const int64_t tile_lo = (int64_t)tile * a.tw;
-  const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + kGenNS + a.k;
-  const bool clean = tile_is_clean<kGenTPB>(a, b_lo, b_hi);
+  const int64_t super_lo = (int64_t)tile * kGenSubs * a.tw;
+  int nsub = 0;
   const int t = threadIdx.x;
-  if (clean) phase1_keys<Key, kGenE, H64, false>(a, tile_lo - 1 + (int64_t)t * kGenE, t * kGenE, keys, wv);
-  else phase1_keys<Key, kGenE, H64, true>(a, tile_lo - 1 + (int64_t)t * kGenE, t * kGenE, keys, wv);
-  __syncthreads();
-  // phase 2: block S/P over slots, blocks of W starting at slot 1 (slot s <-> k-mer tile_lo-1+s)
-  {
-    Key v[kGenE], P[kGenE], S[kGenE];
-#pragma unroll
-    for (int j = 0; j < kGenE; ++j) v[j] = keys[t * kGenE + j];
-    block_prefix_suffix<Op, kGenTPB, kGenE>(v, P, S, W, 1u, sh);
-#pragma unroll
-    for (int j = 0; j < kGenE; ++j) {
-      sP[t * kGenE + j] = P[j];
-      sS[t * kGenE + j] = S[j];
+  for (int sub = 0; sub < kGenSubs; ++sub) {
+    const int64_t tile_lo = super_lo + (int64_t)sub * a.tw;
+    if (tile_lo >= (int64_t)a.nwin) break;
+    ++nsub;
+    const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + kGenNS + a.k;
+    for (int u = t; u < NSW + 3; u += kGenTPB) wvb[u] = 0;
+    const bool clean = tile_is_clean<kGenTPB>(a, b_lo, b_hi);
+    const int64_t q0 = tile_lo - 1 + (int64_t)t * kGenE;
+    if (a.raw) {
+      if (clean) phase1_keys<Key, kGenE, H64, false, 0, true>(a, q0, t * kGenE, keys, wvb);
+      else phase1_keys<Key, kGenE, H64, true, 0, true>(a, q0, t * kGenE, keys, wvb);
+    } else {
+      if (clean) phase1_keys<Key, kGenE, H64, false, 0, false>(a, q0, t * kGenE, keys, wvb);
+      else phase1_keys<Key, kGenE, H64, true, 0, false>(a, q0, t * kGenE, keys, wvb);
     }
-  }
-  __syncthreads();
-  {
-    // windows j in [0, tw): window j = slots j+1 .. j+W; thread t takes a contiguous range
-    const uint32_t per = (a.tw + kGenTPB - 1) / kGenTPB;
-    const int j0 = t * per;
-    const int j1 = min((int)a.tw, j0 + (int)per);
-    auto wmin = [&](int j) -> Key {
-      // j == -1 (window before the tile) spans slot 0 and the first W-1 slots of block 0
-      if (j < 0) return W == 1 ? keys[0] : kmin(keys[0], sP[W - 1]);
-      return (j % W == 0) ? sS[j + 1] : kmin(sS[j + 1], sP[j + W]);
-    };
-    auto valid_of = [&](int j) -> bool {
-      const int64_t i = tile_lo + j;
-      if (i < 0 || (uint64_t)i >= a.nwin) return false;
-      return clean ? true : (wv[j + W] != 0);
-    };
-    if (j0 < j1) {
-      Key yprev = wmin(j0 - 1);
-      bool vprev = valid_of(j0 - 1);
-      for (int j = j0; j < j1; ++j) {
-        const Key y = wmin(j);
-        const bool v = valid_of(j);
-        const int64_t i = tile_lo + j;
-        if (v && (!vprev || y != yprev) && (uint64_t)i >= a.win_lo && (uint64_t)i < a.win_hi) {
-          const uint32_t s = y.slot();
-          atomicOr(&emit[s >> 5], 1u << (s & 31));
-        }
-        vprev = v;
-        yprev = y;
+    __syncthreads();
+    // phase 2: block S/P over slots, blocks of W starting at slot 1 (slot s <-> k-mer tile_lo-1+s)
+    {
+      Key v[kGenE], P[kGenE], S[kGenE];
+#pragma unroll
+      for (int j = 0; j < kGenE; ++j) v[j] = keys[t * kGenE + j];
+      block_prefix_suffix<Op, kGenTPB, kGenE>(v, P, S, W, 1u, sh);
+#pragma unroll
+      for (int j = 0; j < kGenE; ++j) {
+        sP[t * kGenE + j] = P[j];
+        sS[t * kGenE + j] = S[j];
       }
     }
+    __syncthreads();
+    {
+      const uint32_t per = (a.tw + kGenTPB - 1) / kGenTPB;
+      const int j0 = t * per;
+      const int j1 = min((int)a.tw, j0 + (int)per);
+      auto wmin = [&](int j) -> Key {
+        if (j < 0) return W == 1 ? keys[0] : kmin(keys[0], sP[W - 1]);
+        return (j % W == 0) ? sS[j + 1] : kmin(sS[j + 1], sP[j + W]);
+      };
+      auto valid_of = [&](int j) -> bool {
+        const int64_t i = tile_lo + j;
+        if (i < 0 || (uint64_t)i >= a.nwin) return false;
+        return clean ? true : wv_bit(wvb, j + W);
+      };
+      uint32_t* em = emit + sub * NSW;
+      if (j0 < j1) {
+        Key yprev = wmin(j0 - 1);
+        bool vprev = valid_of(j0 - 1);
+        for (int j = j0; j < j1; ++j) {
+          const Key y = wmin(j);
+          const bool v = valid_of(j);
+          const int64_t i = tile_lo + j;
+          if (v && (!vprev || y != yprev) && (uint64_t)i >= a.win_lo && (uint64_t)i < a.win_hi) {
+            const uint32_t s = y.slot();
+            atomicOr(&em[s >> 5], 1u << (s & 31));
+          }
+          vprev = v;
+          yprev = y;
+        }
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  phase3_output<kGenTPB, Key>(a, tile, tile_lo, keys, emit, NSW, warp_sums, &bcast);
+  phase3_output<kGenTPB, H64>(a, tile, super_lo, kGenNS, nsub, emit, reinterpret_cast<uint16_t*>(keys), warp_sums,
+                              &bcast);
 }
 
 // ------------------------------------------------------------------ host side
@@ -481,30 +658,40 @@ int launch_mz(MzArgs a, int path, cudaStream_t st) {
   // 0 = auto, 1 = force generic
   const bool fast = path == 0 && packed_ok && w >= 1 && w <= 16;
   if (fast) {
-#define MZS_FAST(WW)                                                                                   \
-  case WW: {                                                                                           \
+#define MZS_FAST_KK(WW, KKV, H64V)                                                                     \
+  {                                                                                                    \
     using G = FastGeom<WW>;                                                                            \
     a.tw = G::TW;                                                                                      \
-    a.ntiles = (a.nwin + G::TW - 1) / G::TW;                                                           \
+    a.ntiles = (a.nwin + (uint64_t)G::TW * G::SUBS - 1) / ((uint64_t)G::TW * G::SUBS);                 \
     const size_t smem = sizeof(PackedKey) * G::NS;                                                     \
-    auto kern = h64 ? mz_fast_kernel<WW, true> : mz_fast_kernel<WW, false>;                            \
+    auto kern = mz_fast_kernel<WW, H64V, KKV>;                                                         \
     MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
     MZS_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), st));                                \
     MZS_CUDA(cudaMemsetAsync(a.status, 0, sizeof(uint64_t) * a.ntiles, st));                           \
-    kern<<<(unsigned)a.ntiles, G::TPB, smem, st>>>(a);                                                 \
+    int occ = 0;                                                                                       \
+    MZS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::TPB, smem));                 \
+    const uint64_t grid = std::min<uint64_t>(a.ntiles, (uint64_t)num_sms() * (uint64_t)std::max(occ, 1)); \
+    kern<<<(unsigned)grid, G::TPB, smem, st>>>(a);                                                     \
     MZS_LAUNCHED();                                                                                    \
     return SLSUM_OK;                                                                                   \
   }
+#define MZS_FAST(WW)                                                                                   \
+  case WW:                                                                                             \
+    if (h64) MZS_FAST_KK(WW, 0, true) else MZS_FAST_KK(WW, 0, false)
+    // compile-time k for the configurations the paper and BASELINE measure
+    if (w == 10 && k == 19) MZS_FAST_KK(10, 19, true)
+    if (w == 10 && k == 15) MZS_FAST_KK(10, 15, false)
     switch (w) {
       MZS_FAST(1) MZS_FAST(2) MZS_FAST(3) MZS_FAST(4) MZS_FAST(5) MZS_FAST(6) MZS_FAST(7) MZS_FAST(8)
       MZS_FAST(9) MZS_FAST(10) MZS_FAST(11) MZS_FAST(12) MZS_FAST(13) MZS_FAST(14) MZS_FAST(15) MZS_FAST(16)
       default: break;
     }
 #undef MZS_FAST
+#undef MZS_FAST_KK
   }
   if (w > 1024) return SLSUM_EUNSUPPORTED;
   a.tw = (uint32_t)(kGenNS - w - 1);
-  a.ntiles = (a.nwin + a.tw - 1) / a.tw;
+  a.ntiles = (a.nwin + (uint64_t)a.tw * kGenSubs - 1) / ((uint64_t)a.tw * kGenSubs);
   MZS_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), st));
   MZS_CUDA(cudaMemsetAsync(a.status, 0, sizeof(uint64_t) * a.ntiles, st));
   if (packed_ok) {
