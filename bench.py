@@ -32,12 +32,16 @@ sys.path.insert(0, ROOT)
 K_MER, W_WIN, BITS = 19, 10, 24
 # algorithmic bytes per unit
 SEEDTABLE_BYTES_PER_REC = 8 + 12 + 12   # histogram reads 8 B, the scatter reads 12 B and writes 12 B
+# algorithmic 32-bit integer operations per base of the fused minimizer kernel
+# (k=19, w=10): roll 3 + H_38 28 + key 2 + three 64-bit minima 12 + change/emit 3
+MZ_INT_OPS_PER_BASE = {19: 48, 15: 30}
+SM_COUNT, INT32_LANES_PER_SM_CLK = 148, 128   # 4 SMSPs x 32 lanes issue (B200_PROFILING / B300_MICROARCH)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c3", "c1"])
@@ -67,7 +71,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -223,7 +227,8 @@ def main():
             ev["table"].append((e[2], e[3]))
         return res
 
-    launches_per_step = 1 + 1 + (6 if world == 1 else 1 + 6 + 5)  # encode, mz, table kernels
+    # encode + mz + 3 x (upsweep, chunk scan, digit scan, downsweep) + 4 pointer-table kernels
+    launches_per_step = 1 + 1 + (12 + 4 if world == 1 else 1 + 4 + 12 + 4)
 
     def barrier():
         if world > 1:
@@ -291,19 +296,31 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
         del host_in, host_off, host_pos, seq2
 
-    # ---------------- roofline of the dominant kernel group (algorithmic bytes / event time)
+    # ---------------- rooflines (algorithmic work / event time of the launches)
     m_rec = m_local
     per_phase_bytes = {
         "encode": n * (1 + 0.25 + 0.125),
         "extract": n * (0.25 + 0.125) + m_rec * 16,
         "table": m_rec * SEEDTABLE_BYTES_PER_REC + 8 * ((1 << bits) + 1),
     }
-    dom = max(phase_ms, key=phase_ms.get)
-    achieved = per_phase_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-            "phase_ms": phase_ms, "phase_frac_hbm": {kk: per_phase_bytes[kk] / (phase_ms[kk] * 1e-3) / 1e9 / hbm_peak
-                                                     for kk in phase_ms}}
+    clk = clk_sum = clk.summary()
+    sm_mhz = clk.get("sm_mhz") or sm_max
+    int_peak = SM_COUNT * INT32_LANES_PER_SM_CLK * sm_mhz * 1e6 / 1e12          # T int32 ops/s
+    ops = MZ_INT_OPS_PER_BASE.get(k, 48) * n
+    ach = ops / (phase_ms["extract"] * 1e-3) / 1e12
+    roof = {"bound": "alu", "kernel": "mz_fast_kernel (a2-a7 fused, one launch per step)",
+            "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": None,
+            "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
+            "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"]}
+    tab_ach = per_phase_bytes["table"] / (phase_ms["table"] * 1e-3) / 1e9
+    roof_table = {"bound": "hbm", "kernel": "seed table (3 LSD radix passes + pointer table)",
+                  "achieved": tab_ach, "peak": hbm_peak, "unit": "GB/s", "frac": tab_ach / hbm_peak,
+                  "peak_kind": peak_kind, "ms": phase_ms["table"]}
+    step_bytes = sum(per_phase_bytes.values())
+    step_hbm = {"achieved": step_bytes / (ms_step * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
+                "phase_ms": phase_ms,
+                "phase_frac": {kk: per_phase_bytes[kk] / (phase_ms[kk] * 1e-3) / 1e9 / hbm_peak for kk in phase_ms}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -322,10 +339,12 @@ def main():
                        "density": m_rec / max(1, nwin_local) if world == 1 else None,
                        "l2": "inputs (3.1 GB) >> L2 (126 MB); no flush needed", "parallelism": f"shards{world}"},
             "roofline": roof,
+            "roofline_table": roof_table,
+            "hbm_step": step_hbm,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
-            "clocks": clk.summary(),
+            "clocks": clk_sum,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -2,25 +2,25 @@
 // for hashed minimizers, bucketed on the top `bits` bits of the 2k-bit key (R21).
 //
 // The build is a bucket histogram + a STABLE scatter into bucket order.  The scatter is
-// done as an LSD radix sort on the bucket bits with 8-bit digits (one pass per digit):
-// every pass ranks a tile of 4096 entries per digit with warp match_any (stable), gets the
-// tile's per-digit global offset from a per-digit decoupled look-back over tiles, and
-// scatters.  Stability makes the positions inside a bucket ascending (the input minimizer
+// done as an LSD radix sort on the bucket bits with 8-bit digits (one pass per digit,
+// reduce-then-scan: per-chunk digit counts, a scan over chunks, then a stable ranked
+// scatter; see the pass kernels below).  Stability makes the positions inside a bucket ascending (the input minimizer
 // list is ascending by position), for any bucket-size distribution.  The pointer table
 // is then read off the sorted fingerprints (first index of every bucket).
 //
 // Multi-GPU phases: count (histogram for the all-reduce), partition (one stable pass on
 // the owner digit), finalize (stable passes on the remaining bucket bits of the owner).
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace mzs {
 namespace {
 
 constexpr int kTPB = 256;
-constexpr int kIPT = 16;                     // items per thread per pass
-constexpr int kTile = kTPB * kIPT;           // 4096 entries per tile
 constexpr int kNW = kTPB / 32;
 
 __device__ __forceinline__ uint32_t fingerprint(uint64_t key, int k) {
@@ -30,147 +30,398 @@ __device__ __forceinline__ uint32_t fingerprint(uint64_t key, int k) {
 
 __device__ __forceinline__ uint64_t count_of(const uint64_t* d_m, uint64_t m) { return d_m ? *d_m : m; }
 
-// ---------------------------------------------------------------- digit histograms
-// hist[p*256 + d] += number of entries whose pass-p digit is d
-template <bool FROM_HASH>
-__global__ void __launch_bounds__(kTPB) hist_kernel(const void* keys, const uint64_t* d_m, uint64_t m_cap, int k,
-                                                    int lo_bit, int hi_bit, unsigned long long* hist) {
-  __shared__ uint32_t h[4][256];
-  for (int i = threadIdx.x; i < 4 * 256; i += kTPB) (&h[0][0])[i] = 0;
+// min(*d_m, m_cap), read ONCE per block (a per-thread read of one word from every SM is an
+// L2 hot spot).  Must be called by all threads of the block.
+__device__ __forceinline__ uint64_t block_count(const uint64_t* d_m, uint64_t m_cap) {
+  __shared__ uint64_t s_m;
+  if (threadIdx.x == 0) s_m = min(count_of(d_m, m_cap), m_cap);
   __syncthreads();
-  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
-  const int npass = (hi_bit - lo_bit + 7) / 8;
-  for (uint64_t i = (uint64_t)blockIdx.x * kTPB + threadIdx.x; i < m; i += (uint64_t)gridDim.x * kTPB) {
-    const uint32_t f = FROM_HASH ? fingerprint(static_cast<const uint64_t*>(keys)[i], k)
-                                 : static_cast<const uint32_t*>(keys)[i];
-    for (int p = 0; p < npass; ++p) {
-      const int sh = lo_bit + 8 * p;
-      const int nb = min(8, hi_bit - sh);
-      atomicAdd(&h[p][(f >> sh) & ((1u << nb) - 1u)], 1u);
-    }
+  return s_m;
+}
+
+// ---------------------------------------------------------------- stable LSD radix pass
+// Reduce-then-scan (no serial look-back chains): the m entries are cut into chunks of
+// kChunk; (U) counts per (digit, chunk); (S) exclusive scan over chunks per digit, then
+// over digits; (D) every chunk re-reads its entries sub-tile by sub-tile, ranks them
+// stably (ballot multi-split + per-warp counters), stages them in digit order in shared
+// memory and writes each digit run contiguously.
+constexpr int kDTPB = 512;                  // downsweep threads per CTA (16 warps, 1 CTA per SM)
+constexpr int kDNW = kDTPB / 32;
+constexpr int kDIPT = 8;                    // downsweep items per thread per sub-tile
+constexpr int kDTile = kDTPB * kDIPT;       // 4096 entries per downsweep sub-tile
+constexpr int kStages = 2;                  // TMA ring depth (sub-tiles in flight per CTA)
+constexpr int kGrp = 8;                     // write granularity: 8 entries = 32 B fp, 64 B pos
+constexpr int kChunk = 131072;              // entries per chunk
+constexpr int kSubs = kChunk / kDTile;      // 32 sub-tiles per chunk
+
+// Peers of this lane's digit d within the warp (lanes with the same d; d == 256 for
+// invalid lanes), by a bitwise ballot multi-split: nbits+1 ballots, no match.any.
+__device__ __forceinline__ unsigned warp_peers(uint32_t d, int nbits) {
+  unsigned peers = 0xffffffffu;
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const unsigned m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  const bool inv = d >= 256u;
+  const unsigned mi = __ballot_sync(0xffffffffu, inv);
+  return peers & (inv ? mi : ~mi);
+}
+
+template <bool FROM_HASH>
+__device__ __forceinline__ uint32_t load_fp(const void* keys, uint64_t i, int k) {
+  return FROM_HASH ? fingerprint(static_cast<const uint64_t*>(keys)[i], k) : static_cast<const uint32_t*>(keys)[i];
+}
+
+template <bool FROM_HASH>
+__global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const uint64_t* d_m, uint64_t m_cap, int k,
+                                                       int shift, int dbits, uint32_t* counts, uint64_t nchunks) {
+  __shared__ uint32_t h[kNW][256];
+  const unsigned lane = lane_id(), wid = warp_id();
+  for (int i = lane; i < 256; i += 32) h[wid][i] = 0;
+  __syncthreads();
+  const uint64_t m = block_count(d_m, m_cap);
+  const uint64_t c = blockIdx.x;
+  const uint64_t base = c * (uint64_t)kChunk;
+  const uint64_t end = min(m, base + kChunk);
+  const uint32_t dmask = (1u << dbits) - 1u;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t i = base + threadIdx.x; i < end; i += kTPB)
+    atomicAdd(&h[wid][(load_fp<FROM_HASH>(keys, i, k) >> shift) & dmask], 1u);
+  (void)lt;
+  __syncthreads();
+  const uint32_t d = threadIdx.x;
+  uint32_t t = 0;
+#pragma unroll
+  for (int w = 0; w < kNW; ++w) t += h[w][d];
+  counts[(uint64_t)d * nchunks + c] = t;
+}
+
+// block d: offsets[d][c] = exclusive scan over chunks; totals[d] = digit total
+__global__ void __launch_bounds__(kTPB) chunk_scan_kernel(const uint32_t* counts, uint64_t nchunks,
+                                                          uint64_t* offsets, unsigned long long* totals) {
+  __shared__ unsigned long long ws[kNW];
+  const uint64_t d = blockIdx.x;
+  const uint32_t* cn = counts + d * nchunks;
+  uint64_t* of = offsets + d * nchunks;
+  const uint64_t per = (nchunks + kTPB - 1) / kTPB;
+  const uint64_t c0 = threadIdx.x * per, c1 = min(nchunks, c0 + per);
+  unsigned long long s = 0;
+  for (uint64_t c = c0; c < c1; ++c) s += cn[c];
+  unsigned long long tot;
+  unsigned long long ex = block_exclusive_sum<kTPB, unsigned long long>(s, ws, &tot);
+  for (uint64_t c = c0; c < c1; ++c) {
+    of[c] = ex;
+    ex += cn[c];
+  }
+  if (threadIdx.x == 0) totals[d] = tot;
+}
+
+// exclusive scan of the 256 digit totals (one block of 256 threads)
+__global__ void digit_scan_kernel(const unsigned long long* totals, unsigned long long* base) {
+  __shared__ unsigned long long ws[kNW];
+  unsigned long long tot;
+  base[threadIdx.x] = block_exclusive_sum<256, unsigned long long>(totals[threadIdx.x], ws, &tot);
+}
+
+// Shared memory of one downsweep CTA: two input buffers filled by TMA bulk copies (the
+// next sub-tile streams in while the current one is ranked and scattered); the current
+// buffer is then reused in place as the digit-sorted staging area for coalesced writes.
+template <bool FROM_HASH>
+struct DownSmem {
+  using KT = typename std::conditional<FROM_HASH, uint64_t, uint32_t>::type;
+  KT kin[kStages][kDTile];
+  uint64_t pin[kStages][kDTile];
+  uint64_t mbar[kStages];
+  uint32_t cfp[256][kGrp];   // carried run tails, slot = global index & 7
+  uint64_t cpos[256][kGrp];
+  uint64_t run_off[256];     // next global index of digit d
+  uint64_t carry_lo[256];    // digit d's carried entries are [carry_lo, run_off)
+  uint64_t wlim[256];        // this sub-tile writes digit d's indices < wlim (8-aligned)
+  uint64_t gbase[256];       // run_off[d] - dstart[d]: staged entry j of digit d goes to gbase + j
+  uint16_t wcnt[kDNW][256];
+  uint16_t dstart[256];
+  uint16_t tcount[256];
+  unsigned long long ws2[kDNW];
+};
+
+// One chunk per CTA, streamed through a TMA ring of sub-tiles.  Per sub-tile: stable rank
+// by digit (ballot multi-split), stage in digit order (in place), then write every digit's
+// run in whole 8-entry groups; the ragged tail of each run is carried in shared memory to
+// the next sub-tile, so DRAM sees full sectors except at the chunk's edges.
+template <bool FROM_HASH, bool MATCH>
+__global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in, const uint64_t* __restrict__ pos_in,
+                                                         uint32_t* __restrict__ fp_out, uint64_t* __restrict__ pos_out,
+                                                         const uint64_t* d_m, uint64_t m_cap, int k, int shift,
+                                                         int dbits, const uint64_t* __restrict__ offsets,
+                                                         const unsigned long long* __restrict__ dbase,
+                                                         uint64_t nchunks) {
+  using SM = DownSmem<FROM_HASH>;
+  using KT = typename SM::KT;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(smem_raw);
+  const unsigned lane = lane_id(), wid = warp_id();
+  const uint64_t c = blockIdx.x;
+  const uint64_t m = block_count(d_m, m_cap);
+  const uint32_t dmask = (1u << dbits) - 1u;
+  const unsigned lt = (1u << lane) - 1u;
+  const KT* kg = static_cast<const KT*>(keys_in);
+  const uint32_t td = threadIdx.x;  // digit owned by this thread when td < 256
+  if (td < 256) {
+    const uint64_t r = dbase[td] + offsets[(uint64_t)td * nchunks + c];
+    S.run_off[td] = r;
+    S.carry_lo[td] = r;
+  }
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
+    fence_mbar_init();
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < npass * 256; i += kTPB) {
-    const uint32_t v = (&h[0][0])[i];
-    if (v) atomicAdd(&hist[i], (unsigned long long)v);
+  const uint64_t cbase = c * (uint64_t)kChunk;
+  const int nsubs = (int)min((uint64_t)kSubs, (m - min(m, cbase) + kDTile - 1) / kDTile);
+  auto full = [&](int sub) { return cbase + (uint64_t)(sub + 1) * kDTile <= m; };
+  auto issue = [&](int sub) {
+    if (threadIdx.x == 0 && sub < nsubs && full(sub)) {
+      const int b = sub % kStages;
+      const uint64_t base = cbase + (uint64_t)sub * kDTile;
+      mbar_arrive_expect_tx(&S.mbar[b], kDTile * (uint32_t)(sizeof(KT) + sizeof(uint64_t)));
+      bulk_g2s(S.kin[b], kg + base, kDTile * sizeof(KT), &S.mbar[b]);
+      bulk_g2s(S.pin[b], pos_in + base, kDTile * sizeof(uint64_t), &S.mbar[b]);
+    }
+  };
+  for (int p = 0; p < kStages - 1; ++p) issue(p);
+  uint32_t parity = 0;
+  for (int sub = 0; sub < nsubs; ++sub) {
+    const int b = sub % kStages;
+    const uint64_t base = cbase + (uint64_t)sub * kDTile;
+    issue(sub + kStages - 1);
+    if (full(sub)) {
+      mbar_wait(&S.mbar[b], (parity >> b) & 1u);
+      parity ^= 1u << b;
+    } else {
+      for (uint32_t j = threadIdx.x; j < kDTile; j += kDTPB) {
+        const bool v = base + j < m;
+        S.kin[b][j] = v ? kg[base + j] : (KT)0;
+        S.pin[b][j] = v ? pos_in[base + j] : 0ull;
+      }
+      __syncthreads();
+    }
+    for (int i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;
+    __syncwarp();
+    uint32_t key[kDIPT], rank[kDIPT];
+    uint64_t pos[kDIPT];
+#pragma unroll
+    for (int it = 0; it < kDIPT; ++it) {
+      const uint32_t j = wid * (kDIPT * 32) + it * 32 + lane;
+      const bool valid = base + j < m;
+      const KT kv = S.kin[b][j];
+      const uint32_t f = FROM_HASH ? fingerprint((uint64_t)kv, k) : (uint32_t)kv;
+      const uint32_t d = valid ? ((f >> shift) & dmask) : 256u;
+      const unsigned peers = MATCH ? __match_any_sync(0xffffffffu, d) : warp_peers(d, dbits);
+      const uint32_t before = __popc(peers & lt);
+      const uint32_t cc = (d < 256u) ? S.wcnt[wid][d] : 0u;
+      __syncwarp();
+      if (d < 256u && before == 0) S.wcnt[wid][d] = (uint16_t)(cc + __popc(peers));
+      __syncwarp();
+      key[it] = f;
+      pos[it] = S.pin[b][j];
+      rank[it] = (d < 256u) ? cc + before : 0xffffffffu;
+    }
+    __syncthreads();
+    uint32_t run = 0;
+    if (td < 256) {
+#pragma unroll
+      for (int w = 0; w < kDNW; ++w) {
+        const uint32_t cc = S.wcnt[w][td];
+        S.wcnt[w][td] = (uint16_t)run;
+        run += cc;
+      }
+      S.tcount[td] = (uint16_t)run;
+    }
+    {
+      unsigned long long tot;
+      // digits are owned by threads 0..255 (the first 8 warps); the scan runs over them
+      const unsigned long long ex = block_exclusive_sum<kDTPB, unsigned long long>(td < 256 ? run : 0u, S.ws2, &tot);
+      if (td < 256) {
+        S.dstart[td] = (uint16_t)ex;
+        // this sub-tile writes [carry_lo, floor8(run_off + count)); flush the carried part now
+        const uint64_t r0 = S.run_off[td], r1 = r0 + run, g0 = S.carry_lo[td];
+        const uint64_t lim = r1 & ~(uint64_t)(kGrp - 1);
+        S.wlim[td] = lim;
+        S.gbase[td] = r0 - ex;
+        for (uint64_t g = g0; g < min(r0, lim); ++g) {
+          fp_out[g] = S.cfp[td][g & (kGrp - 1)];
+          pos_out[g] = S.cpos[td][g & (kGrp - 1)];
+        }
+      }
+    }
+    __syncthreads();
+    // stage in digit order, in place in ring slot b (fingerprints as u32)
+    uint32_t* sk = reinterpret_cast<uint32_t*>(S.kin[b]);
+#pragma unroll
+    for (int it = 0; it < kDIPT; ++it) {
+      if (rank[it] != 0xffffffffu) {
+        const uint32_t d = (key[it] >> shift) & dmask;
+        const uint32_t j = S.dstart[d] + S.wcnt[wid][d] + rank[it];
+        sk[j] = key[it];
+        S.pin[b][j] = pos[it];
+      }
+    }
+    __syncthreads();
+    const uint32_t nsub = (uint32_t)min((uint64_t)kDTile, m - base);
+    for (uint32_t j = threadIdx.x; j < nsub; j += kDTPB) {
+      const uint32_t f = sk[j];
+      const uint32_t d = (f >> shift) & dmask;
+      const uint64_t g = S.gbase[d] + j;
+      const uint64_t p = S.pin[b][j];
+      if (g < S.wlim[d]) {
+        fp_out[g] = f;
+        pos_out[g] = p;
+      } else {
+        S.cfp[d][g & (kGrp - 1)] = f;
+        S.cpos[d][g & (kGrp - 1)] = p;
+      }
+    }
+    fence_proxy_async();  // ring slot b is refilled by TMA in a later iteration
+    __syncthreads();
+    if (td < 256) {
+      S.carry_lo[td] = max(S.carry_lo[td], S.wlim[td]);
+      S.run_off[td] += S.tcount[td];
+    }
+    __syncthreads();
+  }
+  // flush the carried tails
+  if (td < 256) {
+    for (uint64_t g = S.carry_lo[td]; g < S.run_off[td]; ++g) {
+      fp_out[g] = S.cfp[td][g & (kGrp - 1)];
+      pos_out[g] = S.cpos[td][g & (kGrp - 1)];
+    }
   }
 }
 
-// exclusive scan of each pass's 256 bins (one block of 256 threads)
-__global__ void digit_scan_kernel(const unsigned long long* hist, unsigned long long* base, int npass) {
-  __shared__ unsigned long long ws[kNW];
-  for (int p = 0; p < npass; ++p) {
-    unsigned long long tot;
-    const unsigned long long v = hist[p * 256 + threadIdx.x];
-    const unsigned long long ex = block_exclusive_sum<256, unsigned long long>(v, ws, &tot);
-    base[p * 256 + threadIdx.x] = ex;
+// Pointer table from the bucket-sorted fingerprints, in three data-parallel steps (bucket
+// sizes are very uneven: minimizer hashes are window minima, so high buckets are mostly
+// empty and a "fill every empty bucket you see" loop serialises on a few threads):
+//   1. offsets[*] = UINT64_MAX (memset); offsets[nb] = m
+//   2. boundary scatter: offsets[bucket(i)] = i wherever bucket(i) != bucket(i-1)
+//   3. suffix minimum over offsets[0..nb]: an empty bucket takes the start of the next
+//      non-empty one.
+// bucket(f) = (f >> shift) & bmask.
+__global__ void __launch_bounds__(kTPB) offsets_scatter_kernel(const uint32_t* __restrict__ fp, const uint64_t* d_m,
+                                                               uint64_t m_cap, int shift, uint32_t bmask, uint64_t nb,
+                                                               uint64_t* __restrict__ offsets) {
+  const uint64_t m = block_count(d_m, m_cap);
+  const bool aligned = (reinterpret_cast<uintptr_t>(fp) & 15) == 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) offsets[nb] = m;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t * 16 < m;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i0 = t * 16;
+    uint32_t prev = i0 == 0 ? 0xffffffffu : ((fp[i0 - 1] >> shift) & bmask);
+    uint32_t f[16];
+    if (aligned && i0 + 16 <= m) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(fp + i0 + 4 * q);
+        f[4 * q] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) f[j] = i0 + j < m ? fp[i0 + j] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (i0 + j >= m) break;
+      const uint32_t cur = (f[j] >> shift) & bmask;
+      if (cur != prev) offsets[cur] = i0 + j;
+      prev = cur;
+    }
+  }
+}
+
+constexpr int kSminTile = kTPB * 16;  // 4096 entries per suffix-min tile
+
+// per-tile minimum of offsets[] (tile t covers [t*4096, (t+1)*4096) of [0, n))
+__global__ void __launch_bounds__(kTPB) smin_reduce_kernel(const uint64_t* __restrict__ v, uint64_t n,
+                                                           uint64_t* __restrict__ tile_min) {
+  __shared__ uint64_t ws[kNW];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kSminTile;
+  uint64_t mn = ~0ull;
+  for (uint64_t i = b0 + threadIdx.x; i < min(n, b0 + (uint64_t)kSminTile); i += kTPB) mn = min(mn, v[i]);
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, mn, o));
+  if (lane_id() == 0) ws[warp_id()] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t r = ~0ull;
+    for (int w = 0; w < kNW; ++w) r = min(r, ws[w]);
+    tile_min[blockIdx.x] = r;
+  }
+}
+
+// suffix minimum of the per-tile minima (one block; a few thousand tiles): tile_min[t] <-
+// min over tiles > t (the carry entering tile t from the right)
+__global__ void __launch_bounds__(kTPB) smin_tiles_kernel(uint64_t* tile_min, uint64_t ntiles) {
+  __shared__ uint64_t carry_s;
+  __shared__ uint64_t buf[kTPB];
+  if (threadIdx.x == 0) carry_s = ~0ull;
+  __syncthreads();
+  // process from the right in blocks of kTPB tiles
+  for (int64_t hi = (int64_t)ntiles; hi > 0; hi -= kTPB) {
+    const int64_t lo = max((int64_t)0, hi - kTPB);
+    const int64_t i = lo + threadIdx.x;
+    uint64_t x = i < hi ? tile_min[i] : ~0ull;
+    buf[threadIdx.x] = x;
+    __syncthreads();
+    // inclusive suffix min within the block (Hillis-Steele, right to left)
+    for (int o = 1; o < kTPB; o <<= 1) {
+      const uint64_t y = threadIdx.x + o < kTPB ? buf[threadIdx.x + o] : ~0ull;
+      __syncthreads();
+      buf[threadIdx.x] = min(buf[threadIdx.x], y);
+      __syncthreads();
+    }
+    const uint64_t carry = carry_s;
+    const uint64_t excl = min((uint64_t)(threadIdx.x + 1 < kTPB ? buf[threadIdx.x + 1] : ~0ull), carry);
+    __syncthreads();
+    if (i < hi) tile_min[i] = excl;
+    if (threadIdx.x == 0) carry_s = min(carry, buf[0]);
     __syncthreads();
   }
 }
 
-// ---------------------------------------------------------------- one stable radix pass
-template <bool FROM_HASH>
-__global__ void __launch_bounds__(kTPB) radix_pass_kernel(const void* keys_in, const uint64_t* __restrict__ pos_in,
-                                                          uint32_t* __restrict__ fp_out, uint64_t* __restrict__ pos_out,
-                                                          const uint64_t* d_m, uint64_t m_cap, int k, int shift,
-                                                          int dbits, const unsigned long long* __restrict__ dbase,
-                                                          uint64_t* status, uint32_t* tile_counter) {
-  __shared__ uint32_t wcnt[kNW][256];
-  __shared__ uint64_t doff[256];
-  __shared__ uint32_t s_tile;
+// offsets[i] <- min(offsets[i..end of tile], carry of the tile): serial per thread chunk of 16,
+// then a right-to-left warp/block scan
+__global__ void __launch_bounds__(kTPB) smin_apply_kernel(uint64_t* __restrict__ v, uint64_t n,
+                                                          const uint64_t* __restrict__ tile_carry) {
+  __shared__ uint64_t ws[kNW];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kSminTile + (uint64_t)threadIdx.x * 16;
+  uint64_t x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = b0 + j < n ? v[b0 + j] : ~0ull;
+#pragma unroll
+  for (int j = 14; j >= 0; --j) x[j] = min(x[j], x[j + 1]);
+  // carry from threads to the right (their chunk minima), nearest first
+  uint64_t c = x[0];
   const unsigned lane = lane_id(), wid = warp_id();
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-  for (int i = lane; i < 256; i += 32) wcnt[wid][i] = 0;
+  uint64_t inc = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_down_sync(0xffffffffu, inc, o);
+    if (lane + o < 32) inc = min(inc, y);
+  }
+  uint64_t right = __shfl_down_sync(0xffffffffu, inc, 1);
+  if (lane == 31) right = ~0ull;
+  if (lane == 0) ws[wid] = inc;
   __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
-  const uint64_t base = tile * (uint64_t)kTile;
-  if (base >= m) return;  // no later tile has entries either
-  const uint32_t dmask = (1u << dbits) - 1u;
-  const unsigned lt = (1u << lane) - 1u;
-  uint32_t key[kIPT], rank[kIPT];
-  uint64_t pos[kIPT];
+  uint64_t wr = ~0ull;
+  for (int w = wid + 1; w < kNW; ++w) wr = min(wr, ws[w]);
+  const uint64_t carry = min(min(right, wr), tile_carry[blockIdx.x]);
 #pragma unroll
-  for (int it = 0; it < kIPT; ++it) {
-    const uint64_t idx = base + (uint64_t)wid * (kIPT * 32) + (uint64_t)it * 32 + lane;
-    const bool valid = idx < m;
-    uint32_t f = 0;
-    uint64_t p = 0;
-    if (valid) {
-      f = FROM_HASH ? fingerprint(static_cast<const uint64_t*>(keys_in)[idx], k)
-                    : static_cast<const uint32_t*>(keys_in)[idx];
-      p = pos_in[idx];
-    }
-    const uint32_t d = valid ? ((f >> shift) & dmask) : 256u;
-    const unsigned peers = __match_any_sync(0xffffffffu, d);
-    const uint32_t before = __popc(peers & lt);
-    const uint32_t c = (d < 256u) ? wcnt[wid][d] : 0u;
-    __syncwarp();
-    if (d < 256u && before == 0) wcnt[wid][d] = c + __popc(peers);
-    __syncwarp();
-    key[it] = f;
-    pos[it] = p;
-    rank[it] = (d < 256u) ? c + before : 0xffffffffu;
-  }
-  __syncthreads();
-  // per digit: exclusive prefix over warps, tile total, look-back over tiles
-  {
-    const uint32_t d = threadIdx.x;  // kTPB == 256 digits
-    uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-      const uint32_t c = wcnt[w][d];
-      wcnt[w][d] = run;
-      run += c;
-    }
-    uint64_t* st = status + d;
-    const uint64_t total = run;
-    uint64_t excl = 0;
-    if (tile == 0) {
-      st_volatile_u64(st, kLbInc | total);
-    } else {
-      st_volatile_u64(st + tile * 256, kLbAgg | total);
-      int64_t t = (int64_t)tile - 1;
-      while (t >= 0) {
-        uint64_t v;
-        do { v = ld_volatile_u64(st + (uint64_t)t * 256); } while ((v >> 62) == 0);
-        excl += v & kLbVal;
-        if ((v >> 62) == 2) break;
-        --t;
-      }
-      st_volatile_u64(st + tile * 256, kLbInc | (excl + total));
-    }
-    doff[d] = dbase[d] + excl;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < kIPT; ++it) {
-    if (rank[it] != 0xffffffffu) {
-      const uint32_t d = (key[it] >> shift) & dmask;
-      const uint64_t dst = doff[d] + wcnt[wid][d] + rank[it];
-      fp_out[dst] = key[it];
-      pos_out[dst] = pos[it];
-    }
-  }
-}
-
-// offsets[b] = first index whose bucket >= b (b in [0, nb]); fp sorted by bucket.
-// bucket(f) = (f >> shift) & bmask
-__global__ void offsets_kernel(const uint32_t* __restrict__ fp, const uint64_t* d_m, uint64_t m_cap, int shift,
-                               uint32_t bmask, uint64_t nb, uint64_t* __restrict__ offsets) {
-  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += stride) {
-    const int64_t prev = i == 0 ? -1 : (int64_t)((fp[i - 1] >> shift) & bmask);
-    const int64_t cur = i == m ? (int64_t)nb : (int64_t)((fp[i] >> shift) & bmask);
-    for (int64_t b = prev + 1; b <= cur; ++b) offsets[b] = i;
-  }
+  for (int j = 0; j < 16; ++j)
+    if (b0 + j < n) v[b0 + j] = min(x[j], carry);
 }
 
 // counts[bucket] += 1 (global atomics; the 2^bits counters stay L2-resident)
 __global__ void __launch_bounds__(kTPB) count_kernel(const uint64_t* __restrict__ hash, const uint64_t* d_m,
                                                      uint64_t m_cap, int k, int bits, uint32_t* counts) {
-  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
+  const uint64_t m = block_count(d_m, m_cap);
   for (uint64_t i = (uint64_t)blockIdx.x * kTPB + threadIdx.x; i < m; i += (uint64_t)gridDim.x * kTPB)
     atomicAdd(&counts[fingerprint(hash[i], k) >> (32 - bits)], 1u);
 }
@@ -199,7 +450,7 @@ __global__ void counts_scan_kernel(const uint32_t* counts, uint64_t b0, uint64_t
 __global__ void fp_copy_kernel(const uint64_t* __restrict__ hash, const uint64_t* __restrict__ pos, const uint64_t* d_m,
                                uint64_t m_cap, int k, uint32_t* __restrict__ fp, uint64_t* __restrict__ pos_out,
                                uint64_t* send_counts) {
-  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
+  const uint64_t m = block_count(d_m, m_cap);
   const uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i0 == 0) send_counts[0] = m;
   for (uint64_t i = i0; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -214,10 +465,10 @@ __global__ void u32_to_u64_kernel(const unsigned long long* in, uint64_t* out, i
 
 // ---------------------------------------------------------------- host helpers
 struct SortWs {
-  unsigned long long* hist;   // [npass*256]
-  unsigned long long* dbase;  // [npass*256]
-  uint32_t* counters;         // [npass]
-  uint64_t* status;           // [ntiles*256]
+  uint32_t* counts;           // [256 * nchunks]
+  uint64_t* offs;             // [256 * nchunks]
+  unsigned long long* totals; // [256]
+  unsigned long long* dbase;  // [256]
   uint32_t* fpA;
   uint64_t* posA;
   uint32_t* fpB;
@@ -225,14 +476,14 @@ struct SortWs {
   uint32_t* fpF;              // final fingerprints when the caller gave none
 };
 
-uint64_t tiles_for(uint64_t m) { return (m + kTile - 1) / kTile + 1; }
+uint64_t chunks_for(uint64_t m) { return (m + kChunk - 1) / kChunk + 1; }
 
 template <class C>
 void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
-  c.template take<unsigned long long>(4 * 256);
-  c.template take<unsigned long long>(4 * 256);
-  c.template take<uint32_t>(4);
-  c.template take<uint64_t>(tiles_for(m) * 256);
+  c.template take<uint32_t>(256 * chunks_for(m));
+  c.template take<uint64_t>(256 * chunks_for(m));
+  c.template take<unsigned long long>(256);
+  c.template take<unsigned long long>(256);
   if (npass >= 2) {
     c.template take<uint32_t>(m + 1);
     c.template take<uint64_t>(m + 1);
@@ -246,10 +497,10 @@ void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
 
 bool carve_sort_ws(Carve& c, uint64_t m, int npass, bool need_fp, SortWs& s) {
   s = SortWs{};
-  s.hist = c.take<unsigned long long>(4 * 256);
-  s.dbase = c.take<unsigned long long>(4 * 256);
-  s.counters = c.take<uint32_t>(4);
-  s.status = c.take<uint64_t>(tiles_for(m) * 256);
+  s.counts = c.take<uint32_t>(256 * chunks_for(m));
+  s.offs = c.take<uint64_t>(256 * chunks_for(m));
+  s.totals = c.take<unsigned long long>(256);
+  s.dbase = c.take<unsigned long long>(256);
   if (npass >= 2) { s.fpA = c.take<uint32_t>(m + 1); s.posA = c.take<uint64_t>(m + 1); }
   if (npass >= 3) { s.fpB = c.take<uint32_t>(m + 1); s.posB = c.take<uint64_t>(m + 1); }
   if (need_fp) s.fpF = c.take<uint32_t>(m + 1);
@@ -263,21 +514,22 @@ int grid_stride_blocks(uint64_t m) {
 }
 
 // Stable LSD sort of m entries by fp bits [lo_bit, hi_bit) into (fp_dst, pos_dst).
+// After the call s.totals holds the digit totals of the LAST pass.
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st) {
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
-  MZS_CUDA(cudaMemsetAsync(s.hist, 0, sizeof(unsigned long long) * 256 * npass, st));
-  MZS_CUDA(cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * npass, st));
-  const int hb = grid_stride_blocks(m);
-  if (from_hash)
-    hist_kernel<true><<<hb, kTPB, 0, st>>>(keys, d_m, m, k, lo_bit, hi_bit, s.hist);
-  else
-    hist_kernel<false><<<hb, kTPB, 0, st>>>(keys, d_m, m, k, lo_bit, hi_bit, s.hist);
-  MZS_LAUNCHED();
-  digit_scan_kernel<<<1, 256, 0, st>>>(s.hist, s.dbase, npass);
-  MZS_LAUNCHED();
-  const uint64_t ntiles = (m + kTile - 1) / kTile;
+  const uint64_t nch = (m + kChunk - 1) / kChunk;
+  if (nch == 0) return SLSUM_OK;
+  const size_t dsm1 = sizeof(DownSmem<true>), dsm0 = sizeof(DownSmem<false>);
+  static const bool use_match = [] {
+    const char* e = getenv("MZS_RADIX_MATCH");
+    return e && e[0] == '1';
+  }();
+  auto ds1 = use_match ? downsweep_kernel<true, true> : downsweep_kernel<true, false>;
+  auto ds0 = use_match ? downsweep_kernel<false, true> : downsweep_kernel<false, false>;
+  MZS_CUDA(cudaFuncSetAttribute(ds1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm1));
+  MZS_CUDA(cudaFuncSetAttribute(ds0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm0));
   const void* kin = keys;
   const uint64_t* pin = pos;
   bool kin_hash = from_hash;
@@ -289,16 +541,18 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     else { fo = s.fpB; po = s.posB; }
     const int sh = lo_bit + 8 * p;
     const int nb = std::min(8, hi_bit - sh);
-    MZS_CUDA(cudaMemsetAsync(s.status, 0, sizeof(uint64_t) * 256 * std::max<uint64_t>(ntiles, 1), st));
-    if (ntiles) {
-      if (kin_hash)
-        radix_pass_kernel<true><<<(unsigned)ntiles, kTPB, 0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb,
-                                                                   s.dbase + 256 * p, s.status, s.counters + p);
-      else
-        radix_pass_kernel<false><<<(unsigned)ntiles, kTPB, 0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb,
-                                                                    s.dbase + 256 * p, s.status, s.counters + p);
-      MZS_LAUNCHED();
-    }
+    if (kin_hash) upsweep_kernel<true><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch);
+    else upsweep_kernel<false><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch);
+    MZS_LAUNCHED();
+    chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals);
+    MZS_LAUNCHED();
+    digit_scan_kernel<<<1, 256, 0, st>>>(s.totals, s.dbase);
+    MZS_LAUNCHED();
+    if (kin_hash)
+      ds1<<<(unsigned)nch, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch);
+    else
+      ds0<<<(unsigned)nch, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch);
+    MZS_LAUNCHED();
     kin = fo;
     pin = po;
     kin_hash = false;
@@ -307,12 +561,22 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
 }
 
 int offsets_launch(const uint32_t* fp, const uint64_t* d_m, uint64_t m, int shift, uint32_t bmask, uint64_t nb,
-                   uint64_t* offsets, cudaStream_t st) {
-  const int blocks = grid_stride_blocks(m + 1);
-  offsets_kernel<<<blocks, kTPB, 0, st>>>(fp, d_m, m, shift, bmask, nb, offsets);
+                   uint64_t* offsets, uint64_t* tile_min, cudaStream_t st) {
+  MZS_CUDA(cudaMemsetAsync(offsets, 0xff, sizeof(uint64_t) * (nb + 1), st));
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((m / 16 + kTPB) / kTPB, (uint64_t)num_sms() * 8));
+  offsets_scatter_kernel<<<(unsigned)blocks, kTPB, 0, st>>>(fp, d_m, m, shift, bmask, nb, offsets);
+  MZS_LAUNCHED();
+  const uint64_t n = nb + 1, nt = (n + kSminTile - 1) / kSminTile;
+  smin_reduce_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min);
+  MZS_LAUNCHED();
+  smin_tiles_kernel<<<1, kTPB, 0, st>>>(tile_min, nt);
+  MZS_LAUNCHED();
+  smin_apply_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
+
+uint64_t smin_tiles_for(uint64_t nb) { return (nb + 1 + kSminTile - 1) / kSminTile + 1; }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
@@ -326,6 +590,7 @@ MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
   Sizer z;
   const int npass = (bucket_bits + 7) / 8;
   size_sort_ws(z, m, npass, true);
+  z.take<uint64_t>(smin_tiles_for(1ull << bucket_bits));
   return z.used;
 }
 
@@ -353,11 +618,13 @@ MZS_API int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t 
   const int npass = (bucket_bits + 7) / 8;
   SortWs s;
   if (!carve_sort_ws(c, m, npass, true, s)) return SLSUM_ENOMEM;
+  uint64_t* tile_min = c.take<uint64_t>(smin_tiles_for(nb));
+  if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
   int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st);
   if (rc) return rc;
-  return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, st);
+  return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st);
 }
 
 MZS_API int seedtable_count(const uint64_t* hash, uint64_t m, const uint64_t* d_m, int k, int bucket_bits,
@@ -411,7 +678,7 @@ MZS_API int seedtable_partition(const uint64_t* hash, const uint64_t* pos, uint6
   }
   int rc = stable_sort(true, hash, pos, d_m, m, k, 32 - g, 32, send_fp, send_pos, s, st);
   if (rc) return rc;
-  u32_to_u64_kernel<<<1, 256, 0, st>>>(s.hist, send_counts, nranks);
+  u32_to_u64_kernel<<<1, 256, 0, st>>>(s.totals, send_counts, nranks);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -420,6 +687,7 @@ MZS_API size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bi
   Sizer z;
   const int npass = std::max(1, (bucket_bits - log2i(nranks) + 7) / 8);
   size_sort_ws(z, m_recv, npass, true);
+  z.take<uint64_t>(smin_tiles_for(1ull << (bucket_bits - log2i(nranks))));
   return z.used;
 }
 
@@ -455,12 +723,14 @@ MZS_API int seedtable_finalize(const uint32_t* recv_fp, const uint64_t* recv_pos
   const int npass = std::max(1, (lbits + 7) / 8);
   SortWs s;
   if (!carve_sort_ws(c, m_recv, npass, true, s)) return SLSUM_ENOMEM;
+  uint64_t* tile_min = c.take<uint64_t>(smin_tiles_for(nbl));
+  if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
   const int hi = lbits > 0 ? 32 - g : lo + 1;  // lbits == 0: one bucket per owner; a 1-bit no-op pass
   int rc = stable_sort(false, recv_fp, recv_pos, nullptr, m_recv, 0, lo, hi, fp_final, pos_out, s, st);
   if (rc) return rc;
   if (!global_counts)
-    return offsets_launch(fp_final, nullptr, m_recv, lo, (uint32_t)(nbl - 1), nbl, offsets_local, st);
+    return offsets_launch(fp_final, nullptr, m_recv, lo, (uint32_t)(nbl - 1), nbl, offsets_local, tile_min, st);
   return SLSUM_OK;
 }
