@@ -227,8 +227,10 @@ def main():
             ev["table"].append((e[2], e[3]))
         return res
 
-    # encode + mz + 3 x (upsweep, chunk scan, digit scan, downsweep) + 4 pointer-table kernels
-    launches_per_step = 1 + 1 + (12 + 4 if world == 1 else 1 + 4 + 12 + 4)
+    # encode + mz + seed table: path-select kernel, 3 narrow passes x (upsweep, chunk scan, digit
+    # scan, downsweep), 3 wide passes (enqueued, gated off at entry), 4 pointer-table kernels
+    table_launches = 1 + 12 + 12 + 4
+    launches_per_step = 1 + 1 + (table_launches if world == 1 else 1 + (1 + 4 + 4) + (1 + 12 + 12 + 4))
 
     def barrier():
         if world > 1:
@@ -313,7 +315,7 @@ def main():
             "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
             "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"]}
     tab_ach = per_phase_bytes["table"] / (phase_ms["table"] * 1e-3) / 1e9
-    roof_table = {"bound": "hbm", "kernel": "seed table (3 LSD radix passes + pointer table)",
+    roof_table = {"bound": "hbm", "kernel": "seed table (3 packed-item LSD radix passes + pointer table)",
                   "achieved": tab_ach, "peak": hbm_peak, "unit": "GB/s", "frac": tab_ach / hbm_peak,
                   "peak_kind": peak_kind, "ms": phase_ms["table"]}
     step_bytes = sum(per_phase_bytes.values())

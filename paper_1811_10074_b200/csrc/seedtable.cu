@@ -68,14 +68,27 @@ __device__ __forceinline__ unsigned warp_peers(uint32_t d, int nbits) {
   return peers & (inv ? mi : ~mi);
 }
 
-template <bool FROM_HASH>
-__device__ __forceinline__ uint32_t load_fp(const void* keys, uint64_t i, int k) {
-  return FROM_HASH ? fingerprint(static_cast<const uint64_t*>(keys)[i], k) : static_cast<const uint32_t*>(keys)[i];
+// Path gate: the narrow (packed u64) and wide (u32 fp + u64 pos) passes are both enqueued;
+// each kernel runs only if ctl[0] selects its path (ctl == nullptr: always run).  ctl[0] is
+// only changed by the first narrow downsweep, never while a gated kernel is running.
+__device__ __forceinline__ bool gate_off(const uint64_t* ctl, int want) {
+  return ctl != nullptr && ld_volatile_u64(ctl) != (uint64_t)want;
 }
 
-template <bool FROM_HASH>
+// IN: 0 = u64 hashes (fingerprint taken here), 1 = u32 fingerprints, 2 = packed u64 items
+// (fingerprint in the high half).
+template <int IN>
+__device__ __forceinline__ uint32_t load_key(const void* keys, uint64_t i, int k) {
+  if (IN == 0) return fingerprint(static_cast<const uint64_t*>(keys)[i], k);
+  if (IN == 1) return static_cast<const uint32_t*>(keys)[i];
+  return (uint32_t)(static_cast<const uint64_t*>(keys)[i] >> 32);
+}
+
+template <int IN>
 __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const uint64_t* d_m, uint64_t m_cap, int k,
-                                                       int shift, int dbits, uint32_t* counts, uint64_t nchunks) {
+                                                       int shift, int dbits, uint32_t* counts, uint64_t nchunks,
+                                                       const uint64_t* ctl, int want) {
+  if (gate_off(ctl, want)) return;
   __shared__ uint32_t h[kNW][256];
   const unsigned lane = lane_id(), wid = warp_id();
   for (int i = lane; i < 256; i += 32) h[wid][i] = 0;
@@ -86,8 +99,15 @@ __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const u
   const uint64_t end = min(m, base + kChunk);
   const uint32_t dmask = (1u << dbits) - 1u;
   const unsigned lt = (1u << lane) - 1u;
-  for (uint64_t i = base + threadIdx.x; i < end; i += kTPB)
-    atomicAdd(&h[wid][(load_fp<FROM_HASH>(keys, i, k) >> shift) & dmask], 1u);
+  uint64_t i = base + threadIdx.x;
+  for (; i + 3 * kTPB < end; i += 4 * kTPB) {  // 4 loads in flight per thread
+    uint32_t f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) f[u] = load_key<IN>(keys, i + u * kTPB, k);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) atomicAdd(&h[wid][(f[u] >> shift) & dmask], 1u);
+  }
+  for (; i < end; i += kTPB) atomicAdd(&h[wid][(load_key<IN>(keys, i, k) >> shift) & dmask], 1u);
   (void)lt;
   __syncthreads();
   const uint32_t d = threadIdx.x;
@@ -99,7 +119,9 @@ __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const u
 
 // block d: offsets[d][c] = exclusive scan over chunks; totals[d] = digit total
 __global__ void __launch_bounds__(kTPB) chunk_scan_kernel(const uint32_t* counts, uint64_t nchunks,
-                                                          uint64_t* offsets, unsigned long long* totals) {
+                                                          uint64_t* offsets, unsigned long long* totals,
+                                                          const uint64_t* ctl, int want) {
+  if (gate_off(ctl, want)) return;
   __shared__ unsigned long long ws[kNW];
   const uint64_t d = blockIdx.x;
   const uint32_t* cn = counts + d * nchunks;
@@ -118,7 +140,9 @@ __global__ void __launch_bounds__(kTPB) chunk_scan_kernel(const uint32_t* counts
 }
 
 // exclusive scan of the 256 digit totals (one block of 256 threads)
-__global__ void digit_scan_kernel(const unsigned long long* totals, unsigned long long* base) {
+__global__ void digit_scan_kernel(const unsigned long long* totals, unsigned long long* base, const uint64_t* ctl,
+                                  int want) {
+  if (gate_off(ctl, want)) return;
   __shared__ unsigned long long ws[kNW];
   unsigned long long tot;
   base[threadIdx.x] = block_exclusive_sum<256, unsigned long long>(totals[threadIdx.x], ws, &tot);
@@ -155,7 +179,8 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
                                                          const uint64_t* d_m, uint64_t m_cap, int k, int shift,
                                                          int dbits, const uint64_t* __restrict__ offsets,
                                                          const unsigned long long* __restrict__ dbase,
-                                                         uint64_t nchunks) {
+                                                         uint64_t nchunks, const uint64_t* ctl, int use_tma) {
+  if (gate_off(ctl, 0)) return;
   using SM = DownSmem<FROM_HASH>;
   using KT = typename SM::KT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -179,7 +204,7 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
   __syncthreads();
   const uint64_t cbase = c * (uint64_t)kChunk;
   const int nsubs = (int)min((uint64_t)kSubs, (m - min(m, cbase) + kDTile - 1) / kDTile);
-  auto full = [&](int sub) { return cbase + (uint64_t)(sub + 1) * kDTile <= m; };
+  auto full = [&](int sub) { return use_tma && cbase + (uint64_t)(sub + 1) * kDTile <= m; };
   auto issue = [&](int sub) {
     if (threadIdx.x == 0 && sub < nsubs && full(sub)) {
       const int b = sub % kStages;
@@ -298,6 +323,237 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
     }
   }
 }
+
+
+// ---------------------------------------------------------------- narrow passes (packed items)
+// When every position of the call lies in [pos0, pos0 + 2^32), pos0 = pos[0] (one
+// mz_extract_ex call on < 2^32 bases always qualifies), an entry travels between passes as
+// ONE u64 item = (fp << 32) | (pos - pos0): 8 B per entry per pass instead of 12, one load
+// and one store.  ctl_kernel makes the decision from pos[0] and pos[m-1]; the first narrow
+// downsweep re-checks every entry and, on any violation (unsorted input), switches ctl[0]
+// to the wide path, whose kernels are enqueued behind it and then redo the sort.
+//
+// Ranking (per-pass cost floor on B200, tools/microbench_rank.cu): a bitwise ballot
+// multi-split gives each item its peers (same digit) among the 32 items of a warp step;
+// the lowest peer adds the peer count to the warp's counter with one shared atomic and
+// broadcasts the old value (no __syncwarp round trips, no MATCH.ANY, which runs at half
+// the rate of 8 ballots on sm_100).  Items are numbered warp-major, so rank order = input
+// order (stable).  Writes go out per digit run from a digit-sorted staging copy; partial
+// 32 B sectors at run edges are merged in L2 (tools/microbench_radix.cu: DRAM writes stay
+// at the algorithmic bytes for runs >= 4 items).
+enum { kInHashPos = 0, kInFpPos = 1, kInPk = 2 };
+enum { kOutPk = 0, kOutFpPos = 1 };
+constexpr int kNTPB = 512;
+constexpr int kNNW = kNTPB / 32;
+
+__global__ void ctl_kernel(const uint64_t* pos, const uint64_t* d_m, uint64_t m_cap, uint64_t* ctl) {
+  if (threadIdx.x != 0) return;
+  const uint64_t m = min(count_of(d_m, m_cap), m_cap);
+  uint64_t narrow = 1, p0 = 0;
+  if (m) {
+    p0 = pos[0];
+    const uint64_t p1 = pos[m - 1];
+    narrow = (p1 >= p0 && p1 - p0 <= 0xffffffffull) ? 1 : 0;
+  }
+  ctl[0] = narrow;
+  ctl[1] = p0;
+}
+
+template <int IN> struct NInA { using T = uint64_t; };
+template <> struct NInA<kInFpPos> { using T = uint32_t; };
+
+template <int IN, int T> struct NIn;
+template <int T> struct NIn<kInHashPos, T> { uint64_t a[T]; uint64_t p[T]; };
+template <int T> struct NIn<kInFpPos, T> { uint32_t a[T]; uint64_t p[T]; };
+template <int T> struct NIn<kInPk, T> { uint64_t a[T]; };
+
+template <int IN, int T>
+__device__ __forceinline__ uint64_t* stage_of(NIn<IN, T>& r) {
+  if constexpr (IN == kInPk) return r.a;
+  else return r.p;
+}
+
+template <int IN, int T>
+struct NSmem {
+  NIn<IN, T> ring[kStages];
+  uint64_t mbar[kStages];
+  uint64_t run_off[256];     // next output index of digit d (global)
+  uint64_t gbase[256];       // staged entry j of digit d goes to gbase[d] + j
+  uint32_t wcnt[kNNW][256];  // per-warp digit counters -> per-warp exclusive offsets
+  uint32_t dstart[256];
+  uint32_t ws2[kNNW];
+};
+
+template <int IN, int T>
+__device__ __forceinline__ uint64_t make_item(const NIn<IN, T>& r, uint32_t j, int k, uint64_t p0, bool& bad) {
+  if constexpr (IN == kInPk) {
+    return r.a[j];
+  } else {
+    uint32_t f;
+    if constexpr (IN == kInHashPos) f = fingerprint(r.a[j], k);
+    else f = r.a[j];
+    const uint64_t pr = r.p[j] - p0;
+    bad |= (pr >> 32) != 0;
+    return ((uint64_t)f << 32) | (uint32_t)pr;
+  }
+}
+
+template <int IN, int OUT, int IPT>
+__global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const uint64_t* __restrict__ p_in,
+                                                       void* a_out, uint64_t* __restrict__ p_out, const uint64_t* d_m,
+                                                       uint64_t m_cap, int k, int shift, int dbits,
+                                                       const uint64_t* __restrict__ offsets,
+                                                       const unsigned long long* __restrict__ dbase, uint64_t nchunks,
+                                                       uint64_t* ctl, int use_tma) {
+  constexpr int T = kNTPB * IPT;
+  static_assert(kChunk % T == 0, "chunk must hold whole tiles");
+  using SM = NSmem<IN, T>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(smem_raw);
+  __shared__ uint64_t s_m, s_p0;
+  __shared__ int s_go;
+  const uint32_t td = threadIdx.x;
+  if (td == 0) {
+    s_go = ld_volatile_u64(ctl) == 1;
+    s_m = min(count_of(d_m, m_cap), m_cap);
+    s_p0 = ctl[1];
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const uint64_t m = s_m, p0 = s_p0;
+  const unsigned lane = lane_id(), wid = warp_id(), lt = (1u << lane) - 1u;
+  const uint32_t dmask = (1u << dbits) - 1u;
+  const int dsh = 32 + shift;
+  const uint64_t c = blockIdx.x, cbase = c * (uint64_t)kChunk;
+  if (cbase >= m) return;
+  if (td < 256) S.run_off[td] = dbase[td] + offsets[(uint64_t)td * nchunks + c];
+  for (uint32_t i = td; i < kNNW * 256; i += kNTPB) (&S.wcnt[0][0])[i] = 0;
+  if (td == 0) {
+    for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nsubs = (int)min((uint64_t)(kChunk / T), (m - cbase + T - 1) / T);
+  auto tma_ok = [&](int sub) { return use_tma && cbase + (uint64_t)(sub + 1) * T <= m; };
+  auto issue = [&](int sub) {
+    if (td == 0 && sub < nsubs && tma_ok(sub)) {
+      const int b = sub % kStages;
+      const uint64_t base = cbase + (uint64_t)sub * T;
+      constexpr uint32_t abytes = sizeof(S.ring[0].a);
+      if constexpr (IN == kInPk) {
+        mbar_arrive_expect_tx(&S.mbar[b], abytes);
+        bulk_g2s(S.ring[b].a, static_cast<const uint64_t*>(a_in) + base, abytes, &S.mbar[b]);
+      } else {
+        constexpr uint32_t pbytes = sizeof(S.ring[0].p);
+        mbar_arrive_expect_tx(&S.mbar[b], abytes + pbytes);
+        bulk_g2s(S.ring[b].a, static_cast<const typename NInA<IN>::T*>(a_in) + base, abytes, &S.mbar[b]);
+        bulk_g2s(S.ring[b].p, p_in + base, pbytes, &S.mbar[b]);
+      }
+    }
+  };
+  for (int p = 0; p < kStages - 1; ++p) issue(p);
+  uint32_t parity = 0;
+  bool bad = false;
+  for (int sub = 0; sub < nsubs; ++sub) {
+    const int b = sub % kStages;
+    const uint64_t base = cbase + (uint64_t)sub * T;
+    const uint32_t nvalid = (uint32_t)min((uint64_t)T, m - base);
+    issue(sub + kStages - 1);
+    if (tma_ok(sub)) {
+      mbar_wait(&S.mbar[b], (parity >> b) & 1u);
+      parity ^= 1u << b;
+    } else {
+      for (uint32_t j = td; j < (uint32_t)T; j += kNTPB) {
+        const bool v = j < nvalid;
+        if constexpr (IN == kInPk) {
+          S.ring[b].a[j] = v ? static_cast<const uint64_t*>(a_in)[base + j] : 0ull;
+        } else {
+          S.ring[b].a[j] = v ? static_cast<const typename NInA<IN>::T*>(a_in)[base + j] : 0;
+          S.ring[b].p[j] = v ? p_in[base + j] : p0;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- stable rank of every item within its digit (warp-major item order)
+    const bool whole = nvalid == (uint32_t)T;
+    uint64_t item[IPT];
+    uint32_t rank[IPT];
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      const uint32_t j = wid * (IPT * 32) + it * 32 + lane;
+      const bool valid = j < nvalid;
+      item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
+      const uint32_t d = (uint32_t)(item[it] >> dsh) & dmask;
+      unsigned peers = whole ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int bb = 0; bb < 8; ++bb) {
+        if (bb < dbits) {
+          const uint32_t bit = (d >> bb) & 1u;
+          const unsigned mb = __ballot_sync(0xffffffffu, bit);
+          peers &= ~(mb ^ (0u - bit));
+        }
+      }
+      if (!valid) peers = 1u << lane;
+      const uint32_t before = __popc(peers & lt);
+      uint32_t old = 0;
+      if (valid && before == 0) old = atomicAdd(&S.wcnt[wid][d], (uint32_t)__popc(peers));
+      old = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
+      rank[it] = valid ? old + before : 0xffffffffu;
+    }
+    __syncthreads();
+    // ---- per-digit offsets: over warps (serial per digit), then over digits (block scan)
+    uint32_t run = 0;
+    if (td < 256) {
+#pragma unroll
+      for (int w = 0; w < kNNW; ++w) {
+        const uint32_t cc = S.wcnt[w][td];
+        S.wcnt[w][td] = run;
+        run += cc;
+      }
+    }
+    {
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_sum<kNTPB, uint32_t>(td < 256 ? run : 0u, S.ws2, &tot);
+      if (td < 256) {
+        S.dstart[td] = ex;
+        const uint64_t r0 = S.run_off[td];
+        S.gbase[td] = r0 - ex;
+        S.run_off[td] = r0 + run;
+      }
+    }
+    __syncthreads();
+    // ---- stage in digit order (in place: every item of this tile is in registers)
+    uint64_t* stage = stage_of<IN, T>(S.ring[b]);
+#pragma unroll
+    for (int it = 0; it < IPT; ++it) {
+      if (rank[it] != 0xffffffffu) {
+        const uint32_t d = (uint32_t)(item[it] >> dsh) & dmask;
+        stage[S.dstart[d] + S.wcnt[wid][d] + rank[it]] = item[it];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;  // own row: read only by this warp above
+    // ---- write every digit run contiguously
+    for (uint32_t j = td; j < nvalid; j += kNTPB) {
+      const uint64_t v = stage[j];
+      const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
+      if constexpr (OUT == kOutPk) {
+        static_cast<uint64_t*>(a_out)[g] = v;
+      } else {
+        static_cast<uint32_t*>(a_out)[g] = (uint32_t)(v >> 32);
+        p_out[g] = p0 + (uint32_t)v;
+      }
+    }
+    fence_proxy_async();  // ring slot b is refilled by TMA in a later iteration
+    __syncthreads();
+  }
+  if constexpr (IN != kInPk) {
+    if (__syncthreads_or(bad) && td == 0) st_volatile_u64(ctl, 0);  // precondition broken: wide path redoes it
+  }
+}
+
+template <int IN, int OUT, int IPT>
+size_t nsweep_smem() { return sizeof(NSmem<IN, kNTPB * IPT>); }
 
 // Pointer table from the bucket-sorted fingerprints, in three data-parallel steps (bucket
 // sizes are very uneven: minimizer hashes are window minima, so high buckets are mostly
@@ -469,10 +725,11 @@ struct SortWs {
   uint64_t* offs;             // [256 * nchunks]
   unsigned long long* totals; // [256]
   unsigned long long* dbase;  // [256]
+  uint64_t* ctl;              // [2]: path (1 narrow, 0 wide), pos0
   uint32_t* fpA;
-  uint64_t* posA;
+  uint64_t* posA;             // also the narrow path's packed items (A)
   uint32_t* fpB;
-  uint64_t* posB;
+  uint64_t* posB;             // also the narrow path's packed items (B)
   uint32_t* fpF;              // final fingerprints when the caller gave none
 };
 
@@ -484,6 +741,7 @@ void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
   c.template take<uint64_t>(256 * chunks_for(m));
   c.template take<unsigned long long>(256);
   c.template take<unsigned long long>(256);
+  c.template take<uint64_t>(2);
   if (npass >= 2) {
     c.template take<uint32_t>(m + 1);
     c.template take<uint64_t>(m + 1);
@@ -501,6 +759,7 @@ bool carve_sort_ws(Carve& c, uint64_t m, int npass, bool need_fp, SortWs& s) {
   s.offs = c.take<uint64_t>(256 * chunks_for(m));
   s.totals = c.take<unsigned long long>(256);
   s.dbase = c.take<unsigned long long>(256);
+  s.ctl = c.take<uint64_t>(2);
   if (npass >= 2) { s.fpA = c.take<uint32_t>(m + 1); s.posA = c.take<uint64_t>(m + 1); }
   if (npass >= 3) { s.fpB = c.take<uint32_t>(m + 1); s.posB = c.take<uint64_t>(m + 1); }
   if (need_fp) s.fpF = c.take<uint32_t>(m + 1);
@@ -513,50 +772,132 @@ int grid_stride_blocks(uint64_t m) {
   return (int)std::max<uint64_t>(1, std::min(want, cap));
 }
 
-// Stable LSD sort of m entries by fp bits [lo_bit, hi_bit) into (fp_dst, pos_dst).
-// After the call s.totals holds the digit totals of the LAST pass.
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// One reduce-then-scan pass: upsweep (digit counts per chunk) + chunk scan + digit scan.
+template <int IN>
+int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s,
+               int want, cudaStream_t st) {
+  upsweep_kernel<IN><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want);
+  MZS_LAUNCHED();
+  chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals, s.ctl, want);
+  MZS_LAUNCHED();
+  digit_scan_kernel<<<1, 256, 0, st>>>(s.totals, s.dbase, s.ctl, want);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+template <int IN, int OUT, int IPT>
+int launch_nsweep(const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out, const uint64_t* d_m,
+                  uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s, int use_tma, cudaStream_t st) {
+  auto kern = nsweep_kernel<IN, OUT, IPT>;
+  const size_t sm = nsweep_smem<IN, OUT, IPT>();
+  MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  kern<<<(unsigned)nch, kNTPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                         use_tma);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+template <int IN, int OUT>
+int launch_nsweep_ipt(int ipt, const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out,
+                      const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s, int use_tma,
+                      cudaStream_t st) {
+  if (ipt == 4) return launch_nsweep<IN, OUT, 4>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+  return launch_nsweep<IN, OUT, 8>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+}
+
+// Stable LSD sort of m entries by fp bits [lo_bit, hi_bit) into (fp_dst, pos_dst); input is
+// (u64 hashes | u32 fingerprints) + u64 positions.  Both paths are enqueued: the narrow one
+// (packed u64 items, ctl[0] == 1) and the wide one (u32 + u64 entries, ctl[0] == 0); see
+// ctl_kernel.  After the call s.totals holds the digit totals of the LAST pass.
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st) {
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
   const uint64_t nch = (m + kChunk - 1) / kChunk;
   if (nch == 0) return SLSUM_OK;
-  const size_t dsm1 = sizeof(DownSmem<true>), dsm0 = sizeof(DownSmem<false>);
-  static const bool use_match = [] {
-    const char* e = getenv("MZS_RADIX_MATCH");
-    return e && e[0] == '1';
-  }();
-  auto ds1 = use_match ? downsweep_kernel<true, true> : downsweep_kernel<true, false>;
-  auto ds0 = use_match ? downsweep_kernel<false, true> : downsweep_kernel<false, false>;
-  MZS_CUDA(cudaFuncSetAttribute(ds1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm1));
-  MZS_CUDA(cudaFuncSetAttribute(ds0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm0));
-  const void* kin = keys;
-  const uint64_t* pin = pos;
-  bool kin_hash = from_hash;
-  for (int p = 0; p < npass; ++p) {
-    uint32_t* fo;
-    uint64_t* po;
-    if (p == npass - 1) { fo = fp_dst; po = pos_dst; }
-    else if (p % 2 == 0) { fo = s.fpA; po = s.posA; }
-    else { fo = s.fpB; po = s.posB; }
-    const int sh = lo_bit + 8 * p;
-    const int nb = std::min(8, hi_bit - sh);
-    if (kin_hash) upsweep_kernel<true><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch);
-    else upsweep_kernel<false><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch);
-    MZS_LAUNCHED();
-    chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals);
-    MZS_LAUNCHED();
-    digit_scan_kernel<<<1, 256, 0, st>>>(s.totals, s.dbase);
-    MZS_LAUNCHED();
-    if (kin_hash)
-      ds1<<<(unsigned)nch, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch);
-    else
-      ds0<<<(unsigned)nch, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch);
-    MZS_LAUNCHED();
-    kin = fo;
-    pin = po;
-    kin_hash = false;
+  int rc;
+  static const int force = env_int("MZS_RADIX_PATH", -1);  // tests/tuning: 0 forces the wide path
+  static const int ipt_first = env_int("MZS_NIPT_FIRST", 8);
+  static const int ipt_pk = env_int("MZS_NIPT", 8);
+  ctl_kernel<<<1, 32, 0, st>>>(pos, d_m, m, s.ctl);
+  MZS_LAUNCHED();
+  if (force == 0) MZS_CUDA(cudaMemsetAsync(s.ctl, 0, sizeof(uint64_t), st));
+  const int tma_in = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0;
+  auto pass_out = [&](int p, uint64_t*& pk, uint32_t*& fo, uint64_t*& po) {
+    if (p == npass - 1) { fo = fp_dst; po = pos_dst; pk = nullptr; }
+    else if (p % 2 == 0) { fo = s.fpA; po = s.posA; pk = s.posA; }
+    else { fo = s.fpB; po = s.posB; pk = s.posB; }
+  };
+  // ---- narrow pass 0 (reads the caller's arrays; re-checks the precondition)
+  {
+    uint64_t* pk; uint32_t* fo; uint64_t* po;
+    pass_out(0, pk, fo, po);
+    const int nb = std::min(8, hi_bit - lo_bit);
+    rc = from_hash ? count_pass<0>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st)
+                   : count_pass<1>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st);
+    if (rc) return rc;
+    if (from_hash) {
+      rc = npass == 1 ? launch_nsweep_ipt<kInHashPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
+                      : launch_nsweep_ipt<kInHashPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
+    } else {
+      rc = npass == 1 ? launch_nsweep_ipt<kInFpPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
+                      : launch_nsweep_ipt<kInFpPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
+    }
+    if (rc) return rc;
   }
+  // ---- wide path: every pass (gated off when the narrow path holds)
+  {
+    const size_t dsm1 = sizeof(DownSmem<true>), dsm0 = sizeof(DownSmem<false>);
+    static const bool use_match = env_int("MZS_RADIX_MATCH", 0) == 1;
+    auto ds1 = use_match ? downsweep_kernel<true, true> : downsweep_kernel<true, false>;
+    auto ds0 = use_match ? downsweep_kernel<false, true> : downsweep_kernel<false, false>;
+    MZS_CUDA(cudaFuncSetAttribute(ds1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm1));
+    MZS_CUDA(cudaFuncSetAttribute(ds0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm0));
+    const void* kin = keys;
+    const uint64_t* pin = pos;
+    bool kin_hash = from_hash;
+    for (int p = 0; p < npass; ++p) {
+      uint64_t* pk; uint32_t* fo; uint64_t* po;
+      pass_out(p, pk, fo, po);
+      const int sh = lo_bit + 8 * p;
+      const int nb = std::min(8, hi_bit - sh);
+      rc = kin_hash ? count_pass<0>(kin, d_m, m, k, sh, nb, nch, s, 0, st) : count_pass<1>(kin, d_m, m, k, sh, nb, nch, s, 0, st);
+      if (rc) return rc;
+      if (kin_hash)
+        ds1<<<(unsigned)nch, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                                p == 0 ? tma_in : 1);
+      else
+        ds0<<<(unsigned)nch, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                                p == 0 ? tma_in : 1);
+      MZS_LAUNCHED();
+      kin = fo;
+      pin = po;
+      kin_hash = false;
+    }
+  }
+  // ---- narrow passes 1.. (packed items in, packed or final out)
+  {
+    const uint64_t* kin = nullptr;
+    { uint64_t* pk; uint32_t* fo; uint64_t* po; pass_out(0, pk, fo, po); kin = pk; }
+    for (int p = 1; p < npass; ++p) {
+      uint64_t* pk; uint32_t* fo; uint64_t* po;
+      pass_out(p, pk, fo, po);
+      const int sh = lo_bit + 8 * p;
+      const int nb = std::min(8, hi_bit - sh);
+      rc = count_pass<2>(kin, d_m, m, k, sh, nb, nch, s, 1, st);
+      if (rc) return rc;
+      rc = p == npass - 1 ? launch_nsweep_ipt<kInPk, kOutFpPos>(ipt_pk, kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st)
+                          : launch_nsweep_ipt<kInPk, kOutPk>(ipt_pk, kin, nullptr, pk, nullptr, d_m, m, k, sh, nb, nch, s, 1, st);
+      if (rc) return rc;
+      kin = pk;
+    }
+  }
+  (void)force;
   return SLSUM_OK;
 }
 

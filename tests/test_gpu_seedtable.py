@@ -48,6 +48,61 @@ def test_random_keys(k, bits):
         _cmp(key, pos, k, bits)
 
 
+@pytest.mark.parametrize("k,bits", [(15, 24), (19, 24), (19, 16), (15, 8), (12, 20)])
+def test_random_keys_narrow_span(k, bits):
+    """Positions spanning < 2^32 take the packed-item (narrow) radix path."""
+    rng = np.random.default_rng(k * 131 + bits)
+    for m in (1, 2047, 2048, 4097, 131_071, 131_073, 300_001):
+        key = rng.integers(0, 1 << (2 * k), size=m, dtype=np.uint64)
+        base = int(rng.integers(0, 1 << 40))
+        pos = (np.uint64(base) + np.sort(rng.choice(min(1 << 32, 50 * m), size=m, replace=False))).astype(np.uint64)
+        _cmp(key, pos, k, bits)
+        _cmp(key, pos, k, bits, use_dm=True)
+
+
+@pytest.mark.parametrize("span", [(1 << 32) - 1, 1 << 32])
+def test_span_boundary(span):
+    """Largest narrow span (2^32 - 1) and the smallest wide one."""
+    rng = np.random.default_rng(span & 0xffff)
+    m = 50_000
+    key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
+    mid = np.sort(rng.choice(span - 1, size=m - 2, replace=False) + 1)
+    pos = np.concatenate([[0], mid, [span]]).astype(np.uint64) + np.uint64(7)
+    _cmp(key, pos, 19, 24)
+
+
+def test_unsorted_positions_fall_back():
+    """pos[0] and pos[m-1] are close but an inner position is 2^33 away: the first narrow
+    pass detects it and the wide path redoes the sort (stable = input order inside a bucket)."""
+    rng = np.random.default_rng(5)
+    m = 200_000
+    key = rng.integers(0, 1 << 30, size=m, dtype=np.uint64)
+    pos = np.arange(m, dtype=np.uint64) * 5
+    pos[m // 2] = np.uint64(1 << 33)
+    _cmp(key, pos, 15, 24)
+    pos2 = pos.copy()
+    pos2[m // 3] = np.uint64(0)          # below pos[0]: also outside [pos0, pos0 + 2^32)
+    pos2[0] = np.uint64(10)
+    pos2[m // 2] = np.uint64(m)
+    _cmp(key, pos2, 15, 24)
+
+
+def test_unaligned_inputs():
+    """Inputs 8 B off a 16 B boundary cannot be TMA-staged; the kernels load them directly."""
+    rng = np.random.default_rng(11)
+    for m, span in ((70_001, 10 ** 6), (70_001, 10 ** 11)):
+        key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
+        pos = np.sort(rng.choice(span, size=m, replace=False)).astype(np.uint64)
+        kt = _dev(np.concatenate([[0], key]).astype(np.uint64))[1:]
+        pt = _dev(np.concatenate([[0], pos]).astype(np.uint64))[1:]
+        assert kt.data_ptr() % 16 == 8
+        off, po, fp = P.seedtable_build(kt, pt, 19, 24)
+        wo, wf, wp = O.seedtable(key, pos, 19, 24)
+        assert np.array_equal(off.cpu().numpy(), wo)
+        assert np.array_equal(po[:m].cpu().numpy(), wp)
+        assert np.array_equal(fp[:m].cpu().numpy(), wf)
+
+
 def test_heavy_buckets_and_device_count():
     rng = np.random.default_rng(1)
     m = 300_000
