@@ -12,7 +12,8 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmzslsum.so")
+# MZS_LIB: an alternative build of the same library (tools/prof_nsweep.py's instrumented one)
+LIB_PATH = os.environ.get("MZS_LIB") or os.path.join(HERE, "libmzslsum.so")
 
 # ---------------------------------------------------------------- constants (mzslsum.h)
 SLSUM_OK, SLSUM_EINVAL, SLSUM_EUNSUPPORTED, SLSUM_ECAPACITY, SLSUM_ECUDA, SLSUM_ENOMEM = 0, -1, -2, -3, -4, -5

@@ -91,30 +91,32 @@ __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const u
   if (gate_off(ctl, want)) return;
   __shared__ uint32_t h[kNW][256];
   const unsigned lane = lane_id(), wid = warp_id();
-  for (int i = lane; i < 256; i += 32) h[wid][i] = 0;
-  __syncthreads();
   const uint64_t m = block_count(d_m, m_cap);
-  const uint64_t c = blockIdx.x;
-  const uint64_t base = c * (uint64_t)kChunk;
-  const uint64_t end = min(m, base + kChunk);
   const uint32_t dmask = (1u << dbits) - 1u;
-  const unsigned lt = (1u << lane) - 1u;
-  uint64_t i = base + threadIdx.x;
-  for (; i + 3 * kTPB < end; i += 4 * kTPB) {  // 4 loads in flight per thread
-    uint32_t f[4];
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {  // grid-stride over chunks
+    for (int i = lane; i < 256; i += 32) h[wid][i] = 0;
+    __syncthreads();
+    const uint64_t base = c * (uint64_t)kChunk;
+    const uint64_t end = min(m, base + kChunk);
+    {
+      uint64_t i = base + threadIdx.x;
+      for (; i + 3 * kTPB < end; i += 4 * kTPB) {  // 4 loads in flight per thread
+        uint32_t f[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) f[u] = load_key<IN>(keys, i + u * kTPB, k);
+        for (int u = 0; u < 4; ++u) f[u] = load_key<IN>(keys, i + u * kTPB, k);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) atomicAdd(&h[wid][(f[u] >> shift) & dmask], 1u);
+        for (int u = 0; u < 4; ++u) atomicAdd(&h[wid][(f[u] >> shift) & dmask], 1u);
+      }
+      for (; i < end; i += kTPB) atomicAdd(&h[wid][(load_key<IN>(keys, i, k) >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    const uint32_t d = threadIdx.x;
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) t += h[w][d];
+    counts[(uint64_t)d * nchunks + c] = t;
+    __syncthreads();
   }
-  for (; i < end; i += kTPB) atomicAdd(&h[wid][(load_key<IN>(keys, i, k) >> shift) & dmask], 1u);
-  (void)lt;
-  __syncthreads();
-  const uint32_t d = threadIdx.x;
-  uint32_t t = 0;
-#pragma unroll
-  for (int w = 0; w < kNW; ++w) t += h[w][d];
-  counts[(uint64_t)d * nchunks + c] = t;
 }
 
 // block d: offsets[d][c] = exclusive scan over chunks; totals[d] = digit total
@@ -186,20 +188,22 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SM& S = *reinterpret_cast<SM*>(smem_raw);
   const unsigned lane = lane_id(), wid = warp_id();
-  const uint64_t c = blockIdx.x;
   const uint64_t m = block_count(d_m, m_cap);
   const uint32_t dmask = (1u << dbits) - 1u;
   const unsigned lt = (1u << lane) - 1u;
   const KT* kg = static_cast<const KT*>(keys_in);
   const uint32_t td = threadIdx.x;  // digit owned by this thread when td < 256
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
+    fence_mbar_init();
+  }
+  uint32_t parity = 0;
+  // grid-stride over chunks (a small grid: the gated-off launch costs a few us, not 40 waves)
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
   if (td < 256) {
     const uint64_t r = dbase[td] + offsets[(uint64_t)td * nchunks + c];
     S.run_off[td] = r;
     S.carry_lo[td] = r;
-  }
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
-    fence_mbar_init();
   }
   __syncthreads();
   const uint64_t cbase = c * (uint64_t)kChunk;
@@ -215,7 +219,6 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
     }
   };
   for (int p = 0; p < kStages - 1; ++p) issue(p);
-  uint32_t parity = 0;
   for (int sub = 0; sub < nsubs; ++sub) {
     const int b = sub % kStages;
     const uint64_t base = cbase + (uint64_t)sub * kDTile;
@@ -322,8 +325,28 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
       pos_out[g] = S.cpos[td][g & (kGrp - 1)];
     }
   }
+  __syncthreads();
+  }
 }
 
+
+// Optional per-phase cycle counters of the narrow downsweep (build with -DMZS_PROF; read via
+// seedtable_prof_read).  Thread 0 of every CTA adds each phase's clock64 delta.
+#ifdef MZS_PROF
+__device__ unsigned long long g_prof[8];
+#define MZS_PROF_DECL() long long prof_t = clock64()
+#define MZS_PROF_MARK(i)                                                  \
+  do {                                                                    \
+    if (threadIdx.x == 0) {                                               \
+      const long long now_ = clock64();                                   \
+      if ((i) > 0) atomicAdd(&g_prof[(i) - 1], (unsigned long long)(now_ - prof_t)); \
+      prof_t = now_;                                                      \
+    }                                                                     \
+  } while (0)
+#else
+#define MZS_PROF_DECL() (void)0
+#define MZS_PROF_MARK(i) (void)0
+#endif
 
 // ---------------------------------------------------------------- narrow passes (packed items)
 // When every position of the call lies in [pos0, pos0 + 2^32), pos0 = pos[0] (one
@@ -343,8 +366,9 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
 // at the algorithmic bytes for runs >= 4 items).
 enum { kInHashPos = 0, kInFpPos = 1, kInPk = 2 };
 enum { kOutPk = 0, kOutFpPos = 1 };
-constexpr int kNTPB = 512;
-constexpr int kNNW = kNTPB / 32;
+// items ranked per round of __syncwarp (their shared-memory round trips overlap): 4 for big
+// tiles, 2 where the smaller footprint lets a third CTA fit on the SM
+template <int IPT> constexpr int peer_tables() { return IPT >= 16 ? 4 : 2; }
 
 __global__ void ctl_kernel(const uint64_t* pos, const uint64_t* d_m, uint64_t m_cap, uint64_t* ctl) {
   if (threadIdx.x != 0) return;
@@ -373,15 +397,17 @@ __device__ __forceinline__ uint64_t* stage_of(NIn<IN, T>& r) {
   else return r.p;
 }
 
-template <int IN, int T>
+template <int IN, int TPB, int T>
 struct NSmem {
+  static constexpr int NW = TPB / 32;
   NIn<IN, T> ring[kStages];
   uint64_t mbar[kStages];
   uint64_t run_off[256];     // next output index of digit d (global)
   uint64_t gbase[256];       // staged entry j of digit d goes to gbase[d] + j
-  uint32_t wcnt[kNNW][256];  // per-warp digit counters -> per-warp exclusive offsets
-  uint32_t dstart[256];
-  uint32_t ws2[kNNW];
+  uint32_t wcnt[NW][256];    // per-warp digit counters -> per-warp exclusive offsets
+  uint32_t dummy[NW][32];    // atomic targets of non-leader lanes (branch-free ranking)
+  uint32_t pm[NW][peer_tables<T / TPB>()][256];  // per-warp peer bit tables
+  uint32_t ws2[NW];
 };
 
 template <int IN, int T>
@@ -398,16 +424,34 @@ __device__ __forceinline__ uint64_t make_item(const NIn<IN, T>& r, uint32_t j, i
   }
 }
 
-template <int IN, int OUT, int IPT>
-__global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const uint64_t* __restrict__ p_in,
+
+// Peers of this lane's digit d < 256 among the 32 lanes (bitwise ballot multi-split; a
+// digit narrower than 8 bits has zero high bits in every lane, so its extra ballots are
+// no-ops).  Measured on B200 at ~1.5 items/clk/SM (tools/microbench_rank.cu), half the
+// cost of MATCH.ANY.
+__device__ __forceinline__ unsigned peers8(uint32_t d) {
+  unsigned peers = 0xffffffffu;
+#pragma unroll
+  for (int bb = 0; bb < 8; ++bb) {
+    const bool bit = (d & (1u << bb)) != 0u;
+    const unsigned mb = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? mb : ~mb;
+  }
+  return peers;
+}
+
+template <int IN, int OUT, int TPB, int IPT>
+__global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uint64_t* __restrict__ p_in,
                                                        void* a_out, uint64_t* __restrict__ p_out, const uint64_t* d_m,
                                                        uint64_t m_cap, int k, int shift, int dbits,
                                                        const uint64_t* __restrict__ offsets,
                                                        const unsigned long long* __restrict__ dbase, uint64_t nchunks,
                                                        uint64_t* ctl, int use_tma) {
-  constexpr int T = kNTPB * IPT;
+  constexpr int T = TPB * IPT;
+  constexpr int NW = TPB / 32;
   static_assert(kChunk % T == 0, "chunk must hold whole tiles");
-  using SM = NSmem<IN, T>;
+  static_assert(TPB >= 256, "digit threads");
+  using SM = NSmem<IN, TPB, T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SM& S = *reinterpret_cast<SM*>(smem_raw);
   __shared__ uint64_t s_m, s_p0;
@@ -427,7 +471,9 @@ __global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const u
   const uint64_t c = blockIdx.x, cbase = c * (uint64_t)kChunk;
   if (cbase >= m) return;
   if (td < 256) S.run_off[td] = dbase[td] + offsets[(uint64_t)td * nchunks + c];
-  for (uint32_t i = td; i < kNNW * 256; i += kNTPB) (&S.wcnt[0][0])[i] = 0;
+  for (uint32_t i = td; i < NW * 256; i += TPB) (&S.wcnt[0][0])[i] = 0;
+  constexpr int kPeerTables = peer_tables<IPT>();
+  for (uint32_t i = td; i < NW * kPeerTables * 256; i += TPB) (&S.pm[0][0][0])[i] = 0;
   if (td == 0) {
     for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
     fence_mbar_init();
@@ -454,16 +500,18 @@ __global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const u
   for (int p = 0; p < kStages - 1; ++p) issue(p);
   uint32_t parity = 0;
   bool bad = false;
+  MZS_PROF_DECL();
   for (int sub = 0; sub < nsubs; ++sub) {
     const int b = sub % kStages;
     const uint64_t base = cbase + (uint64_t)sub * T;
     const uint32_t nvalid = (uint32_t)min((uint64_t)T, m - base);
+    MZS_PROF_MARK(0);
     issue(sub + kStages - 1);
     if (tma_ok(sub)) {
       mbar_wait(&S.mbar[b], (parity >> b) & 1u);
       parity ^= 1u << b;
     } else {
-      for (uint32_t j = td; j < (uint32_t)T; j += kNTPB) {
+      for (uint32_t j = td; j < (uint32_t)T; j += TPB) {
         const bool v = j < nvalid;
         if constexpr (IN == kInPk) {
           S.ring[b].a[j] = v ? static_cast<const uint64_t*>(a_in)[base + j] : 0ull;
@@ -474,67 +522,105 @@ __global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const u
       }
       __syncthreads();
     }
+    MZS_PROF_MARK(1);
     // ---- stable rank of every item within its digit (warp-major item order)
-    const bool whole = nvalid == (uint32_t)T;
     uint64_t item[IPT];
     uint32_t rank[IPT];
+    auto rank_tile = [&](auto whole_tag) {
+      constexpr bool kWhole = decltype(whole_tag)::value;
+      // Peers (lanes with the same digit) through per-warp shared bit tables: every lane ORs
+      // its lane bit into pm[u][d], and after a __syncwarp reads its digit's word; after a
+      // second __syncwarp it XORs its bit back out.  Each lane only flips its own bit, so the
+      // atomics of different lanes commute.  kPeerTables items share one round of syncwarps
+      // (one table each), so their shared-memory round trips overlap.  ~20 SASS per item
+      // instead of ~60 for an 8-ballot multi-split (tools/microbench_rank.cu).
+      uint32_t (*pm)[256] = S.pm[wid];
+      unsigned peers[IPT];
 #pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-      const uint32_t j = wid * (IPT * 32) + it * 32 + lane;
-      const bool valid = j < nvalid;
-      item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
-      const uint32_t d = (uint32_t)(item[it] >> dsh) & dmask;
-      unsigned peers = whole ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+      for (int g = 0; g < IPT; g += kPeerTables) {
 #pragma unroll
-      for (int bb = 0; bb < 8; ++bb) {
-        if (bb < dbits) {
-          const uint32_t bit = (d >> bb) & 1u;
-          const unsigned mb = __ballot_sync(0xffffffffu, bit);
-          peers &= ~(mb ^ (0u - bit));
+        for (int u = 0; u < kPeerTables; ++u) {
+          const int it = g + u;
+          const uint32_t j = wid * (IPT * 32) + it * 32 + lane;
+          item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
+          if (kWhole || j < nvalid) atomicOr(&pm[u][(uint32_t)(item[it] >> dsh) & dmask], 1u << lane);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kPeerTables; ++u) {
+          const int it = g + u;
+          const bool valid = kWhole || wid * (IPT * 32) + it * 32 + lane < nvalid;
+          peers[it] = valid ? pm[u][(uint32_t)(item[it] >> dsh) & dmask] : (1u << lane);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < kPeerTables; ++u) {
+          const int it = g + u;
+          if (kWhole || wid * (IPT * 32) + it * 32 + lane < nvalid)
+            atomicXor(&pm[u][(uint32_t)(item[it] >> dsh) & dmask], 1u << lane);
         }
       }
-      if (!valid) peers = 1u << lane;
-      const uint32_t before = __popc(peers & lt);
-      uint32_t old = 0;
-      if (valid && before == 0) old = atomicAdd(&S.wcnt[wid][d], (uint32_t)__popc(peers));
-      old = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
-      rank[it] = valid ? old + before : 0xffffffffu;
-    }
+      // per-warp digit counters, in item order: the lowest peer adds the peer count (every
+      // other lane adds 0 to its own dummy word, so there is no branch); the old value is
+      // broadcast to the peers.  Same-warp shared atomics are performed in issue order.
+      uint32_t old[IPT];
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) {
+        const bool valid = kWhole || wid * (IPT * 32) + it * 32 + lane < nvalid;
+        const bool lead = valid && (peers[it] & lt) == 0u;
+        uint32_t* tgt = lead ? &S.wcnt[wid][(uint32_t)(item[it] >> dsh) & dmask] : &S.dummy[wid][lane];
+        old[it] = atomicAdd(tgt, lead ? (uint32_t)__popc(peers[it]) : 0u);
+      }
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) {
+        const bool valid = kWhole || wid * (IPT * 32) + it * 32 + lane < nvalid;
+        const uint32_t o = __shfl_sync(0xffffffffu, old[it], __ffs(peers[it]) - 1);
+        rank[it] = valid ? o + __popc(peers[it] & lt) : 0xffffffffu;
+      }
+    };
+    if (nvalid == (uint32_t)T) rank_tile(std::true_type{});
+    else rank_tile(std::false_type{});
     __syncthreads();
-    // ---- per-digit offsets: over warps (serial per digit), then over digits (block scan)
+    MZS_PROF_MARK(2);
+    // ---- offsets: digit totals over warps, block scan over digits, then every (warp, digit)
+    // counter becomes its staging base (digit start + earlier warps' count)
+    uint32_t cnt[NW];
     uint32_t run = 0;
     if (td < 256) {
 #pragma unroll
-      for (int w = 0; w < kNNW; ++w) {
-        const uint32_t cc = S.wcnt[w][td];
-        S.wcnt[w][td] = run;
-        run += cc;
+      for (int w = 0; w < NW; ++w) {
+        cnt[w] = S.wcnt[w][td];
+        run += cnt[w];
       }
     }
     {
       uint32_t tot;
-      const uint32_t ex = block_exclusive_sum<kNTPB, uint32_t>(td < 256 ? run : 0u, S.ws2, &tot);
+      const uint32_t ex = block_exclusive_sum<TPB, uint32_t>(td < 256 ? run : 0u, S.ws2, &tot);
       if (td < 256) {
-        S.dstart[td] = ex;
+        uint32_t acc = ex;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          S.wcnt[w][td] = acc;
+          acc += cnt[w];
+        }
         const uint64_t r0 = S.run_off[td];
         S.gbase[td] = r0 - ex;
         S.run_off[td] = r0 + run;
       }
     }
     __syncthreads();
+    MZS_PROF_MARK(3);
     // ---- stage in digit order (in place: every item of this tile is in registers)
     uint64_t* stage = stage_of<IN, T>(S.ring[b]);
+    const uint32_t* wrow = S.wcnt[wid];
 #pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-      if (rank[it] != 0xffffffffu) {
-        const uint32_t d = (uint32_t)(item[it] >> dsh) & dmask;
-        stage[S.dstart[d] + S.wcnt[wid][d] + rank[it]] = item[it];
-      }
-    }
+    for (int it = 0; it < IPT; ++it)
+      if (rank[it] != 0xffffffffu) stage[wrow[(uint32_t)(item[it] >> dsh) & dmask] + rank[it]] = item[it];
     __syncthreads();
     for (uint32_t i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;  // own row: read only by this warp above
+    MZS_PROF_MARK(4);
     // ---- write every digit run contiguously
-    for (uint32_t j = td; j < nvalid; j += kNTPB) {
+    auto put = [&](uint32_t j) {
       const uint64_t v = stage[j];
       const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
       if constexpr (OUT == kOutPk) {
@@ -543,17 +629,24 @@ __global__ void __launch_bounds__(kNTPB) nsweep_kernel(const void* a_in, const u
         static_cast<uint32_t*>(a_out)[g] = (uint32_t)(v >> 32);
         p_out[g] = p0 + (uint32_t)v;
       }
+    };
+    if (nvalid == (uint32_t)T) {
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) put(td + it * TPB);
+    } else {
+      for (uint32_t j = td; j < nvalid; j += TPB) put(j);
     }
     fence_proxy_async();  // ring slot b is refilled by TMA in a later iteration
     __syncthreads();
+    MZS_PROF_MARK(5);
   }
   if constexpr (IN != kInPk) {
     if (__syncthreads_or(bad) && td == 0) st_volatile_u64(ctl, 0);  // precondition broken: wide path redoes it
   }
 }
 
-template <int IN, int OUT, int IPT>
-size_t nsweep_smem() { return sizeof(NSmem<IN, kNTPB * IPT>); }
+template <int IN, int TPB, int IPT>
+size_t nsweep_smem() { return sizeof(NSmem<IN, TPB, TPB * IPT>); }
 
 // Pointer table from the bucket-sorted fingerprints, in three data-parallel steps (bucket
 // sizes are very uneven: minimizer hashes are window minima, so high buckets are mostly
@@ -781,7 +874,8 @@ int env_int(const char* name, int dflt) {
 template <int IN>
 int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s,
                int want, cudaStream_t st) {
-  upsweep_kernel<IN><<<(unsigned)nch, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want);
+  const unsigned grid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms() * 8);
+  upsweep_kernel<IN><<<grid, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want);
   MZS_LAUNCHED();
   chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals, s.ctl, want);
   MZS_LAUNCHED();
@@ -790,24 +884,29 @@ int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, 
   return SLSUM_OK;
 }
 
-template <int IN, int OUT, int IPT>
+template <int IN, int OUT, int TPB, int IPT>
 int launch_nsweep(const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out, const uint64_t* d_m,
                   uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s, int use_tma, cudaStream_t st) {
-  auto kern = nsweep_kernel<IN, OUT, IPT>;
-  const size_t sm = nsweep_smem<IN, OUT, IPT>();
+  auto kern = nsweep_kernel<IN, OUT, TPB, IPT>;
+  const size_t sm = nsweep_smem<IN, TPB, IPT>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-  kern<<<(unsigned)nch, kNTPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                         use_tma);
+  kern<<<(unsigned)nch, TPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                       use_tma);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
 
+// cfg = TPB * 100 + IPT (tuning knob): 51208, 51204, 25616, 25608
 template <int IN, int OUT>
-int launch_nsweep_ipt(int ipt, const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out,
+int launch_nsweep_cfg(int cfg, const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out,
                       const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s, int use_tma,
                       cudaStream_t st) {
-  if (ipt == 4) return launch_nsweep<IN, OUT, 4>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
-  return launch_nsweep<IN, OUT, 8>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+  switch (cfg) {
+    case 51204: return launch_nsweep<IN, OUT, 512, 4>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+    case 25616: return launch_nsweep<IN, OUT, 256, 16>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+    case 25608: return launch_nsweep<IN, OUT, 256, 8>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+    default: return launch_nsweep<IN, OUT, 512, 8>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, nch, s, use_tma, st);
+  }
 }
 
 // Stable LSD sort of m entries by fp bits [lo_bit, hi_bit) into (fp_dst, pos_dst); input is
@@ -822,8 +921,8 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
   if (nch == 0) return SLSUM_OK;
   int rc;
   static const int force = env_int("MZS_RADIX_PATH", -1);  // tests/tuning: 0 forces the wide path
-  static const int ipt_first = env_int("MZS_NIPT_FIRST", 8);
-  static const int ipt_pk = env_int("MZS_NIPT", 8);
+  static const int ipt_first = env_int("MZS_NCFG_FIRST", 25608);
+  static const int ipt_pk = env_int("MZS_NCFG", 25616);
   ctl_kernel<<<1, 32, 0, st>>>(pos, d_m, m, s.ctl);
   MZS_LAUNCHED();
   if (force == 0) MZS_CUDA(cudaMemsetAsync(s.ctl, 0, sizeof(uint64_t), st));
@@ -842,11 +941,11 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
                    : count_pass<1>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st);
     if (rc) return rc;
     if (from_hash) {
-      rc = npass == 1 ? launch_nsweep_ipt<kInHashPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
-                      : launch_nsweep_ipt<kInHashPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
+      rc = npass == 1 ? launch_nsweep_cfg<kInHashPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
+                      : launch_nsweep_cfg<kInHashPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
     } else {
-      rc = npass == 1 ? launch_nsweep_ipt<kInFpPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
-                      : launch_nsweep_ipt<kInFpPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
+      rc = npass == 1 ? launch_nsweep_cfg<kInFpPos, kOutFpPos>(ipt_first, keys, pos, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_in, st)
+                      : launch_nsweep_cfg<kInFpPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
     }
     if (rc) return rc;
   }
@@ -868,11 +967,12 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       const int nb = std::min(8, hi_bit - sh);
       rc = kin_hash ? count_pass<0>(kin, d_m, m, k, sh, nb, nch, s, 0, st) : count_pass<1>(kin, d_m, m, k, sh, nb, nch, s, 0, st);
       if (rc) return rc;
+      const unsigned wgrid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms());
       if (kin_hash)
-        ds1<<<(unsigned)nch, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+        ds1<<<wgrid, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
                                                 p == 0 ? tma_in : 1);
       else
-        ds0<<<(unsigned)nch, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+        ds0<<<wgrid, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
                                                 p == 0 ? tma_in : 1);
       MZS_LAUNCHED();
       kin = fo;
@@ -891,8 +991,8 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       const int nb = std::min(8, hi_bit - sh);
       rc = count_pass<2>(kin, d_m, m, k, sh, nb, nch, s, 1, st);
       if (rc) return rc;
-      rc = p == npass - 1 ? launch_nsweep_ipt<kInPk, kOutFpPos>(ipt_pk, kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st)
-                          : launch_nsweep_ipt<kInPk, kOutPk>(ipt_pk, kin, nullptr, pk, nullptr, d_m, m, k, sh, nb, nch, s, 1, st);
+      rc = p == npass - 1 ? launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st)
+                          : launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, kin, nullptr, pk, nullptr, d_m, m, k, sh, nb, nch, s, 1, st);
       if (rc) return rc;
       kin = pk;
     }
@@ -926,6 +1026,17 @@ int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
 }  // namespace mzs
 
 using namespace mzs;
+
+#ifdef MZS_PROF
+MZS_API int seedtable_prof_read(unsigned long long* out8, int reset) {
+  MZS_CUDA(cudaMemcpyFromSymbol(out8, g_prof, sizeof(unsigned long long) * 8));
+  if (reset) {
+    static const unsigned long long z[8] = {0};
+    MZS_CUDA(cudaMemcpyToSymbol(g_prof, z, sizeof(z)));
+  }
+  return SLSUM_OK;
+}
+#endif
 
 MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
   Sizer z;
