@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark of the hot path of arxiv 1811.10074 on B200 (contract: README of the task / DESIGN.md).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c1|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c1|c2|c4]
 
 One STEP = one pass of the whole hot path over one synthetic genome (default: BASELINE.json
 configs[2], "C3": 3.1 Gbp human-genome-shaped, GC 41 %, 1 % N in runs, k=19, w=10):
@@ -13,6 +13,13 @@ configs[2], "C3": 3.1 Gbp human-genome-shaped, GC 41 %, 1 % N in runs, k=19, w=1
 (pointer table + position table) out (D2H), both inside the timed region.
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the tier's
 reference arm) on a bounded sample of the same workload.
+
+Secondary configs (not the driver's default line; their JSON lines are kept under profiles/):
+  --config c2   BASELINE configs[1]: generic sliding sums slsum_run_ex on 2^28 elements,
+                {MIN_U32, ADD_U32, ADD_F32} x w in {4,16,64,256,1024} x {GENERIC, COMMUTATIVE};
+                Gelem/s and the HBM roofline per run (8 B algorithmic traffic per element).
+  --config c4   BASELINE configs[3]: 1M long reads (9.98e9 bases), k=15 w=10, segmented
+                minimizer extraction (encode + mz_extract_ex with read offsets), Gbases/s.
 """
 from __future__ import annotations
 
@@ -44,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c1"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-bases", type=int, default=32_000_000)
@@ -147,6 +154,162 @@ def reference_main(args, rank, world):
     return 0
 
 
+# ------------------------------------------------------------------ secondary configs
+def _timed(fn, steps, warmup, stream):
+    """Device time per call (CUDA events on the launching stream, synchronize on both sides)."""
+    import torch
+    for _ in range(max(3, warmup)):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def bench_c2(args):
+    """C2: slsum_run_ex on 2^28 elements (inputs 1 GiB >> L2, no flush needed)."""
+    import torch
+    import paper_1811_10074_b200 as P
+    from synthgen import device as SD
+    hbm_peak, peak_kind, _ = load_peaks()
+    n = 1 << 28
+    stream = torch.cuda.current_stream()
+    xu = SD.c2_u32(n)
+    xf = SD.c2_f32(n)
+    yu = torch.empty(n, dtype=torch.uint32, device="cuda")
+    yf = torch.empty(n, dtype=torch.float32, device="cuda")
+    ops = [("MIN_U32", P.SLSUM_MIN_U32, xu, yu), ("ADD_U32", P.SLSUM_ADD_U32, xu, yu),
+           ("ADD_F32", P.SLSUM_ADD_F32, xf, yf)]
+    runs, tot_ms = [], 0.0
+    with Clocks(0) as clk:
+        for name, op, x, y in ops:
+            for w in (4, 16, 64, 256, 1024):
+                for pname, path in (("generic", P.SLSUM_PATH_GENERIC), ("commutative", P.SLSUM_PATH_COMMUTATIVE)):
+                    ms = _timed(lambda: P.slsum_run(op, w, x, y[: n - w + 1], path=path), args.steps, args.warmup,
+                                stream)
+                    tot_ms += ms
+                    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+                    runs.append({"op": name, "w": w, "path": pname, "ms": ms, "gelem_s": n / (ms * 1e-3) / 1e9,
+                                 "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
+    clk_sum = clk.summary()
+    best = max(runs, key=lambda r: r["hbm_frac"])
+    gen = [r for r in runs if r["path"] == "generic"]
+    cpu = None
+    if not args.no_cpu_baseline:
+        # the oracle's strict O(wN) left fold on the same 15 (op, w) runs, first 2^23 elements each
+        import oracle as O
+        ns = 1 << 23
+        xs_u, xs_f = xu[:ns].cpu().numpy(), xf[:ns].cpu().numpy()
+        t0 = time.perf_counter()
+        for oop, xs in ((O.MIN_U32, xs_u), (O.ADD_U32, xs_u), (O.ADD_F32, xs_f)):
+            for w in (4, 16, 64, 256, 1024):
+                O.slsum(oop, w, xs)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 15 * ns / dt / 1e9, "unit": "Gelem/s", "cores": O.num_threads(), "kind": "oracle",
+               "sample": f"the 15 (op, w) runs on the first {ns} C2 elements each ({dt:.1f} s)"}
+    line = {
+        "metric": "generic sliding window sums (Eq. 2), Gelem/s", "value": len(runs) * n / (tot_ms * 1e-3) / 1e9,
+        "unit": "Gelem/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": tot_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f32",
+        "data": "synthetic",
+        "config": {"workload": "C2: 2^28 elements x {MIN_U32, ADD_U32, ADD_F32} x w {4..1024} x {generic, commutative}",
+                   "step": "all 30 runs", "l2": "inputs 1 GiB >> L2; no flush needed"},
+        "roofline": {"bound": "hbm", "kernel": f"slsum {best['path']} {best['op']} w={best['w']} (best)",
+                     "achieved": best["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": best["hbm_frac"],
+                     "traffic": None, "peak_kind": peak_kind},
+        "roofline_generic_min_frac": min(r["hbm_frac"] for r in gen),
+        "runs": runs, "cpu_baseline": cpu, "clocks": clk_sum, "gpu_launches": len(runs) * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_c4(args):
+    """C4: 1M lognormal reads, k=15 w=10; encode + segmented minimizer extraction."""
+    import torch
+    import paper_1811_10074_b200 as P
+    from synthgen import device as SD
+    from synthgen import host as H
+    hbm_peak, peak_kind, sm_max = load_peaks()
+    k, w = 15, 10
+    c4 = H.C4()
+    n = c4.n
+    seq = SD.c4_ascii(c4)
+    ro = torch.from_numpy(c4.read_off.astype(np.uint64).view(np.int64)).cuda().view(torch.uint64)
+    nw = (n + 31) // 32
+    words = torch.empty(nw + 1, dtype=torch.uint64, device="cuda")
+    inval = torch.empty(nw + 1, dtype=torch.uint32, device="cuda")
+    cap = int(0.21 * n) + 1024
+    out_h = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    out_p = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    d_count = torch.zeros(1, dtype=torch.uint64, device="cuda")
+    ws = torch.empty(P.mz_workspace_bytes(n, k, w, P.MZ_IN_PACKED2), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    ev = []
+
+    def step(record=False):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if record else None
+        if record:
+            e[0].record(stream)
+        P.mz_encode(seq, words, inval)
+        if record:
+            e[1].record(stream)
+        P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, read_off=ro, capacity=cap,
+                        out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws)
+        if record:
+            e[2].record(stream)
+            ev.append(e)
+
+    with Clocks(0) as clk:
+        ms = _timed(lambda: step(True), args.steps, args.warmup, stream)
+    m = int(d_count.view(torch.int64).item())
+    if m > cap:
+        raise RuntimeError(f"capacity {cap} < {m} records")
+    ev = ev[-args.steps:]
+    enc_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in ev)
+    mz_ms = statistics.mean(b.elapsed_time(c) for _, b, c in ev)
+    clk_sum = clk.summary()
+    sm_mhz = clk_sum.get("sm_mhz") or sm_max
+    int_peak = SM_COUNT * INT32_LANES_PER_SM_CLK * sm_mhz * 1e6 / 1e12
+    ops = MZ_INT_OPS_PER_BASE[15] * n
+    ach = ops / (mz_ms * 1e-3) / 1e12
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        r1 = 2000
+        hi = int(c4.read_off[r1])
+        s = c4.ascii_range(0, hi)
+        t0 = time.perf_counter()
+        O.mz(s, k, w, read_off=c4.read_off[: r1 + 1].astype(np.uint64))
+        dt = time.perf_counter() - t0
+        cpu = {"value": hi / dt / 1e9, "unit": "Gbases/s", "cores": O.num_threads(), "kind": "oracle",
+               "sample": f"first {r1} reads ({hi} bases) of C4 ({dt:.1f} s)"}
+    line = {
+        "metric": "minimizer extraction over a long-read batch, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
+        "unit": "Gbases/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "C4: 1M reads, lognormal(mean 10 kbp, sd 8 kbp), 10% substitutions", "k": k, "w": w,
+                   "bases": n, "reads": c4.nreads, "records": m, "density": m / n,
+                   "l2": f"inputs ({n / 1e9:.1f} GB) >> L2; no flush needed"},
+        "roofline": {"bound": "alu", "kernel": "mz_fast_kernel<10,0,15> (a2-a7 fused, read-segmented)",
+                     "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": None,
+                     "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
+                     "ops_per_base": MZ_INT_OPS_PER_BASE[15], "ms": mz_ms},
+        "hbm_step": {"encode_ms": enc_ms, "extract_ms": mz_ms,
+                     "encode_frac": n * 1.375 / (enc_ms * 1e-3) / 1e9 / hbm_peak,
+                     "extract_frac": (n * 0.375 + m * 16) / (mz_ms * 1e-3) / 1e9 / hbm_peak, "peak": hbm_peak,
+                     "peak_kind": peak_kind},
+        "cpu_baseline": cpu, "clocks": clk_sum, "gpu_launches": 2 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -159,6 +322,10 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
+    if args.config in ("c2", "c4"):
+        if world > 1 and rank != 0:
+            return 0          # secondary configs are single-GPU measurements
+        return bench_c2(args) if args.config == "c2" else bench_c4(args)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)

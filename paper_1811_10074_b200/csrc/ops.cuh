@@ -163,58 +163,54 @@ template <class Op, int TPB, int E>
 __device__ __forceinline__ void block_prefix_suffix(const typename Op::T (&v)[E], typename Op::T (&P)[E],
                                                     typename Op::T (&S)[E], uint32_t w, uint32_t a,
                                                     SegScratch<Op, TPB>& sh) {
+  static_assert(E <= 31, "head mask holds E+1 bits");
   using T = typename Op::T;
   const uint32_t e0 = threadIdx.x * E;
-  // r0 = position of element e0 inside its block (0 = block start)
-  const uint32_t r0 = (uint32_t)(((int64_t)e0 - (int64_t)a) % (int64_t)w + w) % w;
-  // forward pass
-  bool has_head = false;
+  // r0 = position of element e0 inside its block (0 = block start); 32-bit (e0 < 2^16, a < 2^32)
+  uint32_t r0 = e0 % w;
+  if (a) r0 = (r0 + w - a % w) % w;
+  // heads bit j (0 <= j <= E): element e0+j starts a block; element j ends one iff bit j+1
+  uint32_t heads = 0;
+  for (uint32_t j = r0 ? w - r0 : 0u; j <= (uint32_t)E; j += w) heads |= 1u << j;
+  constexpr uint32_t kMask = (1u << E) - 1u;
+  // forward pass: P
   {
-    uint32_t r = r0;
-    T p = Op::id();
+    T p = v[0];
+    P[0] = p;
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-      if (r == 0) has_head = true;
-      p = (r == 0 || j == 0) ? v[j] : Op::op(p, v[j]);
+    for (int j = 1; j < E; ++j) {
+      p = ((heads >> j) & 1u) ? v[j] : Op::op(p, v[j]);
       P[j] = p;
-      r = (r + 1 == w) ? 0 : r + 1;
     }
+    const bool has_head = (heads & kMask) != 0u;
     Seg<T> c = block_seg_fwd_excl<Op, TPB>(Seg<T>{has_head || threadIdx.x == 0, p}, sh);
     if (threadIdx.x > 0) {
-      uint32_t rr = r0;
-      bool open = true;
+      // elements before this thread's first head continue the block from the left
+      const uint32_t open = (heads & kMask) ? ((heads & kMask) & (0u - (heads & kMask))) - 1u : kMask;
 #pragma unroll
-      for (int j = 0; j < E; ++j) {
-        if (rr == 0) open = false;
-        if (open) P[j] = Op::op(c.v, P[j]);
-        rr = (rr + 1 == w) ? 0 : rr + 1;
-      }
+      for (int j = 0; j < E; ++j)
+        if ((open >> j) & 1u) P[j] = Op::op(c.v, P[j]);
     }
   }
-  // backward pass
+  // backward pass: S
   {
-    // position of the last element within its block
-    uint32_t rl = (r0 + (E - 1)) % w;
-    bool has_tail = false;
-    uint32_t r = rl;
-    T s = Op::id();
+    const uint32_t tails = heads >> 1;  // bit j: element j ends a block (bit E-1: next thread starts one)
+    T s = v[E - 1];
+    S[E - 1] = s;
 #pragma unroll
-    for (int j = E - 1; j >= 0; --j) {
-      if (r == w - 1) has_tail = true;
-      s = (r == w - 1 || j == E - 1) ? v[j] : Op::op(v[j], s);
+    for (int j = E - 2; j >= 0; --j) {
+      s = ((tails >> j) & 1u) ? v[j] : Op::op(v[j], s);
       S[j] = s;
-      r = (r == 0) ? w - 1 : r - 1;
     }
+    const bool has_tail = (tails & kMask) != 0u;
     Seg<T> c = block_seg_bwd_excl<Op, TPB>(Seg<T>{has_tail || threadIdx.x == TPB - 1, s}, sh);
     if (threadIdx.x < TPB - 1) {
-      uint32_t rr = rl;
-      bool open = true;
+      // elements after this thread's last tail continue into the block on the right
+      const uint32_t tm = tails & kMask;
+      const uint32_t open = tm ? (kMask & ~((2u << (31 - __clz(tm))) - 1u)) : kMask;
 #pragma unroll
-      for (int j = E - 1; j >= 0; --j) {
-        if (rr == w - 1) open = false;
-        if (open) S[j] = Op::op(S[j], c.v);
-        rr = (rr == 0) ? w - 1 : rr - 1;
-      }
+      for (int j = 0; j < E; ++j)
+        if ((open >> j) & 1u) S[j] = Op::op(S[j], c.v);
     }
   }
 }

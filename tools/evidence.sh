@@ -1,0 +1,24 @@
+#!/bin/bash
+# Collect the round's GPU evidence on a B200 box (run under gpurun from the repo root):
+#   tests, the bench lines (C3 default, C2, C4, reference arm), the ncu launch list of one C3
+#   step and one `ncu --set full` capture of the top kernels.  Outputs land in gpurun_out/ev/.
+set -u
+O=gpurun_out/ev
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt
+timeout 600 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 600 python bench.py --config c2 --steps 10 > $O/bench_c2.json 2> $O/bench_c2.err
+timeout 900 python bench.py --config c4 --steps 5 > $O/bench_c4.json 2> $O/bench_c4.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+# launch list of one timed C3 step (cold-cache, serialised: compare shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
+  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_c3.log 2>&1
+# full sections of the top kernels of the C3 step (after 3 warm-up steps) and of slsum (C2)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mz_fast|^nsweep|encode_kernel|upsweep" \
+  -s 33 -c 11 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/full_c3.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 19 -c 1 \
+  -o $O/full_c2_generic_w16 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2a.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 11 -c 1 \
+  -o $O/full_c2_doubling_w4 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2b.log 2>&1
+echo done

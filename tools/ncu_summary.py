@@ -63,14 +63,18 @@ def report(path, bases=None):
     print()
 
 
-def launches(path):
+def launches(path, last_step=None):
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     hdr = rows[start]
     iK, iV, iU = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     agg = collections.OrderedDict()
     tot = 0.0
-    for r in rows[start + 1:]:
+    body = rows[start + 1:]
+    if last_step:  # keep only the launches from the last one whose name contains `last_step`
+        cut = max(i for i, r in enumerate(body) if len(r) > iK and last_step in r[iK])
+        body = body[cut:]
+    for r in body:
         if len(r) <= iV:
             continue
         v = float(r[iV].replace(",", ""))
@@ -82,7 +86,8 @@ def launches(path):
         agg[name][0] += ms
         agg[name][1] += 1
         tot += ms
-    print(f"### launch list `{path.split('/')[-1]}` (ncu gpu__time_duration, cold-cache, serialised)\n")
+    what = f", last step (from the last `{last_step}`)" if last_step else ""
+    print(f"### launch list `{path.split('/')[-1]}` (ncu gpu__time_duration, cold-cache, serialised{what})\n")
     print("| kernel | launches | ms | share |")
     print("|---|---|---|---|")
     for k, (ms, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
@@ -95,9 +100,10 @@ if __name__ == "__main__":
     ap.add_argument("mode", choices=["report", "launches"])
     ap.add_argument("path")
     ap.add_argument("--bases", type=float, default=None)
+    ap.add_argument("--last-step", default=None, help="launches mode: keep the last step starting at this kernel")
     a = ap.parse_args()
     if a.mode == "report":
         report(a.path, a.bases)
     else:
-        launches(a.path)
+        launches(a.path, a.last_step)
     sys.exit(0)
