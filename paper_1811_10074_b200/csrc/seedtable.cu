@@ -368,7 +368,7 @@ enum { kInHashPos = 0, kInFpPos = 1, kInPk = 2 };
 enum { kOutPk = 0, kOutFpPos = 1 };
 // items ranked per round of __syncwarp (their shared-memory round trips overlap): 4 for big
 // tiles, 2 where the smaller footprint lets a third CTA fit on the SM
-template <int IPT> constexpr int peer_tables() { return IPT >= 16 ? 4 : 2; }
+template <int TPB, int IPT> constexpr int peer_tables() { return TPB >= 512 ? 1 : (IPT >= 16 ? 4 : 2); }
 
 __global__ void ctl_kernel(const uint64_t* pos, const uint64_t* d_m, uint64_t m_cap, uint64_t* ctl) {
   if (threadIdx.x != 0) return;
@@ -406,8 +406,8 @@ struct NSmem {
   uint64_t gbase[256];       // staged entry j of digit d goes to gbase[d] + j
   uint32_t wcnt[NW][256];    // per-warp digit counters -> per-warp exclusive offsets
   uint32_t dummy[NW][32];    // atomic targets of non-leader lanes (branch-free ranking)
-  uint32_t pm[NW][peer_tables<T / TPB>()][256];  // per-warp peer bit tables
-  uint32_t ws2[NW];
+  uint32_t pm[NW][peer_tables<TPB, T / TPB>()][256];  // per-warp peer bit tables
+  uint32_t ws2[NW > 8 ? NW : 8];  // per-warp digit-scan totals
 };
 
 template <int IN, int T>
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
   if (cbase >= m) return;
   if (td < 256) S.run_off[td] = dbase[td] + offsets[(uint64_t)td * nchunks + c];
   for (uint32_t i = td; i < NW * 256; i += TPB) (&S.wcnt[0][0])[i] = 0;
-  constexpr int kPeerTables = peer_tables<IPT>();
+  constexpr int kPeerTables = peer_tables<TPB, IPT>();
   for (uint32_t i = td; i < NW * kPeerTables * 256; i += TPB) (&S.pm[0][0][0])[i] = 0;
   if (td == 0) {
     for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
@@ -593,20 +593,31 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
         run += cnt[w];
       }
     }
-    {
-      uint32_t tot;
-      const uint32_t ex = block_exclusive_sum<TPB, uint32_t>(td < 256 ? run : 0u, S.ws2, &tot);
-      if (td < 256) {
-        uint32_t acc = ex;
+    // exclusive scan of the 256 digit totals with one barrier: warps 0..7 own 32 digits each
+    uint32_t incl = run;
+    if (td < 256) {
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          S.wcnt[w][td] = acc;
-          acc += cnt[w];
-        }
-        const uint64_t r0 = S.run_off[td];
-        S.gbase[td] = r0 - ex;
-        S.run_off[td] = r0 + run;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += y;
       }
+      if (lane == 31) S.ws2[wid] = incl;
+    }
+    __syncthreads();
+    if (td < 256) {
+      uint32_t ex = incl - run;
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        if (v < (int)wid) ex += S.ws2[v];
+      uint32_t acc = ex;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        S.wcnt[w][td] = acc;
+        acc += cnt[w];
+      }
+      const uint64_t r0 = S.run_off[td];
+      S.gbase[td] = r0 - ex;
+      S.run_off[td] = r0 + run;
     }
     __syncthreads();
     MZS_PROF_MARK(3);
