@@ -103,59 +103,137 @@ __global__ void __launch_bounds__(TPB) slsum_generic_kernel(const typename Op::T
   }
 }
 
+// Doubling rounds over a tile of L inputs held in two ping-pong shared buffers.  Every step of
+// the rounds, loads and stores works on 16-byte vectors of OV = 16/sizeof(T) consecutive
+// elements (one LDS.128 of A[e..], one of A[e+d..] when d is a multiple of OV, otherwise the
+// shifted vector is assembled from two aligned ones; one STS.128), so a round costs a few
+// instructions per element.  Interior tiles are loaded and stored with 16-byte global accesses.
+template <class T, uint32_t OV, uint32_t R>
+__device__ __forceinline__ void take_shifted(const T (&lo)[OV], const T (&hi)[OV], T (&o)[OV]) {
+#pragma unroll
+  for (uint32_t q = 0; q < OV; ++q) o[q] = (R + q < OV) ? lo[R + q] : hi[R + q - OV];
+}
+// o[q] = A[e + d + q] for e a multiple of OV: one or two aligned 16-byte loads; the shift
+// r = d mod OV is uniform across the CTA, so the switch does not diverge
+template <class T, uint32_t OV>
+__device__ __forceinline__ void ld_shifted(const T* A, uint32_t e, uint32_t d, T (&o)[OV]) {
+  const uint32_t base = e + d, r = base % OV, a0 = base - r;
+  T lo[OV], hi[OV];
+  *reinterpret_cast<uint4*>(lo) = *reinterpret_cast<const uint4*>(A + a0);
+  if (r == 0) {
+#pragma unroll
+    for (uint32_t q = 0; q < OV; ++q) o[q] = lo[q];
+    return;
+  }
+  *reinterpret_cast<uint4*>(hi) = *reinterpret_cast<const uint4*>(A + a0 + OV);
+  if constexpr (OV == 4) {
+    if (r == 1) take_shifted<T, OV, 1>(lo, hi, o);
+    else if (r == 2) take_shifted<T, OV, 2>(lo, hi, o);
+    else take_shifted<T, OV, 3>(lo, hi, o);
+  } else {
+    take_shifted<T, OV, 1>(lo, hi, o);
+  }
+}
+
 template <class Op, int TPB>
 __global__ void __launch_bounds__(TPB) slsum_doubling_kernel(const typename Op::T* __restrict__ x,
                                                             typename Op::T* __restrict__ y, uint64_t n,
                                                             uint32_t w, uint64_t nout, uint32_t L,
                                                             uint32_t tout) {
   using T = typename Op::T;
+  constexpr uint32_t OV = 16 / sizeof(T);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* A = reinterpret_cast<T*>(smem_raw);
-  T* B = A + L;
+  T* B = A + L + 2 * OV;  // (+2 vectors: shifted reads past L stay inside the buffer)
   const uint64_t g0 = (uint64_t)blockIdx.x * tout;
-  for (uint32_t e = threadIdx.x; e < L; e += TPB) A[e] = (g0 + e < n) ? x[g0 + e] : Op::id();
+  const uint32_t t = threadIdx.x;
+  const bool vin = ((reinterpret_cast<uintptr_t>(x + g0) & 15) == 0) && g0 + L <= n;
+  if (vin) {
+    for (uint32_t e = t * OV; e < L; e += TPB * OV)
+      *reinterpret_cast<uint4*>(A + e) = __ldg(reinterpret_cast<const uint4*>(x + g0 + e));
+  } else {
+    for (uint32_t e = t; e < L; e += TPB) A[e] = (g0 + e < n) ? x[g0 + e] : Op::id();
+  }
+  for (uint32_t e = L + t; e < L + 2 * OV; e += TPB) A[e] = Op::id();
   __syncthreads();
   // m = floor(log2 w)
   const int m = 31 - __clz(w);
+  const uint32_t e_end = (uint32_t)min((uint64_t)tout, nout - g0);
+  const bool vout = ((reinterpret_cast<uintptr_t>(y + g0) & 15) == 0) && e_end == tout;
   if (Op::kIdempotent) {
     for (int r = 0; r < m; ++r) {
       const uint32_t d = 1u << r;
-      for (uint32_t e = threadIdx.x; e + d < L; e += TPB) B[e] = Op::op(A[e], A[e + d]);
+      for (uint32_t e = t * OV; e + d < L; e += TPB * OV) {
+        T a[OV], c[OV], o[OV];
+        *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(A + e);
+        ld_shifted<T, OV>(A, e, d, c);
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q) o[q] = Op::op(a[q], c[q]);
+        *reinterpret_cast<uint4*>(B + e) = *reinterpret_cast<const uint4*>(o);
+      }
       __syncthreads();
       T* tmp = A; A = B; B = tmp;
     }
     const uint32_t d = w - (1u << m);
-    for (uint32_t e = threadIdx.x; e < tout; e += TPB) {
-      if (g0 + e >= nout) break;
-      y[g0 + e] = d ? Op::op(A[e], A[e + d]) : A[e];
+    if (vout) {
+      for (uint32_t e = t * OV; e < tout; e += TPB * OV) {
+        T a[OV], c[OV], o[OV];
+        *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(A + e);
+        ld_shifted<T, OV>(A, e, d, c);
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q) o[q] = d ? Op::op(a[q], c[q]) : a[q];
+        *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(o);
+      }
+    } else {
+      for (uint32_t e = t; e < e_end; e += TPB) y[g0 + e] = d ? Op::op(A[e], A[e + d]) : A[e];
     }
   } else {
     // binary digits of w, smallest piece leftmost: y_i = t_c0[i] (+) t_c1[i+2^c0] (+) ...
-    constexpr int NACC = 8;  // outputs per thread held in registers (tout <= 8*TPB, host-enforced)
-    T acc[NACC];
+    constexpr int NV = 8 / (int)OV;  // output vectors per thread: 8 outputs (tout = 8*TPB, host-enforced)
+    T acc[NV][OV];
 #pragma unroll
-    for (int j = 0; j < NACC; ++j) acc[j] = Op::id();
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+      for (uint32_t q = 0; q < OV; ++q) acc[j][q] = Op::id();
     uint32_t off = 0;
     for (int r = 0; r <= m; ++r) {
       if ((w >> r) & 1u) {
 #pragma unroll
-        for (int j = 0; j < NACC; ++j) {
-          const uint32_t e = threadIdx.x + j * TPB;
-          if (e < tout) acc[j] = Op::op(acc[j], A[e + off]);
+        for (int j = 0; j < NV; ++j) {
+          const uint32_t e = (t + j * TPB) * OV;
+          if (e < tout) {
+            T c[OV];
+            ld_shifted<T, OV>(A, e, off, c);
+#pragma unroll
+            for (uint32_t q = 0; q < OV; ++q) acc[j][q] = Op::op(acc[j][q], c[q]);
+          }
         }
         off += 1u << r;
       }
       if (r < m) {
         const uint32_t d = 1u << r;
-        for (uint32_t e = threadIdx.x; e + d < L; e += TPB) B[e] = Op::op(A[e], A[e + d]);
+        for (uint32_t e = t * OV; e + d < L; e += TPB * OV) {
+          T a[OV], c[OV], o[OV];
+          *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(A + e);
+          ld_shifted<T, OV>(A, e, d, c);
+#pragma unroll
+          for (uint32_t q = 0; q < OV; ++q) o[q] = Op::op(a[q], c[q]);
+          *reinterpret_cast<uint4*>(B + e) = *reinterpret_cast<const uint4*>(o);
+        }
         __syncthreads();
         T* tmp = A; A = B; B = tmp;
       }
     }
 #pragma unroll
-    for (int j = 0; j < NACC; ++j) {
-      const uint32_t e = threadIdx.x + j * TPB;
-      if (e < tout && g0 + e < nout) y[g0 + e] = acc[j];
+    for (int j = 0; j < NV; ++j) {
+      const uint32_t e = (t + j * TPB) * OV;
+      if (vout) {
+        if (e < tout) *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(acc[j]);
+      } else {
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q)
+          if (e + q < e_end) y[g0 + e + q] = acc[j][q];
+      }
     }
   }
 }
@@ -202,7 +280,7 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
   if (2 * sizeof(T) * Lw > 200 * 1024) return SLSUM_EUNSUPPORTED;  // w > ~21500 (4-byte)
   const uint32_t L = (uint32_t)Lw;
   const uint64_t grid = (nout + tout - 1) / tout;
-  const size_t smem = 2 * sizeof(T) * (size_t)L;
+  const size_t smem = 2 * sizeof(T) * ((size_t)L + 2 * (16 / sizeof(T)));
   auto k = slsum_doubling_kernel<Op, TPB>;
   MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const typename Op::T*>(xv), static_cast<typename Op::T*>(yv),
