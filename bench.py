@@ -189,7 +189,10 @@ def bench_c2(args):
     with Clocks(0) as clk:
         for name, op, x, y in ops:
             for w in (4, 16, 64, 256, 1024):
-                for pname, path in (("generic", P.SLSUM_PATH_GENERIC), ("commutative", P.SLSUM_PATH_COMMUTATIVE)):
+                paths = [("generic", P.SLSUM_PATH_GENERIC), ("commutative", P.SLSUM_PATH_COMMUTATIVE)]
+                if op == P.SLSUM_ADD_U32:   # the invertible op also has the recurrent path (NEXT f2)
+                    paths.append(("recurrent", P.SLSUM_PATH_RECURRENT))
+                for pname, path in paths:
                     ms = _timed(lambda: P.slsum_run(op, w, x, y[: n - w + 1], path=path), args.steps, args.warmup,
                                 stream)
                     tot_ms += ms
@@ -217,8 +220,9 @@ def bench_c2(args):
         "unit": "Gelem/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": tot_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f32",
         "data": "synthetic",
-        "config": {"workload": "C2: 2^28 elements x {MIN_U32, ADD_U32, ADD_F32} x w {4..1024} x {generic, commutative}",
-                   "step": "all 30 runs", "l2": "inputs 1 GiB >> L2; no flush needed"},
+        "config": {"workload": "C2: 2^28 elements x {MIN_U32, ADD_U32, ADD_F32} x w {4..1024} x {generic, commutative}"
+                               " (+ recurrent for ADD_U32)",
+                   "step": f"all {len(runs)} runs", "l2": "inputs 1 GiB >> L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": f"slsum {best['path']} {best['op']} w={best['w']} (best)",
                      "achieved": best["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": best["hbm_frac"],
                      "traffic": None, "peak_kind": peak_kind},

@@ -75,6 +75,12 @@ int slsum_version(void);
  *                           sum with commutative operator"); rejects AFFINE with
  *                           SLSUM_EUNSUPPORTED.
  *   SLSUM_PATH_AUTO         GENERIC (the faster path on B200 for every w).
+ *   SLSUM_PATH_RECURRENT    Conclusion (L229): a "recurrent interpretation", speedup
+ *                           independent of w.  For an invertible op, y_i = PS[i+w-1] (-)
+ *                           PS[i-1] with PS the prefix sums (tile-local; the difference
+ *                           cancels the offset).  SLSUM_ADD_U32 only (exact mod 2^32); any
+ *                           other op returns SLSUM_EUNSUPPORTED (min/max are not invertible,
+ *                           f32 add would lose the tolerance to cancellation).
  * x, y: device arrays of n and max(0, n-w+1) elements; x and y must not overlap.
  */
 enum {
@@ -85,7 +91,7 @@ enum {
   SLSUM_AFFINE_U32X2 = 4,
   SLSUM_MIN_U64 = 5
 };
-enum { SLSUM_PATH_GENERIC = 0, SLSUM_PATH_COMMUTATIVE = 1, SLSUM_PATH_AUTO = 2 };
+enum { SLSUM_PATH_GENERIC = 0, SLSUM_PATH_COMMUTATIVE = 1, SLSUM_PATH_AUTO = 2, SLSUM_PATH_RECURRENT = 3 };
 
 /* GENERIC path on the default stream; returns after completion. */
 int slsum_run(int op, uint32_t w, const void* x, void* y, uint64_t n);

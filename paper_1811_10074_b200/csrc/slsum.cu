@@ -289,6 +289,104 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
   return SLSUM_OK;
 }
 
+
+// RECURRENT path (Conclusion: sums with a "recurrent interpretation" run at a
+// speedup independent of w): for an invertible (+) -- here uint32 add, exact mod 2^32 --
+//   y_i = PS[i+w-1] (-) PS[i-1],   PS = the prefix sums.
+// The prefix sums are tile-local (the tile's first element starts them); the difference
+// cancels the offset, so no cross-tile scan is needed.  One scan plus one subtraction per
+// element, whatever w is.
+template <int TPB, int E>
+__global__ void __launch_bounds__(TPB) slsum_prefixdiff_kernel(const uint32_t* __restrict__ x, uint32_t* __restrict__ y,
+                                                              uint64_t n, uint32_t w, uint64_t nout, uint32_t tout) {
+  constexpr uint32_t L = TPB * E;
+  constexpr uint32_t NW = TPB / 32;
+  constexpr uint32_t OV = 4, G = 32;
+  auto sidx = [](uint32_t i) { return i + OV * (i / G); };
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* sPS = reinterpret_cast<uint32_t*>(smem_raw);
+  __shared__ uint32_t wsum[NW];
+  const uint64_t g0 = (uint64_t)blockIdx.x * tout;
+  const uint32_t t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  uint32_t v[E];
+  {
+    const uint64_t g = g0 + (uint64_t)t * E;
+    if (g + E <= n && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < E / 4; ++q) *reinterpret_cast<uint4*>(v + 4 * q) = __ldg(reinterpret_cast<const uint4*>(x + g) + q);
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) v[j] = (g + j < n) ? x[g + j] : 0u;
+    }
+  }
+  // inclusive scan: serial in the thread, then warp shuffles, then over warps
+#pragma unroll
+  for (int j = 1; j < E; ++j) v[j] += v[j - 1];
+  uint32_t s = v[E - 1];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= (unsigned)o) s += u;
+  }
+  if (lane == 31) wsum[wid] = s;
+  __syncthreads();
+  uint32_t base = s - v[E - 1];
+#pragma unroll
+  for (uint32_t q = 0; q < NW; ++q)
+    if (q < wid) base += wsum[q];
+  {
+    const uint32_t b0 = sidx(t * E);
+#pragma unroll
+    for (int q = 0; q < E; q += 4) {
+      uint4 o4 = make_uint4(v[q] + base, v[q + 1] + base, v[q + 2] + base, v[q + 3] + base);
+      *reinterpret_cast<uint4*>(sPS + b0 + q) = o4;
+    }
+  }
+  __syncthreads();
+  const uint32_t e_end = (uint32_t)min((uint64_t)tout, nout - g0);
+  uint32_t e_scalar = 0;
+  if ((reinterpret_cast<uintptr_t>(y + g0) & 15) == 0) {
+    for (uint32_t e = t * OV; e + OV <= e_end; e += TPB * OV) {
+      uint32_t o[OV];
+#pragma unroll
+      for (uint32_t q = 0; q < OV; ++q) {
+        const uint32_t i = e + q;
+        o[q] = sPS[sidx(i + w - 1)] - (i ? sPS[sidx(i - 1)] : 0u);
+      }
+      *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(o);
+    }
+    e_scalar = e_end / OV * OV;
+  }
+  for (uint32_t i = e_scalar + t; i < e_end; i += TPB) y[g0 + i] = sPS[sidx(i + w - 1)] - (i ? sPS[sidx(i - 1)] : 0u);
+}
+
+int launch_prefixdiff(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  constexpr int E = 16;
+  const uint64_t nout = n - w + 1;
+  int tpb = 256;
+  while (tpb < 1024 && (uint64_t)(w - 1) * 8 > (uint64_t)tpb * E) tpb *= 2;
+  const uint32_t L = tpb * E;
+  if (w - 1 >= L / 2) return SLSUM_EUNSUPPORTED;
+  uint32_t tout = (L - (w - 1)) & ~31u;
+  if (tout == 0) tout = L - (w - 1);
+  const uint64_t grid = (nout + tout - 1) / tout;
+  const size_t smem = sizeof(uint32_t) * slsum_smem_len<uint32_t>(L);
+  const uint32_t* x = static_cast<const uint32_t*>(xv);
+  uint32_t* y = static_cast<uint32_t*>(yv);
+#define MZS_PD(TPB_)                                                                           \
+  do {                                                                                         \
+    auto k = slsum_prefixdiff_kernel<TPB_, E>;                                                 \
+    MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k<<<(unsigned)grid, TPB_, smem, st>>>(x, y, n, w, nout, tout);                            \
+  } while (0)
+  if (tpb == 256) MZS_PD(256);
+  else if (tpb == 512) MZS_PD(512);
+  else MZS_PD(1024);
+#undef MZS_PD
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 }  // namespace
 }  // namespace mzs
 
@@ -296,11 +394,17 @@ using namespace mzs;
 
 MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n, int path, void* stream) {
   if (w == 0 || op < SLSUM_MIN_U32 || op > SLSUM_MIN_U64) return SLSUM_EINVAL;
-  if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_AUTO) return SLSUM_EINVAL;
+  if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_RECURRENT) return SLSUM_EINVAL;
   if (n < w) return SLSUM_OK;  // zero outputs (not an error)
   if (!x || !y) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
   if (path == SLSUM_PATH_AUTO) path = SLSUM_PATH_GENERIC;
+  if (path == SLSUM_PATH_RECURRENT) {
+    // invertible (+) only: uint32 add (exact).  min/max have no inverse; f32 add loses the
+    // tolerance to cancellation (4-53x over); the affine maps are not all invertible.
+    if (op != SLSUM_ADD_U32) return SLSUM_EUNSUPPORTED;
+    return launch_prefixdiff(x, y, n, w, st);
+  }
   if (path == SLSUM_PATH_GENERIC) {
     switch (op) {
       case SLSUM_MIN_U32: return launch_generic<OpMinU32>(x, y, n, w, st);

@@ -64,6 +64,35 @@ def test_commutative_vs_oracle(op, w):
         _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_COMMUTATIVE))
 
 
+@pytest.mark.parametrize("w", WS + [4095, 4096, 4097, 8000])
+def test_recurrent_vs_oracle(w):
+    """RECURRENT path (Conclusion): prefix differences for the invertible u32 add,
+    bit-exact vs the strict left fold, across several tiles and a ragged tail."""
+    rng = np.random.default_rng(4242 + w)
+    for n in sorted({w, w + 1, 2 * w + 3, 5000, 70_001, 3 * 4096 + 17}):
+        if n < w:
+            continue
+        x = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)
+        _check(P.SLSUM_ADD_U32, w, x, _run(P.SLSUM_ADD_U32, w, x, P.SLSUM_PATH_RECURRENT))
+    # unaligned output and input views take the scalar loads / stores
+    x = rng.integers(0, 2 ** 32, size=20_000, dtype=np.uint64).astype(np.uint32)
+    xt = torch.from_numpy(np.concatenate([[0], x]).astype(np.uint32)).cuda()[1:]
+    yb = torch.empty(20_000 - w + 2, dtype=torch.uint32, device="cuda")
+    if w <= 20_000:
+        y = P.slsum_run(P.SLSUM_ADD_U32, w, xt, y=yb[1:], path=P.SLSUM_PATH_RECURRENT)
+        assert np.array_equal(y.cpu().numpy(), O.slsum(O.ADD_U32, w, x))
+
+
+@pytest.mark.parametrize("op", [o for o, _ in OPS if o != P.SLSUM_ADD_U32])
+def test_recurrent_rejects_non_invertible(op):
+    x = torch.zeros((100, 2) if op == P.SLSUM_AFFINE_U32X2 else (100,),
+                    dtype={P.SLSUM_ADD_F32: torch.float32, P.SLSUM_MIN_U64: torch.uint64}.get(op, torch.uint32),
+                    device="cuda")
+    with pytest.raises(P.SlsumError) as e:
+        P.slsum_run(op, 4, x, path=P.SLSUM_PATH_RECURRENT)
+    assert e.value.rc == P.SLSUM_EUNSUPPORTED
+
+
 def test_affine_rejected_by_commutative_path():
     x = torch.zeros((100, 2), dtype=torch.uint32, device="cuda")
     with pytest.raises(P.SlsumError) as e:
@@ -94,7 +123,8 @@ def test_c2_full_size_sampled(w):
     idx = np.concatenate([[0, n - w], rng.integers(0, n - w + 1, size=200)])
     it = torch.from_numpy(idx).cuda()
     for op in (P.SLSUM_MIN_U32, P.SLSUM_ADD_U32):
-        for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE):
+        paths = (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE) + ((P.SLSUM_PATH_RECURRENT,) if op == P.SLSUM_ADD_U32 else ())
+        for path in paths:
             y = P.slsum_run(op, w, xu, path=path)
             ys = y.view(torch.int32)[it].cpu().numpy().view(np.uint32)
             for j, i in enumerate(idx):
