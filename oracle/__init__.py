@@ -22,6 +22,8 @@ Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
                 instance, SPEC.md examples, numpy argmin brute force, exhaustive
                 4^L strings, density band (L85), invariants.
   * orc_seedtable  sort-based construction (Python sorted), partition property.
+  * orc_lookup  SPEC S:L327-330 examples, a Python dict of every stored seed, the partition
+                property (looking up every stored seed reproduces the table).
 """
 from __future__ import annotations
 
@@ -68,6 +70,8 @@ def lib():
         L.orc_fingerprint.restype = u32
         L.orc_seedtable.argtypes = [vp, vp, u64, i32, i32, vp, vp, vp]
         L.orc_seedtable.restype = i32
+        L.orc_lookup.argtypes = [vp, u64, i32, i32, vp, vp, vp, vp, vp, u64]
+        L.orc_lookup.restype = i64
         L.orc_num_threads.restype = i32
         L.orc_set_num_threads.argtypes = [i32]
         _lib = L
@@ -175,6 +179,22 @@ def mz(seq, k: int, w: int, read_off=None, keymode: int = KEY_HASH, pos_base: in
 
 def fingerprint(key: int, k: int) -> int:
     return int(lib().orc_fingerprint(key, k))
+
+
+def lookup(q: np.ndarray, k: int, bits: int, offsets: np.ndarray, fp: np.ndarray, pos_tab: np.ndarray):
+    """Seed lookup (Fig. 1, L63-65; NEXT f1): returns (hit_off[nq+1], hit_pos[total])."""
+    q = np.ascontiguousarray(q, dtype=np.uint64)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    fp = np.ascontiguousarray(fp, dtype=np.uint32)
+    pos_tab = np.ascontiguousarray(pos_tab, dtype=np.uint64)
+    nq = len(q)
+    hit_off = np.zeros(nq + 1, np.uint64)
+    tot = lib().orc_lookup(_p(q), nq, k, bits, _p(offsets), _p(fp), _p(pos_tab), _p(hit_off), None, 0)
+    if tot < 0:
+        raise ValueError(f"orc_lookup: error {tot}")
+    hit_pos = np.zeros(max(1, tot), np.uint64)
+    lib().orc_lookup(_p(q), nq, k, bits, _p(offsets), _p(fp), _p(pos_tab), _p(hit_off), _p(hit_pos), tot)
+    return hit_off, hit_pos[:tot]
 
 
 def seedtable(key: np.ndarray, pos: np.ndarray, k: int, bits: int):

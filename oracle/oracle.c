@@ -385,3 +385,43 @@ int orc_seedtable(const uint64_t* key, const uint64_t* pos, uint64_t m, int k, i
     free(cursor);
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------- */
+/* Seed lookup (Sec. 2.4, Fig. 1: "lookups to 'CG' and 'CT'"; NEXT f1) */
+/* ---------------------------------------------------------------------- */
+/*
+ * For every query key q[i]: f = fingerprint(q[i]), b = f >> (32 - bits); the hits of q[i]
+ * are the table entries e in b's slice [offsets[b], offsets[b+1]) with fp[e] == f, in table
+ * order (ascending position).  When 2k <= 32 the fingerprint is the whole key, so the hits
+ * are exactly the stored positions of that seed (R30).
+ * hit_off[nq + 1]: hit_off[i] = number of hits of queries < i.  hit_pos[cap]: the hits of
+ * query i at hit_off[i] ..; hits beyond cap are counted but not written.
+ * Returns the total number of hits, or a negative error.
+ */
+int64_t orc_lookup(const uint64_t* q, uint64_t nq, int k, int bits, const uint64_t* offsets,
+                   const uint32_t* fp, const uint64_t* pos_tab, uint64_t* hit_off,
+                   uint64_t* hit_pos, uint64_t cap) {
+    if (k < 1 || k > 31 || bits < 1 || bits > 30 || bits > 2 * k) return ORC_EINVAL;
+    /* counts, one query at a time */
+    hit_off[0] = 0;
+    for (uint64_t i = 0; i < nq; i++) {
+        uint32_t f = orc_fingerprint(q[i], k);
+        uint64_t b = f >> (32 - bits);
+        uint64_t c = 0;
+        for (uint64_t e = offsets[b]; e < offsets[b + 1]; e++) c += (fp[e] == f);
+        hit_off[i + 1] = hit_off[i] + c;
+    }
+    /* positions (independent per query) */
+    #pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t i = 0; i < (int64_t)nq; i++) {
+        uint32_t f = orc_fingerprint(q[i], k);
+        uint64_t b = f >> (32 - bits);
+        uint64_t o = hit_off[i];
+        for (uint64_t e = offsets[b]; e < offsets[b + 1]; e++)
+            if (fp[e] == f) {
+                if (o < cap) hit_pos[o] = pos_tab[e];
+                o++;
+            }
+    }
+    return (int64_t)hit_off[nq];
+}
