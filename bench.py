@@ -20,6 +20,9 @@ Secondary configs (not the driver's default line; their JSON lines are kept unde
                 Gelem/s and the HBM roofline per run (8 B algorithmic traffic per element).
   --config c4   BASELINE configs[3]: 1M long reads (9.98e9 bases), k=15 w=10, segmented
                 minimizer extraction (encode + mz_extract_ex with read offsets), Gbases/s.
+  --config lookup  SURVEY NEXT f1: seed lookup of the minimizers of the first 100k C4 reads
+                against the seed table (2^28 buckets) of their 2^30-base template, k=15 w=10;
+                Gqueries/s of seedtable_lookup (count + scan + emit).
 """
 from __future__ import annotations
 
@@ -51,7 +54,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4", "lookup"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-bases", type=int, default=32_000_000)
@@ -314,6 +317,88 @@ def bench_c4(args):
     return 0
 
 
+def bench_lookup(args):
+    """NEXT f1: batch seed lookup (Fig. 1 lookups) of read minimizers against a template table."""
+    import torch
+    import paper_1811_10074_b200 as P
+    from synthgen import device as SD
+    from synthgen import host as H
+    hbm_peak, peak_kind, _ = load_peaks()
+    # 2^28 buckets (offsets 2 GiB): minimizer hashes are skewed low, so with 2^24 buckets a query
+    # scans ~120 fingerprints of its (size-biased) bucket; at 2^28 about 8 (DESIGN.md R30)
+    k, w, bits = 15, 10, 28
+    nq_reads = 100_000
+    c4 = H.C4()
+    tn = c4.tlen
+    # template table (untimed): encode + minimizers + seed table, all through the library
+    tmpl = SD.c1_ascii(tn, seed=c4.seed_t)
+    tw, ti = P.mz_encode(tmpl)
+    th, tp, tc = P.mz_extract_ex(tw, k, w, n=tn, kind=P.MZ_IN_PACKED2, invalid=ti, capacity=int(0.25 * tn))
+    torch.cuda.synchronize()
+    mt = int(tc.view(torch.int64).item())
+    off, pos_tab, fp = P.seedtable_build(th[:mt], tp[:mt], k, bits)
+    del tmpl, tw, ti, th, tp
+    # queries (untimed): minimizers of the first 100k reads
+    seq = SD.c4_ascii(c4)
+    nb = int(c4.read_off[nq_reads])
+    ro = torch.from_numpy(c4.read_off[: nq_reads + 1].astype(np.int64)).cuda().view(torch.uint64)
+    qh, qp, qc = P.mz_extract_ex(seq[:nb], k, w, read_off=ro, capacity=int(0.25 * nb))
+    torch.cuda.synchronize()
+    nq = int(qc.view(torch.int64).item())
+    del seq
+    q = qh[:nq]
+    hit_off = torch.empty(nq + 1, dtype=torch.uint64, device="cuda")
+    d_total = torch.zeros(1, dtype=torch.uint64, device="cuda")
+    ws = torch.empty(P.seedtable_lookup_workspace_bytes(nq), dtype=torch.uint8, device="cuda")
+    P.seedtable_lookup(q, k, bits, off, fp, pos_tab, hit_off=hit_off, d_total=d_total, hit_cap=0, ws=ws)
+    torch.cuda.synchronize()
+    hits = int(d_total.view(torch.int64).item())
+    hit_pos = torch.empty(max(1, hits), dtype=torch.uint64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.seedtable_lookup(q, k, bits, off, fp, pos_tab, hit_off=hit_off, hit_pos=hit_pos, hit_cap=hits,
+                           d_total=d_total, ws=ws)
+
+    with Clocks(0) as clk:
+        ms = _timed(step, args.steps, args.warmup, stream)
+    clk_sum = clk.summary()
+    mean_slice = mt / (1 << bits)
+    # algorithmic bytes per query: key 8, two offsets 16, the bucket's fingerprints 4/entry,
+    # its CSR offset written + read 16, and per hit its position read + written 16 -- count
+    # and emit both read key, offsets and fingerprints (2 passes)
+    alg = nq * (2 * (8 + 16 + 4 * mean_slice) + 16) + hits * 16
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        ts = 1 << 25                                   # a 32 Mbp template prefix for the oracle table
+        tk, tpp = O.mz(H.c1_ascii(ts, seed=c4.seed_t), k, w)
+        to, tf, tpt = O.seedtable(tk, tpp, k, bits)
+        qs = q[: 40_000_000].cpu().numpy()
+        t0 = time.perf_counter()
+        O.lookup(qs, k, bits, to, tf, tpt)
+        dt = time.perf_counter() - t0
+        cpu = {"value": len(qs) / dt / 1e9, "unit": "Gqueries/s", "cores": O.num_threads(), "kind": "oracle",
+               "sample": f"{len(qs)} of the queries against the oracle's table of a {ts}-base template prefix "
+                         f"({dt:.1f} s)"}
+    line = {
+        "metric": "seed lookup (Fig. 1) of read minimizers against a template seed table, Gqueries/s",
+        "value": nq / (ms * 1e-3) / 1e9, "unit": "Gqueries/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"minimizers of the first {nq_reads} C4 reads vs the 2^30-base C4 template table",
+                   "k": k, "w": w, "bucket_bits": bits, "queries": nq, "table_entries": mt, "hits": hits,
+                   "hits_per_query": hits / max(1, nq), "l2": "table (>1.6 GB) >> L2; no flush needed"},
+        "roofline": {"bound": "hbm", "kernel": "lookup_kernel count + emit, scan (one step)",
+                     "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": alg / (ms * 1e-3) / 1e9 / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                     "algorithmic_bytes": alg},
+        "cpu_baseline": cpu, "clocks": clk_sum, "gpu_launches": 5 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -326,10 +411,10 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if args.config in ("c2", "c4"):
+    if args.config in ("c2", "c4", "lookup"):
         if world > 1 and rank != 0:
             return 0          # secondary configs are single-GPU measurements
-        return bench_c2(args) if args.config == "c2" else bench_c4(args)
+        return {"c2": bench_c2, "c4": bench_c4, "lookup": bench_lookup}[args.config](args)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)

@@ -208,6 +208,29 @@ int seedtable_finalize(const uint32_t* recv_fp, const uint64_t* recv_pos, uint64
                        uint64_t* offsets_local, uint64_t* pos_out, uint32_t* fp_out,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------ seed lookup
+ * Fig. 1 (L63-65): "The seed pointer table enables fast lookups to 'CG' and 'CT'" -- the
+ * seeding step that consumes the table.  For query key qkey[i] (a 2k-bit
+ * hash, or a raw code for a raw table): f = fp(qkey[i]), b = f >> (32 - bucket_bits); its
+ * hits are the entries e of bucket b's slice [offsets[b], offsets[b+1]) with fp[e] == f,
+ * in table order (ascending position).  When 2k <= 32 the fingerprint is the whole key and
+ * the hits are exactly the stored positions of that seed; for 2k > 32 they are the
+ * entries that agree on the key's top 32 bits (R30).
+ * offsets/fp/pos_tab: a table from seedtable_build (fp_out must have been requested).
+ * nq: number of queries, or its upper bound when d_nq (device) holds the count.
+ * hit_off[nq + 1] (uint64, device): hit_off[i] = hits of the queries before i;
+ *   hit_off[count] = total.  hit_pos[hit_cap]: the hits of query i at hit_off[i]...; hits at
+ *   or beyond hit_cap are counted, not written (hit_cap = 0: count only, hit_pos may be NULL).
+ * d_total (device, may be NULL): the total number of hits.
+ * Asynchronous on `stream`; scratch from ws (seedtable_lookup_workspace_bytes), or an
+ * internal cudaMallocAsync when ws == NULL.
+ */
+size_t seedtable_lookup_workspace_bytes(uint64_t nq);
+int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* d_nq, int k, int bucket_bits,
+                     const uint64_t* offsets, const uint32_t* fp, const uint64_t* pos_tab,
+                     uint64_t* hit_off, uint64_t* hit_pos, uint64_t hit_cap, uint64_t* d_total,
+                     void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,12 +75,14 @@ _st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
 _st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
 _st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _st_fin_ws = _sig("seedtable_finalize_workspace_bytes", _sz, _u64, _i32, _i32)
+_st_lk_ws = _sig("seedtable_lookup_workspace_bytes", _sz, _u64)
+_st_lk = _sig("seedtable_lookup", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _sz, _vp)
 _st_fin = _sig("seedtable_finalize", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 
 EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_encode", "mz_workspace_bytes",
            "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_count",
            "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
-           "seedtable_finalize"]
+           "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup"]
 
 
 def strerror(rc: int) -> str:
@@ -210,6 +212,37 @@ def seedtable_build(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *
     _check(_st_build(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out), _ptr(pos_out),
                      _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build")
     return offsets, pos_out, fp_out
+
+
+def seedtable_lookup_workspace_bytes(nq: int) -> int:
+    return int(_st_lk_ws(nq))
+
+
+def seedtable_lookup(qkey: torch.Tensor, k: int, bits: int, offsets: torch.Tensor, fp: torch.Tensor,
+                     pos_tab: torch.Tensor, *, nq: int | None = None, d_nq: torch.Tensor | None = None,
+                     hit_cap: int | None = None, hit_off: torch.Tensor | None = None,
+                     hit_pos: torch.Tensor | None = None, d_total: torch.Tensor | None = None,
+                     ws: torch.Tensor | None = None, stream=None):
+    """Batch seed lookup (Fig. 1).  Returns (hit_off[nq+1], hit_pos, d_total).  With
+    hit_cap=None the hits are counted first and hit_pos is sized from the total (one sync)."""
+    if nq is None:
+        nq = qkey.numel()
+    dev = qkey.device
+    if hit_off is None:
+        hit_off = torch.empty(nq + 1, dtype=torch.uint64, device=dev)
+    if d_total is None:
+        d_total = torch.zeros(1, dtype=torch.uint64, device=dev)
+    if ws is None:
+        ws = _ws(seedtable_lookup_workspace_bytes(max(1, nq)), dev)
+    if hit_cap is None:
+        _check(_st_lk(_ptr(qkey), nq, _ptr(d_nq), k, bits, _ptr(offsets), _ptr(fp), _ptr(pos_tab), _ptr(hit_off),
+                      None, 0, _ptr(d_total), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_lookup")
+        hit_cap = int(d_total.view(torch.int64).item())
+    if hit_pos is None:
+        hit_pos = torch.empty(max(1, hit_cap), dtype=torch.uint64, device=dev)
+    _check(_st_lk(_ptr(qkey), nq, _ptr(d_nq), k, bits, _ptr(offsets), _ptr(fp), _ptr(pos_tab), _ptr(hit_off),
+                  _ptr(hit_pos), hit_cap, _ptr(d_total), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_lookup")
+    return hit_off, hit_pos, d_total
 
 
 def seedtable_count(hash_: torch.Tensor, k: int, bits: int, *, m: int | None = None, d_m=None, counts=None,

@@ -1,0 +1,208 @@
+// lookup.cu -- batch seed lookup against the seed table (Sec. 2.4, Fig. 1:
+// "The seed pointer table enables fast lookups to 'CG' and 'CT'").
+//
+// For query key q: f = fingerprint(q) (the top 32 bits of the 2k-bit key, R21),
+// b = f >> (32 - bits); the hits are the entries of b's slice [offsets[b], offsets[b+1]) with
+// fp == f, in table order (ascending position).  When 2k <= 32 the fingerprint is the whole
+// key and the hits are exactly the stored positions of the seed (R30).
+//
+// Three steps: count (per query), exclusive scan of the counts (-> CSR offsets), emit.
+// A group of kG lanes (8 by default) serves one query: the slice's fingerprints are read kG
+// at a time, matches are counted with a group ballot, and in the emit step written in order
+// (ballot prefix inside the group).  Minimizer hashes are skewed low, so queries land in the
+// long buckets more often than the mean bucket length suggests.
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace mzs {
+namespace {
+
+constexpr int kLTPB = 256;
+
+__device__ __forceinline__ uint32_t fp_of(uint64_t key, int k) {
+  const int b = 2 * k;
+  return b >= 32 ? (uint32_t)(key >> (b - 32)) : (uint32_t)(key << (32 - b));
+}
+
+__device__ __forceinline__ uint64_t query_count(const uint64_t* d_nq, uint64_t nq) {
+  return d_nq ? min(*d_nq, nq) : nq;
+}
+
+// EMIT = false: hit_off[i] = number of hits of query i.  EMIT = true: write them at hit_off[i].
+template <bool EMIT, int kG>
+__global__ void __launch_bounds__(kLTPB) lookup_kernel(const uint64_t* __restrict__ q, uint64_t nq_cap,
+                                                       const uint64_t* d_nq, int k, int bits,
+                                                       const uint64_t* __restrict__ offsets,
+                                                       const uint32_t* __restrict__ fp,
+                                                       const uint64_t* __restrict__ pos_tab, uint64_t* hit_off,
+                                                       uint64_t* __restrict__ hit_pos, uint64_t hit_cap) {
+  const uint64_t nq = query_count(d_nq, nq_cap);
+  const unsigned lane = lane_id();
+  const unsigned gl = lane & (kG - 1);                   // lane inside the group
+  const unsigned gshift = lane & ~(unsigned)(kG - 1);    // group's first lane
+  const unsigned gmask = (kG == 32 ? 0xffffffffu : ((1u << kG) - 1u)) << gshift;
+  const uint64_t groups = (uint64_t)gridDim.x * (kLTPB / kG);
+  for (uint64_t i0 = ((uint64_t)blockIdx.x * kLTPB + threadIdx.x) / kG; i0 < ((nq + groups - 1) / groups) * groups;
+       i0 += groups) {
+    const bool live = i0 < nq;
+    uint32_t f = 0;
+    uint64_t lo = 0, hi = 0, o = 0;
+    if (live) {
+      f = fp_of(q[i0], k);
+      const uint64_t b = f >> (32 - bits);
+      lo = offsets[b];
+      hi = offsets[b + 1];
+      if (EMIT) o = hit_off[i0];
+    }
+    uint64_t cnt = 0;
+    // all groups of the warp iterate together (ballots need the full warp)
+    uint64_t len = hi - lo;
+    uint64_t steps = (len + kG - 1) / kG;
+    for (int o2 = kG; o2 < 32; o2 <<= 1) steps = max(steps, (uint64_t)__shfl_xor_sync(0xffffffffu, steps, o2));
+    for (uint64_t s = 0; s < steps; ++s) {
+      const uint64_t e = lo + s * kG + gl;
+      const bool hit = e < hi && fp[e] == f;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit) & gmask;
+      if (EMIT && hit) {
+        const uint64_t r = o + cnt + __popc(bal & ((1u << lane) - 1u));
+        if (r < hit_cap) hit_pos[r] = pos_tab[e];
+      }
+      cnt += __popc(bal);
+    }
+    if (!EMIT && live && gl == 0) hit_off[i0] = cnt;
+  }
+}
+
+// ---- exclusive scan of u64 counts in place (reduce, scan of block sums, add)
+constexpr int kSE = 8;                   // elements per thread
+constexpr int kSB = kLTPB * kSE;         // elements per block
+
+__global__ void __launch_bounds__(kLTPB) scan_reduce_kernel(const uint64_t* x, uint64_t nq_cap, const uint64_t* d_nq,
+                                                            uint64_t* bsum) {
+  __shared__ uint64_t ws[kLTPB / 32];
+  const uint64_t n = query_count(d_nq, nq_cap);
+  const uint64_t b0 = (uint64_t)blockIdx.x * kSB;
+  uint64_t s = 0;
+  for (uint64_t i = b0 + threadIdx.x; i < min(n, b0 + kSB); i += kLTPB) s += x[i];
+  uint64_t tot;
+  block_exclusive_sum<kLTPB, uint64_t>(s, ws, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// one block: exclusive scan of the block sums; total -> x[n] and *d_total
+__global__ void __launch_bounds__(kLTPB) scan_blocks_kernel(uint64_t* bsum, uint64_t nb, uint64_t* x, uint64_t nq_cap,
+                                                            const uint64_t* d_nq, uint64_t* d_total) {
+  __shared__ uint64_t ws[kLTPB / 32];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint64_t c0 = 0; c0 < nb; c0 += kLTPB) {
+    const uint64_t i = c0 + threadIdx.x;
+    const uint64_t v = i < nb ? bsum[i] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_sum<kLTPB, uint64_t>(v, ws, &tot);
+    if (i < nb) bsum[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t n = query_count(d_nq, nq_cap);
+    x[n] = carry;
+    if (d_total) *d_total = carry;
+  }
+}
+
+__global__ void __launch_bounds__(kLTPB) scan_apply_kernel(uint64_t* x, uint64_t nq_cap, const uint64_t* d_nq,
+                                                           const uint64_t* bsum) {
+  __shared__ uint64_t ws[kLTPB / 32];
+  const uint64_t n = query_count(d_nq, nq_cap);
+  const uint64_t i0 = (uint64_t)blockIdx.x * kSB + (uint64_t)threadIdx.x * kSE;
+  uint64_t v[kSE];
+  uint64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kSE; ++j) {
+    v[j] = i0 + j < n ? x[i0 + j] : 0;
+    s += v[j];
+  }
+  uint64_t tot;
+  uint64_t ex = block_exclusive_sum<kLTPB, uint64_t>(s, ws, &tot) + bsum[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kSE; ++j) {
+    if (i0 + j < n) x[i0 + j] = ex;
+    ex += v[j];
+  }
+}
+
+}  // namespace
+}  // namespace mzs
+
+using namespace mzs;
+
+MZS_API size_t seedtable_lookup_workspace_bytes(uint64_t nq) {
+  Sizer z;
+  z.take<uint64_t>((nq + kSB - 1) / kSB + 1);
+  z.take<uint64_t>(1);
+  return z.used;
+}
+
+MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* d_nq, int k, int bucket_bits,
+                             const uint64_t* offsets, const uint32_t* fp, const uint64_t* pos_tab,
+                             uint64_t* hit_off, uint64_t* hit_pos, uint64_t hit_cap, uint64_t* d_total, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
+  if (!hit_off) return SLSUM_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  if (nq == 0) {
+    MZS_CUDA(cudaMemsetAsync(hit_off, 0, sizeof(uint64_t), st));
+    if (d_total) MZS_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint64_t), st));
+    return SLSUM_OK;
+  }
+  if (!qkey || !offsets || !fp || (hit_cap && (!hit_pos || !pos_tab))) return SLSUM_EINVAL;
+  TempWs tmp;
+  const size_t need = seedtable_lookup_workspace_bytes(nq);
+  if (!ws) {
+    MZS_CUDA(cudaMallocAsync(&tmp.p, need, st));
+    tmp.s = st;
+    ws = tmp.p;
+    ws_bytes = need;
+  }
+  if (ws_bytes < need) return SLSUM_ENOMEM;
+  Carve c(ws, ws_bytes);
+  const uint64_t nb = (nq + kSB - 1) / kSB;
+  uint64_t* bsum = c.take<uint64_t>(nb + 1);
+  if (!c.ok) return SLSUM_ENOMEM;
+  static const int lanes = [] {
+    const char* e = getenv("MZS_LOOKUP_LANES");
+    const int v = e && *e ? atoi(e) : 8;
+    return (v == 8 || v == 16 || v == 32) ? v : 8;
+  }();
+  const uint64_t want = (nq * lanes + kLTPB - 1) / kLTPB;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)num_sms() * 8));
+  auto launch = [&](auto emit_tag) -> int {
+    constexpr bool E = decltype(emit_tag)::value;
+    uint64_t* hp = E ? hit_pos : nullptr;
+    const uint64_t hc = E ? hit_cap : 0;
+    if (lanes == 8)
+      lookup_kernel<E, 8><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+    else if (lanes == 32)
+      lookup_kernel<E, 32><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+    else
+      lookup_kernel<E, 16><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+    MZS_LAUNCHED();
+    return SLSUM_OK;
+  };
+  int rc = launch(std::false_type{});
+  if (rc) return rc;
+  scan_reduce_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, d_nq, bsum);
+  MZS_LAUNCHED();
+  scan_blocks_kernel<<<1, kLTPB, 0, st>>>(bsum, nb, hit_off, nq, d_nq, d_total);
+  MZS_LAUNCHED();
+  scan_apply_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, d_nq, bsum);
+  MZS_LAUNCHED();
+  if (hit_cap) return launch(std::true_type{});
+  return SLSUM_OK;
+}
