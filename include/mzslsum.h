@@ -81,6 +81,12 @@ int slsum_version(void);
  *                           cancels the offset).  SLSUM_ADD_U32 only (exact mod 2^32); any
  *                           other op returns SLSUM_EUNSUPPORTED (min/max are not invertible,
  *                           f32 add would lose the tolerance to cancellation).
+ *   SLSUM_PATH_SCALAR       Algorithm 1 "ScalarInput" (L95-120): a warp-wide shift register
+ *                           of window accumulators; every window is the strict left fold,
+ *                           so the result is bit-identical to Eq. 2 evaluated naively for
+ *                           EVERY op (f32 add and AFFINE included; "no additional
+ *                           requirements on the operator").  O(w) work per output;
+ *                           w <= 1024, else SLSUM_EUNSUPPORTED.
  * x, y: device arrays of n and max(0, n-w+1) elements; x and y must not overlap.
  */
 enum {
@@ -91,7 +97,13 @@ enum {
   SLSUM_AFFINE_U32X2 = 4,
   SLSUM_MIN_U64 = 5
 };
-enum { SLSUM_PATH_GENERIC = 0, SLSUM_PATH_COMMUTATIVE = 1, SLSUM_PATH_AUTO = 2, SLSUM_PATH_RECURRENT = 3 };
+enum {
+  SLSUM_PATH_GENERIC = 0,
+  SLSUM_PATH_COMMUTATIVE = 1,
+  SLSUM_PATH_AUTO = 2,
+  SLSUM_PATH_RECURRENT = 3,
+  SLSUM_PATH_SCALAR = 4
+};
 
 /* GENERIC path on the default stream; returns after completion. */
 int slsum_run(int op, uint32_t w, const void* x, void* y, uint64_t n);

@@ -61,6 +61,13 @@ __device__ __forceinline__ uint2 shfl_down(uint2 v, int o) {
   return make_uint2(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
 }
 
+__device__ __forceinline__ uint32_t shfl_idx(uint32_t v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ float shfl_idx(float v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ unsigned long long shfl_idx(unsigned long long v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+__device__ __forceinline__ uint2 shfl_idx(uint2 v, int l) {
+  return make_uint2(__shfl_sync(0xffffffffu, v.x, l), __shfl_sync(0xffffffffu, v.y, l));
+}
+
 // ---------------------------------------------------------------- segmented scans
 // A segment value: f = "a segment boundary lies inside", v = fold of the open part.
 template <class T>

@@ -387,6 +387,89 @@ int launch_prefixdiff(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStre
   return SLSUM_OK;
 }
 
+// SCALAR path: Algorithm 1 "ScalarInput".  A warp is the vector Y: lane l holds
+// Y[l + 32 r] (r < K), the partial fold of the window that will complete r*32 + l steps later.
+// Every input x_t is broadcast to the first w entries (Y <- Y (+) X), the newest window
+// Y[w-1] starts with x_t itself, Y[0] is the finished window y_{t-w+1}, then Y <<< 1.  Each
+// window is the strict left fold x_i (+) x_{i+1} (+) ... (+) x_{i+w-1}, with "no additional
+// requirements on the operator": the outputs are bit-identical to the oracle's fold
+// for every op, f32 add and the non-commutative affine maps included.  O(w) work per output;
+// each warp runs a chunk of consecutive outputs (w-1 inputs of warm-up per chunk).
+template <class Op, int K>
+__global__ void __launch_bounds__(256) slsum_scalar_kernel(const typename Op::T* __restrict__ x,
+                                                          typename Op::T* __restrict__ y, uint64_t n, uint32_t w,
+                                                          uint64_t nout, uint32_t chunk) {
+  using T = typename Op::T;
+  const uint64_t warp = ((uint64_t)blockIdx.x * 256 + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t c0 = warp * chunk;
+  if (c0 >= nout) return;  // uniform per warp
+  const uint64_t c1 = min(nout, c0 + chunk);
+  const uint64_t t_end = c1 + w - 1;  // inputs [c0, c1 + w - 1) <= n
+  T acc[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) acc[r] = Op::id();  // windows that started before c0: never output
+  T stash = Op::id();
+  uint64_t obase = c0;  // first output of the current stash
+  uint32_t ocnt = 0;    // outputs in the stash (lane ocnt receives the next one)
+  for (uint64_t tb = c0; tb < t_end; tb += 32) {
+    const uint64_t ti = tb + lane;
+    const T xv = ti < t_end ? x[ti] : Op::id();
+    const uint32_t nb = (uint32_t)min((uint64_t)32, t_end - tb);
+    for (uint32_t s = 0; s < nb; ++s) {
+      const T xs = shfl_idx(xv, (int)s);
+      // Y <- Y (+) X, X = x_t broadcast to the first w entries; the newest window starts at x_t
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const uint32_t j = lane + 32u * r;
+        if (j < w) acc[r] = (j == w - 1) ? xs : Op::op(acc[r], xs);
+      }
+      // y_{t-w+1} <- Y[0]
+      if (tb + s >= c0 + w - 1) {
+        const T o = shfl_idx(acc[0], 0);
+        if (lane == ocnt) stash = o;
+        if (++ocnt == 32) {
+          y[obase + lane] = stash;
+          obase += 32;
+          ocnt = 0;
+        }
+      }
+      // Y <- Y <<< 1
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const T up = shfl_down(acc[r], 1);
+        const T wrap = (r + 1 < K) ? shfl_idx(acc[r + 1 < K ? r + 1 : r], 0) : up;
+        acc[r] = (lane == 31) ? wrap : up;
+      }
+    }
+  }
+  if (lane < ocnt) y[obase + lane] = stash;
+}
+
+template <class Op, int K>
+int launch_scalar_k(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  const uint64_t nout = n - w + 1;
+  const uint32_t chunk = std::max<uint32_t>(2048u, 32u * w);
+  const uint64_t warps = (nout + chunk - 1) / chunk;
+  const uint64_t grid = (warps + 7) / 8;
+  slsum_scalar_kernel<Op, K><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, w,
+                                                            nout, chunk);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+template <class Op>
+int launch_scalar(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  if (w <= 32) return launch_scalar_k<Op, 1>(xv, yv, n, w, st);
+  if (w <= 64) return launch_scalar_k<Op, 2>(xv, yv, n, w, st);
+  if (w <= 128) return launch_scalar_k<Op, 4>(xv, yv, n, w, st);
+  if (w <= 256) return launch_scalar_k<Op, 8>(xv, yv, n, w, st);
+  if (w <= 512) return launch_scalar_k<Op, 16>(xv, yv, n, w, st);
+  if (w <= 1024) return launch_scalar_k<Op, 32>(xv, yv, n, w, st);
+  return SLSUM_EUNSUPPORTED;  // the shift register holds at most 1024 windows
+}
+
 }  // namespace
 }  // namespace mzs
 
@@ -394,11 +477,22 @@ using namespace mzs;
 
 MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n, int path, void* stream) {
   if (w == 0 || op < SLSUM_MIN_U32 || op > SLSUM_MIN_U64) return SLSUM_EINVAL;
-  if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_RECURRENT) return SLSUM_EINVAL;
+  if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_SCALAR) return SLSUM_EINVAL;
   if (n < w) return SLSUM_OK;  // zero outputs (not an error)
   if (!x || !y) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
   if (path == SLSUM_PATH_AUTO) path = SLSUM_PATH_GENERIC;
+  if (path == SLSUM_PATH_SCALAR) {
+    switch (op) {
+      case SLSUM_MIN_U32: return launch_scalar<OpMinU32>(x, y, n, w, st);
+      case SLSUM_MAX_U32: return launch_scalar<OpMaxU32>(x, y, n, w, st);
+      case SLSUM_ADD_U32: return launch_scalar<OpAddU32>(x, y, n, w, st);
+      case SLSUM_ADD_F32: return launch_scalar<OpAddF32>(x, y, n, w, st);
+      case SLSUM_AFFINE_U32X2: return launch_scalar<OpAffine>(x, y, n, w, st);
+      case SLSUM_MIN_U64: return launch_scalar<OpMinU64>(x, y, n, w, st);
+    }
+    return SLSUM_EINVAL;
+  }
   if (path == SLSUM_PATH_RECURRENT) {
     // invertible (+) only: uint32 add (exact).  min/max have no inverse; f32 add loses the
     // tolerance to cancellation (4-53x over); the affine maps are not all invertible.

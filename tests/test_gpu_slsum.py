@@ -83,6 +83,29 @@ def test_recurrent_vs_oracle(w):
         assert np.array_equal(y.cpu().numpy(), O.slsum(O.ADD_U32, w, x))
 
 
+@pytest.mark.parametrize("op", [o for o, _ in OPS])
+@pytest.mark.parametrize("w", WS)
+def test_scalar_alg1_bit_exact(op, w):
+    """SCALAR path = Algorithm 1: every window is the strict left fold, so the
+    result equals the oracle's bit for bit for every op -- f32 add included (no tolerance)."""
+    rng = np.random.default_rng(op * 31337 + w)
+    for n in sorted({w, w + 1, 2 * w + 3, 5000, 70_001}):
+        x = _input(op, n, rng)
+        got = _run(op, w, x, P.SLSUM_PATH_SCALAR)
+        want = O.slsum(dict(OPS)[op], w, x)
+        if op == P.SLSUM_ADD_F32:
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), w
+        else:
+            assert np.array_equal(got, want), (op, w)
+
+
+def test_scalar_rejects_w_over_1024():
+    x = torch.zeros(5000, dtype=torch.uint32, device="cuda")
+    with pytest.raises(P.SlsumError) as e:
+        P.slsum_run(P.SLSUM_MIN_U32, 1025, x, path=P.SLSUM_PATH_SCALAR)
+    assert e.value.rc == P.SLSUM_EUNSUPPORTED
+
+
 @pytest.mark.parametrize("op", [o for o, _ in OPS if o != P.SLSUM_ADD_U32])
 def test_recurrent_rejects_non_invertible(op):
     x = torch.zeros((100, 2) if op == P.SLSUM_AFFINE_U32X2 else (100,),
@@ -143,10 +166,13 @@ def test_c2_full_size_sampled(w):
                 del ref, got
             del y
     xf = D.c2_f32(n)
-    for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE):
+    for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE, P.SLSUM_PATH_SCALAR):
         y = P.slsum_run(P.SLSUM_ADD_F32, w, xf, path=path)
         ys = y[it].cpu().numpy()
         for j, i in enumerate(idx):
             o = O.slsum(O.ADD_F32, w, G.c2_f32(w, lo=int(i)))[0]
-            assert abs(float(ys[j]) - float(o)) <= 1e-5 * abs(float(o)) + 1e-6 * w
+            if path == P.SLSUM_PATH_SCALAR:      # Alg. 1 is the strict left fold: bit-exact
+                assert np.float32(ys[j]).view(np.uint32) == np.float32(o).view(np.uint32)
+            else:
+                assert abs(float(ys[j]) - float(o)) <= 1e-5 * abs(float(o)) + 1e-6 * w
         del y
