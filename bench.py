@@ -61,6 +61,18 @@ def parse():
     return ap.parse_args()
 
 
+def load_traffic(name):
+    """DRAM bytes per launch of the step's kernels from the committed ncu --set full capture
+    (profiles/r01/traffic_c3.json, written by tools/ncu_summary.py traffic); None if absent."""
+    p = os.path.join(ROOT, "profiles", "r01", name)
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -612,13 +624,21 @@ def main():
     int_peak = SM_COUNT * INT32_LANES_PER_SM_CLK * sm_mhz * 1e6 / 1e12          # T int32 ops/s
     ops = MZ_INT_OPS_PER_BASE.get(k, 48) * n
     ach = ops / (phase_ms["extract"] * 1e-3) / 1e12
+    tr = load_traffic("traffic_c3.json") if k == 19 else None
+    mz_traffic = tr.get("mz_fast_kernel<10, 1, 19>", {}).get("dram_bytes") if tr else None
+    tab_traffic = sum(v["dram_bytes"] for kk, v in tr.items() if kk.startswith(("nsweep", "upsweep"))) if tr else None
     roof = {"bound": "alu", "kernel": "mz_fast_kernel (a2-a7 fused, one launch per step)",
-            "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": None,
+            "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": mz_traffic,
+            "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01/traffic_c3.json); algorithmic "
+                            f"{per_phase_bytes['extract']:.3e} B",
             "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
             "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"]}
     tab_ach = per_phase_bytes["table"] / (phase_ms["table"] * 1e-3) / 1e9
     roof_table = {"bound": "hbm", "kernel": "seed table (3 packed-item LSD radix passes + pointer table)",
                   "achieved": tab_ach, "peak": hbm_peak, "unit": "GB/s", "frac": tab_ach / hbm_peak,
+                  "traffic": tab_traffic,
+                  "traffic_note": "DRAM bytes of the 3 passes' upsweeps + downsweeps (ncu); the SURVEY's "
+                                  "algorithmic model is 32 B/entry, the 3-pass LSD moves 84 B/entry",
                   "peak_kind": peak_kind, "ms": phase_ms["table"]}
     step_bytes = sum(per_phase_bytes.values())
     step_hbm = {"achieved": step_bytes / (ms_step * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",

@@ -95,14 +95,41 @@ def launches(path, last_step=None):
     print(f"| **total** | | **{tot:.3f}** | |\n")
 
 
+def traffic(path):
+    """JSON {kernel base name: {"dram_bytes": read + write per launch, "time_ms": ...}} of a
+    --set full capture (first launch of each kernel name) -- bench.py's roofline `traffic`."""
+    import json
+    rows = _csv([path, "--page", "raw"])
+    hdr = rows[0]
+    out = {}
+    for r in rows[2:]:
+        name = re.sub(r"\(.*", "", r[hdr.index("Kernel Name")]).replace("(anonymous namespace)::", "")
+        name = re.sub(r"^.*unnamed>::", "", name.replace("mzs::", "").replace("void ", "")).strip()
+        if name in out:
+            continue
+
+        def val(m, scale):
+            i = hdr.index(m)
+            v = float(r[i].replace(",", ""))
+            u = rows[1][i]
+            return v * scale.get(u, 1.0)
+        gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
+        ms = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}
+        out[name] = {"dram_bytes": val("dram__bytes_read.sum", gb) + val("dram__bytes_write.sum", gb),
+                     "time_ms": val("gpu__time_duration.sum", ms)}
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["report", "launches"])
+    ap.add_argument("mode", choices=["report", "launches", "traffic"])
     ap.add_argument("path")
     ap.add_argument("--bases", type=float, default=None)
     ap.add_argument("--last-step", default=None, help="launches mode: keep the last step starting at this kernel")
     a = ap.parse_args()
-    if a.mode == "report":
+    if a.mode == "traffic":
+        traffic(a.path)
+    elif a.mode == "report":
         report(a.path, a.bases)
     else:
         launches(a.path, a.last_step)
