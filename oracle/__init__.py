@@ -22,6 +22,9 @@ Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
                 instance, SPEC.md examples, numpy argmin brute force, exhaustive
                 4^L strings, density band (L85), invariants.
   * orc_seedtable  sort-based construction (Python sorted), partition property.
+  * orc_kmer_rc / canonical keys: hand-computed reverse complements, involution, the
+                canonical code of a k-mer equals that of its reverse complement, and strand
+                symmetry of canonical minimizers (S and revcomp(S) give mirrored positions).
   * orc_lookup  SPEC S:L327-330 examples, a Python dict of every stored seed, the partition
                 property (looking up every stored seed reproduces the table).
 """
@@ -36,7 +39,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 MIN_U32, MAX_U32, ADD_U32, ADD_F32, AFFINE_U32X2, MIN_U64 = range(6)
-KEY_HASH, KEY_RAW = 0, 1
+KEY_HASH, KEY_RAW, KEY_CANON, KEY_CANON_RAW = 0, 1, 2, 3
 _DTYPE = {MIN_U32: np.uint32, MAX_U32: np.uint32, ADD_U32: np.uint32, ADD_F32: np.float32,
           AFFINE_U32X2: np.uint32, MIN_U64: np.uint64}
 
@@ -59,6 +62,8 @@ def lib():
         L.orc_pack.argtypes = [vp, u64, vp, vp]
         L.orc_kmer.argtypes = [vp, u64, i32]
         L.orc_kmer.restype = u64
+        L.orc_kmer_rc.argtypes = [vp, u64, i32]
+        L.orc_kmer_rc.restype = u64
         L.orc_hash.argtypes = [u64, i32]
         L.orc_hash.restype = u64
         L.orc_unhash.argtypes = [u64, i32]
@@ -143,6 +148,12 @@ def pack(seq):
 def kmer(codes: np.ndarray, i: int, k: int) -> int:
     codes = np.ascontiguousarray(codes, dtype=np.uint8)
     return int(lib().orc_kmer(_p(codes), i, k))
+
+
+def kmer_rc(codes: np.ndarray, i: int, k: int) -> int:
+    """Code of the reverse complement of the k-mer at i (R32)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    return int(lib().orc_kmer_rc(_p(codes), i, k))
 
 
 def hash_(x: int, b: int) -> int:

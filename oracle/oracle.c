@@ -218,6 +218,14 @@ uint64_t orc_kmer(const uint8_t* codes, uint64_t i, int k) {
     return code;
 }
 
+/* code of the REVERSE COMPLEMENT of the k-mer starting at base i, from scratch: the k-mer
+ * read backwards with every base complemented (A<->T, C<->G, i.e. b -> 3 - b), R32. */
+uint64_t orc_kmer_rc(const uint8_t* codes, uint64_t i, int k) {
+    uint64_t code = 0;
+    for (int t = k - 1; t >= 0; t--) code = code * 4 + (uint64_t)(3 - codes[i + (uint64_t)t]);
+    return code;
+}
+
 /* H_b (R5): all arithmetic mod 2^b, input x in [0, 2^b).
  *   (1) x <- (2^21 - 1) x - 1    (2) x <- x xor (x >> 24)   (3) x <- 265 x
  *   (4) x <- x xor (x >> 14)     (5) x <- 21 x              (6) x <- x xor (x >> 28)
@@ -271,7 +279,9 @@ void orc_hash_array(const uint64_t* x, uint64_t* y, uint64_t n, int b) {
 /* ---------------------------------------------------------------------- */
 /* Minimizers (Sec. 2.4, Fig. 2).                                      */
 /* ---------------------------------------------------------------------- */
-enum { ORC_KEY_HASH = 0, ORC_KEY_RAW = 1 };
+/* key modes: hashed / raw forward code (R4); canonical = the smaller of the forward and the
+ * reverse-complement code (strand-symmetric, R32; NEXT f4), hashed or raw */
+enum { ORC_KEY_HASH = 0, ORC_KEY_RAW = 1, ORC_KEY_CANON = 2, ORC_KEY_CANON_RAW = 3 };
 
 /*
  * s[0..n)        ASCII bases (local to this call; global position = pos_base + local)
@@ -290,7 +300,7 @@ int64_t orc_mz(const uint8_t* s, uint64_t n, int k, int w,
                const uint64_t* read_off, uint64_t nreads, int keymode,
                uint64_t pos_base, uint64_t win_lo, uint64_t win_hi,
                uint64_t* out_key, uint64_t* out_pos, uint64_t cap) {
-    if (k < 1 || k > 31 || w < 1 || (keymode != ORC_KEY_HASH && keymode != ORC_KEY_RAW))
+    if (k < 1 || k > 31 || w < 1 || keymode < ORC_KEY_HASH || keymode > ORC_KEY_CANON_RAW)
         return ORC_EINVAL;
     const uint64_t span = (uint64_t)k + (uint64_t)w - 1;   /* bases per window */
     if (n < span) return 0;
@@ -319,7 +329,11 @@ int64_t orc_mz(const uint8_t* s, uint64_t n, int k, int w,
     #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < (int64_t)nk; i++) {
         uint64_t c = orc_kmer(code, (uint64_t)i, k);
-        key[i] = keymode == ORC_KEY_HASH ? orc_hash(c, 2 * k) : c;
+        if (keymode == ORC_KEY_CANON || keymode == ORC_KEY_CANON_RAW) {
+            uint64_t r = orc_kmer_rc(code, (uint64_t)i, k);
+            if (r < c) c = r;
+        }
+        key[i] = (keymode == ORC_KEY_HASH || keymode == ORC_KEY_CANON) ? orc_hash(c, 2 * k) : c;
     }
     /* every window: validity by scanning its bases; argmin by a strict '<' scan */
     #pragma omp parallel for schedule(static)
