@@ -123,7 +123,10 @@ int mz_encode(const uint8_t* seq, uint64_t n, uint64_t* words, uint32_t* invalid
  * PAPER.md L85 (Sec. 2.4, Fig. 2) with the readings of DESIGN.md:
  *   k-mer q       code_q = sum_{t<k} b_{q+t} 4^(k-1-t) (2k bits, MSB-first, R6)
  *   key_q         H_2k(code_q) (MZ_KEY_HASH; the masked Wang/minimap2 mix, R5)
- *                 or code_q (MZ_KEY_RAW, Fig. 2's lexicographic order, R4)
+ *                 or code_q (MZ_KEY_RAW, Fig. 2's lexicographic order, R4);
+ *                 MZ_KEY_CANON / MZ_KEY_CANON_RAW: the same on the canonical code
+ *                 min(code_q, revcomp(code_q)) (strand-symmetric minimizers, R32; the
+ *                 paper's Fig. 2 is forward-strand only, R10)
  *   window i      the w k-mers q = i .. i+w-1 = bases [i, i+k+w-2] (R1); valid iff all
  *                 those bases are A/C/G/T and no segment (read) starts in (i, i+k+w-2] (R8)
  *   p_i           the leftmost position of the minimum key in window i (R2)
@@ -147,7 +150,7 @@ int mz_encode(const uint8_t* seq, uint64_t n, uint64_t* words, uint32_t* invalid
  *   number of windows always suffices.
  */
 enum { MZ_IN_ASCII = 0, MZ_IN_PACKED2 = 1 };
-enum { MZ_KEY_HASH = 0, MZ_KEY_RAW = 1 };
+enum { MZ_KEY_HASH = 0, MZ_KEY_RAW = 1, MZ_KEY_CANON = 2, MZ_KEY_CANON_RAW = 3 };
 
 typedef struct mz_in {
   int kind;                  /* MZ_IN_ASCII or MZ_IN_PACKED2                    */

@@ -20,7 +20,7 @@ SLSUM_OK, SLSUM_EINVAL, SLSUM_EUNSUPPORTED, SLSUM_ECAPACITY, SLSUM_ECUDA, SLSUM_
 SLSUM_MIN_U32, SLSUM_MAX_U32, SLSUM_ADD_U32, SLSUM_ADD_F32, SLSUM_AFFINE_U32X2, SLSUM_MIN_U64 = range(6)
 SLSUM_PATH_GENERIC, SLSUM_PATH_COMMUTATIVE, SLSUM_PATH_AUTO, SLSUM_PATH_RECURRENT, SLSUM_PATH_SCALAR = range(5)
 MZ_IN_ASCII, MZ_IN_PACKED2 = 0, 1
-MZ_KEY_HASH, MZ_KEY_RAW = 0, 1
+MZ_KEY_HASH, MZ_KEY_RAW, MZ_KEY_CANON, MZ_KEY_CANON_RAW = 0, 1, 2, 3
 U64_MAX = 2 ** 64 - 1
 
 OP_DTYPE = {SLSUM_MIN_U32: torch.uint32, SLSUM_MAX_U32: torch.uint32, SLSUM_ADD_U32: torch.uint32,

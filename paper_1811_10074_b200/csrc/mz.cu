@@ -16,6 +16,7 @@
 // Fast path: w in [1,16] as a compile-time block length (S/P in registers), k <= 25.
 // Generic path: any w <= 1024 and any k <= 31, S/P by block-wide segmented scans.
 #include <algorithm>
+#include <type_traits>
 
 #include "ops.cuh"
 
@@ -47,6 +48,21 @@ __device__ __forceinline__ uint64_t hash_b64(uint64_t x, uint64_t m) {
   return x;
 }
 
+// Reverse complement of a k-mer code (R32): complement every base (b -> 3 - b =
+// bitwise not of its 2 bits) and reverse the order of the 2-bit groups.  Bit-reversal then a
+// swap of the two bits of every group reverses the groups of a 64/32-bit word; the shift
+// drops the complemented garbage above 2k bits.
+__device__ __forceinline__ uint64_t revcomp64(uint64_t code, int k) {
+  uint64_t x = __brevll(~code);
+  x = ((x >> 1) & 0x5555555555555555ull) | ((x & 0x5555555555555555ull) << 1);
+  return x >> (64 - 2 * k);
+}
+__device__ __forceinline__ uint32_t revcomp32(uint32_t code, int k) {
+  uint32_t x = __brev(~code);
+  x = ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
+  return x >> (32 - 2 * k);
+}
+
 struct MzArgs {
   const uint64_t* words;     // packed bases (MSB-first, 32 per word)
   const uint32_t* invalid;   // invalid bitmap or nullptr
@@ -56,7 +72,7 @@ struct MzArgs {
   const uint64_t* read_off;  // nreads+1 or nullptr
   uint64_t nreads;
   uint64_t pos_base, win_lo, win_hi;
-  int k, w, raw;
+  int k, w, raw, canon;      // key mode: raw code (R4) / canonical strand (R32)
   uint64_t* out_hash;
   uint64_t* out_pos;
   uint64_t capacity;
@@ -96,8 +112,10 @@ __device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
 // bitmask wvb (zeroed by the caller) is set iff the window whose LAST k-mer is that slot's
 // k-mer is valid (run of valid same-read bases ending at the k-mer's last base >= k+w-1).
 // KK != 0: k is the compile-time constant KK (lets the compiler drop the masking and the
-// xor-shift work on the always-zero high bits); RAW: keys are the codes themselves.
-template <class Key, int Q, bool H64, bool CHECK, int KK = 0, bool RAW = false>
+// xor-shift work on the always-zero high bits); KM bit 0 (RAW): keys are the codes themselves;
+// KM bit 1 (CANON): the code is min(forward, reverse complement), the reverse complement
+// rolled alongside (the entering base's complement enters at the top, R32).
+template <class Key, int Q, bool H64, bool CHECK, int KK = 0, int KM = 0>
 __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint32_t* wvb) {
   static_assert(Q <= 33, "validity bits of one strip fit in a u64 shifted by < 32");
   uint64_t vbits = 0;
@@ -141,10 +159,13 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   if (H64) {
     // 2k > 32: the low word of the mask is all ones (lets the compiler mask the high word only)
     const uint64_t km = ((uint64_t)((1u << (kk - 32)) - 1u) << 32) | 0xffffffffull;
+    constexpr bool RAW = KM & 1, CANON = KM & 2;
     uint64_t code = X >> (64 - kk);
+    uint64_t rc = CANON ? revcomp64(code, k) : 0;
 #pragma unroll
     for (int s = 0; s < Q; ++s) {
       if (s > 0) {
+        if (CANON) rc = (rc >> 2) | ((uint64_t)(3u - (uint32_t)(Z >> 62)) << (kk - 2));
         code = ((code << 2) | (Z >> 62)) & km;
         Z <<= 2;
       }
@@ -159,15 +180,19 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
         run = inv ? 0u : run + 1u;
         vbits |= (uint64_t)(run >= (uint32_t)span) << s;
       }
-      const uint64_t h = RAW ? code : hash_b64(code, km);
+      const uint64_t c = (CANON && rc < code) ? rc : code;
+      const uint64_t h = RAW ? c : hash_b64(c, km);
       keys[s0 + s] = Key::make(h, s0 + s);
     }
   } else {
     const uint32_t km = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
+    constexpr bool RAW = KM & 1, CANON = KM & 2;
     uint32_t code = (uint32_t)(X >> (64 - kk));
+    uint32_t rc = CANON ? revcomp32(code, k) : 0u;
 #pragma unroll
     for (int s = 0; s < Q; ++s) {
       if (s > 0) {
+        if (CANON) rc = (rc >> 2) | ((3u - (uint32_t)(Z >> 62)) << (kk - 2));
         code = ((code << 2) | (uint32_t)(Z >> 62)) & km;
         Z <<= 2;
       }
@@ -182,7 +207,8 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
         run = inv ? 0u : run + 1u;
         vbits |= (uint64_t)(run >= (uint32_t)span) << s;
       }
-      const uint32_t h = RAW ? code : hash_b32(code, km);
+      const uint32_t c = (CANON && rc < code) ? rc : code;
+      const uint32_t h = RAW ? c : hash_b32(c, km);
       keys[s0 + s] = Key::make(h, s0 + s);
     }
   }
@@ -275,19 +301,22 @@ __device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int
 
 // Code + key of the k-mer at local position q, from scratch (phase 3 re-derives the hash
 // of every emitted position instead of keeping all keys of a super-tile resident).
-template <bool H64, int KK = 0>
+template <bool H64, int KK = 0, int CNM = -1>
 __device__ __forceinline__ uint64_t key_at(const MzArgs& a, int64_t q) {
+  const bool canon = CNM < 0 ? a.canon != 0 : CNM == 1;
   const int64_t wi = q >> 5;
   const uint32_t off = (uint32_t)(q & 31) * 2;
   const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1);
   const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
   const int kk = 2 * (KK ? KK : a.k);
   if (H64) {
-    const uint64_t code = X >> (64 - kk);
+    uint64_t code = X >> (64 - kk);
+    if (canon) code = min(code, revcomp64(code, kk / 2));
     const uint64_t km = ((uint64_t)((1u << (kk - 32)) - 1u) << 32) | 0xffffffffull;
     return a.raw ? code : hash_b64(code, km);
   } else {
-    const uint32_t code = (uint32_t)(X >> (64 - kk));
+    uint32_t code = (uint32_t)(X >> (64 - kk));
+    if (canon) code = min(code, revcomp32(code, kk / 2));
     const uint32_t km = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
     return a.raw ? code : hash_b32(code, km);
   }
@@ -434,7 +463,7 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
 // Output of one finished super-tile (fast path): its emit bitmask -> ordered slot list in
 // `list` -> prefix via look-back -> records.  Called one super-tile LATE (see the kernel), so
 // the look-back finds its predecessors' aggregates already published.
-template <int W, bool H64, int KK>
+template <int W, bool H64, int KK, bool CN>
 __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, const uint32_t* emit, uint32_t excl,
                                             uint32_t total, uint16_t* list, uint64_t* bcast) {
   using G = FastGeom<W>;
@@ -470,7 +499,7 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
     const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
     const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
     const int64_t q = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
-    a.out_hash[oo] = key_at<H64, KK>(a, q);
+    a.out_hash[oo] = key_at<H64, KK, CN ? 1 : 0>(a, q);
     a.out_pos[oo] = a.pos_base + (uint64_t)q;
   }
   __syncthreads();  // `list` and `emit` are reused next
@@ -480,7 +509,7 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
 // all SUBS sub-tiles into one of two emit bitmasks, publishes the super-tile's record count,
 // and only then outputs its PREVIOUS super-tile -- one super-tile of slack for the
 // predecessors' counts to arrive.
-template <int W, bool H64, int KK>
+template <int W, bool H64, int KK, bool CN>
 __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   using G = FastGeom<W>;
   constexpr int NSWT = G::SUBS * G::NSW;
@@ -510,12 +539,14 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       for (int u = t; u < G::NSW + 3; u += G::TPB) wvb[u] = 0;
       const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi);  // (also the barrier for wvb)
       const int64_t q0 = tile_lo - 1 + (int64_t)t * G::Q;
-      if (a.raw) {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, true>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, true>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+      const uint32_t s0 = (uint32_t)(t * G::Q);
+      constexpr int KMC = CN ? 2 : 0;  // canonical keys: a separate kernel instantiation
+      if (!a.raw) {
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb);
       } else {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, false>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, false>(a, q0, (uint32_t)(t * G::Q), keys, wvb);
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb);
       }
       __syncthreads();
       // window ranges relative to the sub-tile
@@ -545,7 +576,7 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
     const uint32_t excl = (uint32_t)block_exclusive_sum<G::TPB, uint64_t>(cnt, warp_sums, &total);
     if (t == 0) lookback_publish(a.status, tile, total);
     if (pend >= 0)
-      fast_output<W, H64, KK>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
+      fast_output<W, H64, KK, CN>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
                               reinterpret_cast<uint16_t*>(keys), &bcast);
     pend = (int64_t)tile;
     pend_excl = excl;
@@ -553,7 +584,7 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
     cur ^= 1;
   }
   if (pend >= 0)
-    fast_output<W, H64, KK>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
+    fast_output<W, H64, KK, CN>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
                             reinterpret_cast<uint16_t*>(keys), &bcast);
 }
 
@@ -593,12 +624,17 @@ __global__ void __launch_bounds__(kGenTPB) mz_generic_kernel(MzArgs a) {
     for (int u = t; u < NSW + 3; u += kGenTPB) wvb[u] = 0;
     const bool clean = tile_is_clean<kGenTPB>(a, b_lo, b_hi);
     const int64_t q0 = tile_lo - 1 + (int64_t)t * kGenE;
-    if (a.raw) {
-      if (clean) phase1_keys<Key, kGenE, H64, false, 0, true>(a, q0, t * kGenE, keys, wvb);
-      else phase1_keys<Key, kGenE, H64, true, 0, true>(a, q0, t * kGenE, keys, wvb);
+    auto p1 = [&](auto km_tag) {
+      constexpr int KMV = decltype(km_tag)::value;
+      if (clean) phase1_keys<Key, kGenE, H64, false, 0, KMV>(a, q0, t * kGenE, keys, wvb);
+      else phase1_keys<Key, kGenE, H64, true, 0, KMV>(a, q0, t * kGenE, keys, wvb);
+    };
+    if (a.canon) {
+      if (a.raw) p1(std::integral_constant<int, 3>{});
+      else p1(std::integral_constant<int, 2>{});
     } else {
-      if (clean) phase1_keys<Key, kGenE, H64, false, 0, false>(a, q0, t * kGenE, keys, wvb);
-      else phase1_keys<Key, kGenE, H64, true, 0, false>(a, q0, t * kGenE, keys, wvb);
+      if (a.raw) p1(std::integral_constant<int, 1>{});
+      else p1(std::integral_constant<int, 0>{});
     }
     __syncthreads();
     // phase 2: block S/P over slots, blocks of W starting at slot 1 (slot s <-> k-mer tile_lo-1+s)
@@ -664,7 +700,7 @@ int launch_mz(MzArgs a, int path, cudaStream_t st) {
     a.tw = G::TW;                                                                                      \
     a.ntiles = (a.nwin + (uint64_t)G::TW * G::SUBS - 1) / ((uint64_t)G::TW * G::SUBS);                 \
     const size_t smem = sizeof(PackedKey) * G::NS;                                                     \
-    auto kern = mz_fast_kernel<WW, H64V, KKV>;                                                         \
+    auto kern = a.canon ? mz_fast_kernel<WW, H64V, KKV, true> : mz_fast_kernel<WW, H64V, KKV, false>;   \
     MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));      \
     MZS_CUDA(cudaMemsetAsync(a.tile_counter, 0, sizeof(uint32_t), st));                                \
     MZS_CUDA(cudaMemsetAsync(a.status, 0, sizeof(uint64_t) * a.ntiles, st));                           \
@@ -737,7 +773,7 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
                             size_t ws_bytes, void* stream, int path) {
   if (!in || !out || !out->d_count || k < 1 || k > 31 || w < 1) return SLSUM_EINVAL;
   if (in->kind != MZ_IN_ASCII && in->kind != MZ_IN_PACKED2) return SLSUM_EINVAL;
-  if (keymode != MZ_KEY_HASH && keymode != MZ_KEY_RAW) return SLSUM_EINVAL;
+  if (keymode < MZ_KEY_HASH || keymode > MZ_KEY_CANON_RAW) return SLSUM_EINVAL;
   if (in->read_off && in->nreads == 0) return SLSUM_EINVAL;
   if (out->capacity && (!out->hash || !out->pos)) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
@@ -782,7 +818,8 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   a.win_hi = in->win_hi;
   a.k = k;
   a.w = w;
-  a.raw = keymode == MZ_KEY_RAW;
+  a.raw = keymode == MZ_KEY_RAW || keymode == MZ_KEY_CANON_RAW;
+  a.canon = keymode == MZ_KEY_CANON || keymode == MZ_KEY_CANON_RAW;
   a.out_hash = out->hash;
   a.out_pos = out->pos;
   a.capacity = out->capacity;

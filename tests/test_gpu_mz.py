@@ -85,6 +85,23 @@ def test_random_vs_oracle(k, w, path):
 
 
 @pytest.mark.parametrize("path", [0, 1])
+@pytest.mark.parametrize("keymode", [P.MZ_KEY_CANON, P.MZ_KEY_CANON_RAW])
+@pytest.mark.parametrize("k,w", [(15, 10), (19, 10), (1, 1), (2, 3), (4, 5), (8, 7), (16, 5), (17, 9), (26, 6),
+                                 (31, 8), (11, 64)])
+def test_canonical_vs_oracle(k, w, keymode, path):
+    """Canonical (strand-symmetric) keys, NEXT f4 (R32), vs the oracle."""
+    rng = np.random.default_rng(77 * k + w + path + keymode)
+    for n, pn in [(k + w - 1, 0), (5000, 0.0), (60_000, 0.002)]:
+        s = _rand_seq(rng, n, pn=pn, lower=0.05)
+        _same(s, k, w, path=path, keymode=keymode)
+        if n >= 5000:
+            _same(s, k, w, path=path, keymode=keymode, packed=True)
+    c4 = G.C4(nreads=60, tlen=1 << 20)
+    ro = c4.read_off.astype(np.uint64)
+    _same(c4.ascii_range(0, c4.n), k, w, path=path, keymode=keymode, read_off=ro)
+
+
+@pytest.mark.parametrize("path", [0, 1])
 def test_ties_small_alphabets(path):
     rng = np.random.default_rng(3)
     for alpha in (b"A", b"AC", b"ACG"):
@@ -193,7 +210,7 @@ def test_exhaustive_4_pow_8():
     ro = np.arange(0, len(seq) + 1, L, dtype=np.uint64)
     for k in (1, 2, 3):
         for w in (1, 2, 3, 4):
-            for km in (P.MZ_KEY_RAW, P.MZ_KEY_HASH):
+            for km in (P.MZ_KEY_RAW, P.MZ_KEY_HASH, P.MZ_KEY_CANON, P.MZ_KEY_CANON_RAW):
                 for path in (0, 1):
                     _same(seq, k, w, read_off=ro, keymode=km, path=path)
 
