@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4", "lookup"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--canonical", action="store_true",
+                    help="c3/c4: canonical (strand-symmetric) minimizers, MZ_KEY_CANON (NEXT f4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-bases", type=int, default=32_000_000)
     return ap.parse_args()
@@ -273,6 +275,7 @@ def bench_c4(args):
     d_count = torch.zeros(1, dtype=torch.uint64, device="cuda")
     ws = torch.empty(P.mz_workspace_bytes(n, k, w, P.MZ_IN_PACKED2), dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    keymode = P.MZ_KEY_CANON if args.canonical else P.MZ_KEY_HASH
     ev = []
 
     def step(record=False):
@@ -283,7 +286,7 @@ def bench_c4(args):
         if record:
             e[1].record(stream)
         P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, read_off=ro, capacity=cap,
-                        out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws)
+                        out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws, keymode=keymode)
         if record:
             e[2].record(stream)
             ev.append(e)
@@ -316,7 +319,8 @@ def bench_c4(args):
         "metric": "minimizer extraction over a long-read batch, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
         "unit": "Gbases/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "C4: 1M reads, lognormal(mean 10 kbp, sd 8 kbp), 10% substitutions", "k": k, "w": w,
+        "config": {"workload": "C4: 1M reads, lognormal(mean 10 kbp, sd 8 kbp), 10% substitutions"
+                               + (" (canonical minimizers)" if args.canonical else ""), "k": k, "w": w,
                    "bases": n, "reads": c4.nreads, "records": m, "density": m / n,
                    "l2": f"inputs ({n / 1e9:.1f} GB) >> L2; no flush needed"},
         "roofline": {"bound": "alu", "kernel": "mz_fast_kernel<10,0,15> (a2-a7 fused, read-segmented)",
@@ -491,7 +495,8 @@ def main():
             e[1].record(st)
         P.mz_extract_ex(bf.words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=bf.inval, pos_base=sh.base_lo,
                         win_lo=sh.win_lo, win_hi=sh.win_hi, capacity=cap, out_hash=bf.out_h, out_pos=bf.out_p,
-                        d_count=bf.d_count, ws=bf.mz_ws)
+                        d_count=bf.d_count, ws=bf.mz_ws,
+                        keymode=P.MZ_KEY_CANON if args.canonical else P.MZ_KEY_HASH)
         if record:
             e[2].record(st)
         if world == 1:
@@ -658,7 +663,8 @@ def main():
             "value": gbases, "unit": "Gbases/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C3: 3.1 Gbp GC41% 1% N-runs" if c3 is not None else "C1: 1 Mbp uniform",
+            "config": {"workload": ("C3: 3.1 Gbp GC41% 1% N-runs" if c3 is not None else "C1: 1 Mbp uniform")
+                       + (" (canonical minimizers)" if args.canonical else ""),
                        "k": k, "w": w, "bucket_bits": bits, "bases": n_total, "records": m_rec if world == 1 else None,
                        "density": m_rec / max(1, nwin_local) if world == 1 else None,
                        "l2": "inputs (3.1 GB) >> L2 (126 MB); no flush needed", "parallelism": f"shards{world}"},
