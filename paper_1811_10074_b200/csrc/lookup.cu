@@ -7,7 +7,7 @@
 // key and the hits are exactly the stored positions of the seed (R30).
 //
 // Three steps: count (per query), exclusive scan of the counts (-> CSR offsets), emit.
-// A group of kG lanes (8 by default) serves one query: the slice's fingerprints are read kG
+// A group of kG lanes (8; one lane per query for short buckets, see lookup1_kernel) serves one query: the slice's fingerprints are read kG
 // at a time, matches are counted with a group ballot, and in the emit step written in order
 // (ballot prefix inside the group).  Minimizer hashes are skewed low, so queries land in the
 // long buckets more often than the mean bucket length suggests.
@@ -73,6 +73,33 @@ __global__ void __launch_bounds__(kLTPB) lookup_kernel(const uint64_t* __restric
       cnt += __popc(bal);
     }
     if (!EMIT && live && gl == 0) hit_off[i0] = cnt;
+  }
+}
+
+// One thread per query (no ballots): 32 independent random lookups in flight per warp, for
+// tables whose buckets are short (the scan of a bucket is a serial loop in the thread).
+template <bool EMIT>
+__global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restrict__ q, uint64_t nq_cap,
+                                                        const uint64_t* d_nq, int k, int bits,
+                                                        const uint64_t* __restrict__ offsets,
+                                                        const uint32_t* __restrict__ fp,
+                                                        const uint64_t* __restrict__ pos_tab, uint64_t* hit_off,
+                                                        uint64_t* __restrict__ hit_pos, uint64_t hit_cap) {
+  const uint64_t nq = query_count(d_nq, nq_cap);
+  for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
+    const uint32_t f = fp_of(q[i], k);
+    const uint64_t b = f >> (32 - bits);
+    const uint64_t lo = offsets[b], hi = offsets[b + 1];
+    uint64_t o = EMIT ? hit_off[i] : 0;
+    uint64_t cnt = 0;
+    for (uint64_t e = lo; e < hi; ++e) {
+      if (fp[e] == f) {
+        if (EMIT && o < hit_cap) hit_pos[o] = pos_tab[e];
+        ++o;
+        ++cnt;
+      }
+    }
+    if (!EMIT) hit_off[i] = cnt;
   }
 }
 
@@ -175,18 +202,23 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
   const uint64_t nb = (nq + kSB - 1) / kSB;
   uint64_t* bsum = c.take<uint64_t>(nb + 1);
   if (!c.ok) return SLSUM_ENOMEM;
-  static const int lanes = [] {
+  // lanes per query: 1 (a thread per query, the most lookups in flight) when buckets are short
+  // (>= 2^26 buckets for the tables measured), else 8; MZS_LOOKUP_LANES overrides (tuning)
+  static const int lanes_env = [] {
     const char* e = getenv("MZS_LOOKUP_LANES");
-    const int v = e && *e ? atoi(e) : 8;
-    return (v == 8 || v == 16 || v == 32) ? v : 8;
+    const int v = e && *e ? atoi(e) : 0;
+    return (v == 1 || v == 8 || v == 16 || v == 32) ? v : 0;
   }();
+  const int lanes = lanes_env ? lanes_env : (bucket_bits >= 26 ? 1 : 8);
   const uint64_t want = (nq * lanes + kLTPB - 1) / kLTPB;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)num_sms() * 8));
   auto launch = [&](auto emit_tag) -> int {
     constexpr bool E = decltype(emit_tag)::value;
     uint64_t* hp = E ? hit_pos : nullptr;
     const uint64_t hc = E ? hit_cap : 0;
-    if (lanes == 8)
+    if (lanes == 1)
+      lookup1_kernel<E><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+    else if (lanes == 8)
       lookup_kernel<E, 8><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
     else if (lanes == 32)
       lookup_kernel<E, 32><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
