@@ -302,11 +302,9 @@ __device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int
 // Code + key of the k-mer at local position q, from scratch (phase 3 re-derives the hash
 // of every emitted position instead of keeping all keys of a super-tile resident).
 template <bool H64, int KK = 0, int CNM = -1>
-__device__ __forceinline__ uint64_t key_at(const MzArgs& a, int64_t q) {
+__device__ __forceinline__ uint64_t key_from_words(const MzArgs& a, int64_t q, uint64_t A, uint64_t B) {
   const bool canon = CNM < 0 ? a.canon != 0 : CNM == 1;
-  const int64_t wi = q >> 5;
   const uint32_t off = (uint32_t)(q & 31) * 2;
-  const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1);
   const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
   const int kk = 2 * (KK ? KK : a.k);
   if (H64) {
@@ -320,6 +318,10 @@ __device__ __forceinline__ uint64_t key_at(const MzArgs& a, int64_t q) {
     const uint32_t km = (kk == 32) ? 0xffffffffu : ((1u << kk) - 1u);
     return a.raw ? code : hash_b32(code, km);
   }
+}
+template <bool H64, int KK = 0, int CNM = -1>
+__device__ __forceinline__ uint64_t key_at(const MzArgs& a, int64_t q) {
+  return key_from_words<H64, KK, CNM>(a, q, ldw(a, q >> 5), ldw(a, (q >> 5) + 1));
 }
 
 // Phase 3: ordered output of the slots marked in `emit` (S sub-tiles x NS slots each; slot s
@@ -492,15 +494,30 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
   __syncthreads();
   const uint64_t base = *bcast;
   const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
-  for (uint32_t i = threadIdx.x; i < total; i += G::TPB) {
-    const uint64_t oo = base + i;
-    if (oo >= a.capacity) break;
-    const uint32_t slot_all = list[i];
-    const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
-    const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
-    const int64_t q = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
-    a.out_hash[oo] = key_at<H64, KK, CN ? 1 : 0>(a, q);
-    a.out_pos[oo] = a.pos_base + (uint64_t)q;
+  // four records per thread per step: their word loads are all in flight before the hashes
+  const uint32_t lim = (uint32_t)min((uint64_t)total, a.capacity > base ? a.capacity - base : (uint64_t)0);
+  constexpr int U = 4;
+  for (uint32_t i0 = threadIdx.x; i0 < lim; i0 += U * G::TPB) {
+    int64_t q[U];
+    uint64_t A[U], B[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * G::TPB;
+      const uint32_t slot_all = i < lim ? list[i] : 0u;
+      const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
+      const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
+      q[u] = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
+      A[u] = i < lim ? ldw(a, q[u] >> 5) : 0ull;
+      B[u] = i < lim ? ldw(a, (q[u] >> 5) + 1) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * G::TPB;
+      if (i < lim) {
+        a.out_hash[base + i] = key_from_words<H64, KK, CN ? 1 : 0>(a, q[u], A[u], B[u]);
+        a.out_pos[base + i] = a.pos_base + (uint64_t)q[u];
+      }
+    }
   }
   __syncthreads();  // `list` and `emit` are reused next
 }
