@@ -116,13 +116,15 @@ __device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
 // KM bit 1 (CANON): the code is min(forward, reverse complement), the reverse complement
 // rolled alongside (the entering base's complement enters at the top, R32).
 template <class Key, int Q, bool H64, bool CHECK, int KK = 0, int KM = 0>
-__device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint32_t* wvb) {
+__device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint32_t* wvb,
+                                            const uint64_t* pre = nullptr) {
   static_assert(Q <= 33, "validity bits of one strip fit in a u64 shifted by < 32");
   uint64_t vbits = 0;
   const int k = KK ? KK : a.k;
   const int64_t wi = q0 >> 5;
   const uint32_t off = (uint32_t)(q0 & 31) * 2;
-  const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1), C = ldw(a, wi + 2);
+  // pre: the three packed words, already loaded by the caller (prefetched a phase earlier)
+  const uint64_t A = pre ? pre[0] : ldw(a, wi), B = pre ? pre[1] : ldw(a, wi + 1), C = pre ? pre[2] : ldw(a, wi + 2);
   const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
   const uint64_t Y = off ? (B << off) | (C >> (64 - off)) : B;
   // stream of the bases entering after the first k-mer: q0+k, q0+k+1, ...
@@ -279,12 +281,13 @@ namespace {
 
 // Tile cleanliness: no invalid base and no read start strictly inside the tile's bases.
 template <int TPB>
-__device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int64_t b_hi) {
+__device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int64_t b_hi, const uint32_t* pre = nullptr) {
   int dirty = 0;
   if (a.invalid) {
     const int64_t w0 = max((int64_t)0, b_lo >> 5), w1 = min((int64_t)a.nwords - 1, (b_hi - 1) >> 5);
     for (int64_t wi = w0 + threadIdx.x; wi <= w1; wi += TPB) {
-      uint32_t m = __ldg(a.invalid + wi);
+      // pre: this thread's first word, prefetched by the caller
+      uint32_t m = (pre && wi == w0 + (int64_t)threadIdx.x) ? *pre : __ldg(a.invalid + wi);
       // restrict to [b_lo, b_hi)
       const int64_t base = wi << 5;
       if (base < b_lo) m &= 0xffffffffu << (uint32_t)(b_lo - base);
@@ -549,22 +552,38 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
     const uint64_t tile = s_tile;
     if (tile >= a.ntiles) break;
     const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
+    // the packed words and the first invalid-bitmap word a sub-tile needs are loaded one
+    // sub-tile ahead (issued before phase 2 of the previous one), hiding their latency
+    uint64_t pw[3];
+    uint32_t pinv = 0;
+    auto prefetch = [&](int64_t tlo) {
+      const int64_t wi = (tlo - 1 + (int64_t)t * G::Q) >> 5;
+      pw[0] = ldw(a, wi);
+      pw[1] = ldw(a, wi + 1);
+      pw[2] = ldw(a, wi + 2);
+      const int64_t w0 = max((int64_t)0, (tlo - 1) >> 5) + t;
+      pinv = ldi(a, w0);
+    };
+    prefetch(super_lo);
     for (int sub = 0; sub < G::SUBS; ++sub) {
       const int64_t tile_lo = super_lo + (int64_t)sub * G::TW;
       if (tile_lo >= (int64_t)a.nwin) break;
       const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + G::NS + a.k;  // bases touched
       for (int u = t; u < G::NSW + 3; u += G::TPB) wvb[u] = 0;
-      const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi);  // (also the barrier for wvb)
+      const uint32_t inv0 = pinv;
+      const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi, &inv0);  // (also the barrier for wvb)
       const int64_t q0 = tile_lo - 1 + (int64_t)t * G::Q;
       const uint32_t s0 = (uint32_t)(t * G::Q);
+      const uint64_t w3[3] = {pw[0], pw[1], pw[2]};
       constexpr int KMC = CN ? 2 : 0;  // canonical keys: a separate kernel instantiation
       if (!a.raw) {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb);
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb, w3);
       } else {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb);
+        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
       }
+      if (sub + 1 < G::SUBS) prefetch(tile_lo + G::TW);
       __syncthreads();
       // window ranges relative to the sub-tile
       const int vlo = (int)max((int64_t)-1, -tile_lo);
