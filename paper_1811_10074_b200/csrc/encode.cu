@@ -30,14 +30,28 @@ __device__ __forceinline__ void enc4(uint32_t v, uint32_t& packed_byte, uint32_t
   inv4 = ((((~z & 0x80808080u) >> 7) * 0x00204081u) >> 21) & 0xFu;
 }
 
-__global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__ seq, uint64_t n,
-                                                     uint64_t* __restrict__ words, uint32_t* __restrict__ invalid,
-                                                     uint64_t nwords) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nwords) return;
-  const uint64_t b0 = t * 32;
-  uint32_t v[8];
-  if (b0 + 32 <= n && ((reinterpret_cast<uintptr_t>(seq) & 15) == 0)) {
+// Encode the 32 bases of word t from its 8 little-endian 4-byte groups.
+__device__ __forceinline__ void enc_word(const uint32_t (&v)[8], uint64_t b0, uint64_t n, uint64_t& word, uint32_t& inv) {
+  word = 0;
+  inv = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t pb, m;
+    enc4(v[i], pb, m);
+    // bases 4i..4i+3 -> bits (63-8i .. 56-8i)
+    word |= (uint64_t)pb << (56 - 8 * i);
+    inv |= m << (4 * i);
+  }
+  if (b0 + 32 > n) {  // bits past n are 0
+    const uint32_t valid_bases = (uint32_t)(n - b0);
+    word &= valid_bases ? ~0ull << (64 - 2 * valid_bases) : 0ull;
+    inv &= valid_bases >= 32 ? 0xffffffffu : ((1u << valid_bases) - 1u);
+  }
+}
+
+__device__ __forceinline__ void load_word_bytes(const uint8_t* __restrict__ seq, uint64_t b0, uint64_t n, bool al,
+                                                uint32_t (&v)[8]) {
+  if (al && b0 + 32 <= n) {
     const uint4 p = __ldg(reinterpret_cast<const uint4*>(seq + b0));
     const uint4 q = __ldg(reinterpret_cast<const uint4*>(seq + b0 + 16));
     v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w; v[4] = q.x; v[5] = q.y; v[6] = q.z; v[7] = q.w;
@@ -53,23 +67,31 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__
       v[i] = x;
     }
   }
-  uint64_t word = 0;
-  uint32_t inv = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint32_t pb, m;
-    enc4(v[i], pb, m);
-    // bases 4i..4i+3 -> bits (63-8i .. 56-8i)
-    word |= (uint64_t)pb << (56 - 8 * i);
-    inv |= m << (4 * i);
+}
+
+// Two words per thread (words t and t + nthreads): four 16-byte loads in flight before any
+// arithmetic, so each thread covers more of the memory latency.
+__global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__ seq, uint64_t n,
+                                                     uint64_t* __restrict__ words, uint32_t* __restrict__ invalid,
+                                                     uint64_t nwords) {
+  const uint64_t half = (nwords + 1) / 2;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= half) return;
+  const bool al = (reinterpret_cast<uintptr_t>(seq) & 15) == 0;
+  const uint64_t t2 = t + half;
+  uint32_t v0[8], v1[8];
+  load_word_bytes(seq, t * 32, n, al, v0);
+  if (t2 < nwords) load_word_bytes(seq, t2 * 32, n, al, v1);
+  uint64_t w;
+  uint32_t m;
+  enc_word(v0, t * 32, n, w, m);
+  words[t] = w;
+  invalid[t] = m;
+  if (t2 < nwords) {
+    enc_word(v1, t2 * 32, n, w, m);
+    words[t2] = w;
+    invalid[t2] = m;
   }
-  if (b0 + 32 > n) {  // bits past n are 0
-    const uint32_t valid_bases = (uint32_t)(n - b0);
-    word &= valid_bases ? ~0ull << (64 - 2 * valid_bases) : 0ull;
-    inv &= valid_bases >= 32 ? 0xffffffffu : ((1u << valid_bases) - 1u);
-  }
-  words[t] = word;
-  invalid[t] = inv;
 }
 
 }  // namespace
@@ -77,7 +99,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint8_t* __restrict__
 int encode_launch(const uint8_t* seq, uint64_t n, uint64_t* words, uint32_t* invalid, cudaStream_t st) {
   const uint64_t nwords = (n + 31) / 32;
   if (nwords == 0) return SLSUM_OK;
-  const unsigned grid = (unsigned)((nwords + 255) / 256);
+  const unsigned grid = (unsigned)(((nwords + 1) / 2 + 255) / 256);
   encode_kernel<<<grid, 256, 0, st>>>(seq, n, words, invalid, nwords);
   MZS_LAUNCHED();
   return SLSUM_OK;
