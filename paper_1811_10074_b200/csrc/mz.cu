@@ -403,6 +403,7 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
   const int jb = threadIdx.x * G::R;
   PackedKey S[W], kb[W];
   uint32_t sprev;  // slot of the previous window's argmin
+  uint32_t s_carry;  // argmin slot of window jb-1 (FULL strips)
   bool vprev;
   uint64_t em = 0;  // bit i <-> slot jb + 1 + i
   auto valid_of = [&](int j) -> bool {
@@ -413,7 +414,10 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
   auto visit = [&](int j, PackedKey y) {
     const uint32_t s = y.slot();
     if (FULL) {
-      em |= (uint64_t)(s != sprev) << (s - (uint32_t)(jb + 1));
+      // every window's argmin is marked (argmins never decrease, so a repeat hits the same
+      // bit); the carried-in argmin of window jb-1, owned by the strip on the left, is cleared
+      // once after the strip (R3)
+      em |= 1ull << (s - (uint32_t)(jb + 1));
     } else {
       const bool v = valid_of(j);
       const bool e = v && (!vprev || s != sprev) && ((unsigned)(j - elo) < (unsigned)(ehi - elo));
@@ -430,6 +434,7 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
 #pragma unroll
     for (int q = 1; q < W - 1; ++q) p = kmin(p, kb[q]);
     sprev = ((W == 1) ? k0 : kmin(k0, p)).slot();
+    s_carry = sprev;
     vprev = valid_of(jb - 1);
     S[W - 1] = kb[W - 1];
 #pragma unroll
@@ -451,6 +456,10 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
     S[W - 1] = kb[W - 1];
 #pragma unroll
     for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
+  }
+  if (FULL) {
+    const uint32_t rel = s_carry - (uint32_t)(jb + 1);  // wraps (large) when the carry is left of the strip
+    if (rel < 64u) em &= ~(1ull << rel);
   }
   // OR the strip's mask into the shared bitmask (slots jb+1 .. jb+R+W)
   if (em) {
