@@ -238,6 +238,27 @@ struct PackedKey {
 };
 __device__ __forceinline__ PackedKey kmin(PackedKey a, PackedKey b) { return a.v <= b.v ? a : b; }
 
+// The same packed key with the bit pattern of the double 2^52 + (hash << 14 | slot): for keys
+// below 2^52 (2k <= 38) the IEEE order of these doubles is the integer order, so one FP64
+// compare (DSETP, on the FP64 pipe) replaces the two 32-bit compares a 64-bit integer min
+// needs on the ALU pipe -- the minimizer kernel is ALU-issue bound.
+struct DKey {
+  unsigned long long v;
+  __device__ __forceinline__ static DKey make(uint64_t h, uint32_t slot) {
+    return DKey{0x4330000000000000ull | (h << kSlotBits) | slot};
+  }
+  __device__ __forceinline__ uint32_t slot() const { return (uint32_t)(v & kSlotMask); }
+  __device__ __forceinline__ uint64_t hash() const { return (v & 0x000FFFFFFFFFFFFFull) >> kSlotBits; }
+  __device__ __forceinline__ bool operator!=(const DKey& o) const { return v != o.v; }
+};
+__device__ __forceinline__ DKey kmin(DKey a, DKey b) {
+  unsigned long long r;
+  asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\tselp.b64 %0, %3, %4, p;\n\t}"
+      : "=l"(r)
+      : "d"(__longlong_as_double((long long)a.v)), "d"(__longlong_as_double((long long)b.v)), "l"(a.v), "l"(b.v));
+  return DKey{r};
+}
+
 // Wide key for 2k > 50: hash and slot kept apart (ties broken by the slot).
 struct WideKey {
   unsigned long long h;
@@ -396,12 +417,12 @@ struct FastGeom {
 // [vlo, vhi): windows that exist; [elo, ehi): windows allowed to emit (shard range).
 // FULL: every window of the strip (and the one before it) is valid and may emit -- the
 // common case -- so the per-window work is the 3 minima plus the change test.
-template <int W, bool CHECK, bool FULL>
-__device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_t* wvb, int vlo, int vhi, int elo,
+template <int W, bool CHECK, bool FULL, class Key>
+__device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb, int vlo, int vhi, int elo,
                                             int ehi, uint32_t* emit) {
   using G = FastGeom<W>;
   const int jb = threadIdx.x * G::R;
-  PackedKey S[W], kb[W];
+  Key S[W], kb[W];
   uint32_t sprev;  // slot of the previous window's argmin
   uint32_t s_carry;  // argmin slot of window jb-1 (FULL strips)
   bool vprev;
@@ -411,7 +432,7 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
     const bool in = (unsigned)(j - vlo) < (unsigned)(vhi - vlo);
     return CHECK ? (in && wv_bit(wvb, j + W)) : in;
   };
-  auto visit = [&](int j, PackedKey y) {
+  auto visit = [&](int j, Key y) {
     const uint32_t s = y.slot();
     if (FULL) {
       // every window's argmin is marked (argmins never decrease, so a repeat hits the same
@@ -427,10 +448,10 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
     sprev = s;
   };
   {
-    const PackedKey k0 = keys[jb];
+    const Key k0 = keys[jb];
 #pragma unroll
     for (int q = 0; q < W; ++q) kb[q] = keys[jb + 1 + q];
-    PackedKey p = kb[0];
+    Key p = kb[0];
 #pragma unroll
     for (int q = 1; q < W - 1; ++q) p = kmin(p, kb[q]);
     sprev = ((W == 1) ? k0 : kmin(k0, p)).slot();
@@ -447,7 +468,7 @@ __device__ __forceinline__ void fast_phase2(const PackedKey* keys, const uint32_
     const int sb = jb + 1 + b * W;
 #pragma unroll
     for (int q = 0; q < W; ++q) kb[q] = keys[sb + q];
-    PackedKey p = kb[0];
+    Key p = kb[0];
 #pragma unroll
     for (int q = 0; q < W - 1; ++q) {
       if (q > 0) p = kmin(p, kb[q]);
@@ -544,7 +565,9 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   constexpr int NSWT = G::SUBS * G::NSW;
   constexpr int WPT = (NSWT + G::TPB - 1) / G::TPB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PackedKey* keys = reinterpret_cast<PackedKey*>(smem_raw);
+  // 2k <= 38 with a compile-time k: FP64-compare keys (DKey); otherwise 64-bit integer keys
+  using Key = typename std::conditional<(KK > 0 && 2 * KK + kSlotBits <= 52), DKey, PackedKey>::type;
+  Key* keys = reinterpret_cast<Key*>(smem_raw);
   __shared__ uint32_t emit[2][NSWT + 2];
   __shared__ uint32_t wvb[G::NSW + 3];
   __shared__ uint64_t warp_sums[G::TPB / 32];
@@ -586,11 +609,11 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       const uint64_t w3[3] = {pw[0], pw[1], pw[2]};
       constexpr int KMC = CN ? 2 : 0;  // canonical keys: a separate kernel instantiation
       if (!a.raw) {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb, w3);
+        if (clean) phase1_keys<Key, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<Key, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb, w3);
       } else {
-        if (clean) phase1_keys<PackedKey, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
-        else phase1_keys<PackedKey, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
+        if (clean) phase1_keys<Key, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<Key, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
       }
       if (sub + 1 < G::SUBS) prefetch(tile_lo + G::TW);
       __syncthreads();
