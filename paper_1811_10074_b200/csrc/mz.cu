@@ -26,6 +26,8 @@ namespace {
 constexpr int kSlotBits = 14;  // slot index inside a tile (< 16384)
 constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1;
 
+struct DKey;  // defined with the other key types below
+
 // H_b (R5): the masked Wang/minimap2 integer mix, all arithmetic mod 2^b.
 __device__ __forceinline__ uint32_t hash_b32(uint32_t x, uint32_t m) {
   x = (x * 0x1FFFFFu - 1u) & m;  // (2^21-1) x - 1
@@ -211,7 +213,12 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
       }
       const uint32_t c = (CANON && rc < code) ? rc : code;
       const uint32_t h = RAW ? c : hash_b32(c, km);
-      keys[s0 + s] = Key::make(h, s0 + s);
+      if constexpr (std::is_same<Key, DKey>::value) {
+        // h * 2^14 + slot as one 32x32->64 multiply-add (FMA pipe), then the exponent bits
+        keys[s0 + s] = Key{0x4330000000000000ull | ((uint64_t)h * (1ull << kSlotBits) + (s0 + s))};
+      } else {
+        keys[s0 + s] = Key::make(h, s0 + s);
+      }
     }
   }
   if (CHECK && vbits) {
