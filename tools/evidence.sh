@@ -21,4 +21,14 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sls
   -o $O/full_c2_generic_w16 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2a.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 11 -c 1 \
   -o $O/full_c2_doubling_w4 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2b.log 2>&1
+timeout 600 python bench.py --config lookup --steps 5 > $O/bench_lookup.json 2> $O/bench_lookup.err
+# summaries are made here (gpurun copies back at most 64 MiB): launch list, --set full table,
+# per-kernel DRAM traffic; the large reports are then dropped
+python tools/ncu_summary.py launches $O/launches_c3.csv --last-step encode_kernel > $O/summary_launches.md
+for r in full_c3 full_c2_generic_w16 full_c2_doubling_w4; do
+  python tools/ncu_summary.py report $O/$r.ncu-rep --bases 3.1e9 > $O/summary_$r.md 2>&1
+done
+python tools/ncu_summary.py traffic $O/full_c3.ncu-rep > $O/traffic_c3.json
+python tools/src_hot.py $O/full_c3.ncu-rep mz_fast --per 3.1e9 --top 40 > $O/srchot_mz.txt 2>&1
+rm -f $O/full_c3.ncu-rep
 echo done
