@@ -616,6 +616,43 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
                "pipeline": "2 buffer sets, streams H2D | compute | D2H; step i's D2H overlaps step i+1"}
         del host_in, host_off, host_pos, seqd, B1
+    elif not args.no_e2e and world > 1:
+        # N GPUs: every rank copies its shard's ASCII in (H2D), runs the step (extraction, then
+        # the seed-table exchange over NCCL) and reads its slice of the table back (D2H); the
+        # time is the max over ranks (no cross-step pipelining here)
+        host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        host_in.copy_(seq)
+        seq2 = torch.empty_like(seq)
+        torch.cuda.synchronize()
+
+        def e2e_step_mg():
+            seq2.copy_(host_in, non_blocking=True)
+            off, pl, fl, base = step(seq2)
+            ho = torch.empty(off.numel(), dtype=off.dtype, pin_memory=True)
+            hp = torch.empty(pl.numel(), dtype=pl.dtype, pin_memory=True)
+            ho.copy_(off, non_blocking=True)
+            hp.copy_(pl, non_blocking=True)
+            torch.cuda.synchronize()
+            return 8 * (off.numel() + pl.numel())
+
+        e2e_step_mg()
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        bev = torch.cuda.Event(enable_timing=True)
+        ke = max(1, min(args.steps, 3))
+        a.record(stream)
+        d2h = 0
+        for _ in range(ke):
+            d2h = e2e_step_mg()
+        bev.record(stream)
+        barrier()
+        tt = torch.tensor([a.elapsed_time(bev) / ke], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+        e2e = {"value": n_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gbases/s", "h2d_bytes_per_step": n,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
+               "note": "per-rank bytes (rank 0); time = max over ranks"}
+        del host_in, seq2
 
     # ---------------- rooflines (algorithmic work / event time of the launches)
     m_rec = m_local
