@@ -15,6 +15,7 @@
 // shared memory (L44: "every sum ... is a prefix sum ... O(log(w))"; abstract L8), finished
 // by the overlap t_m[i] (+) t_m[i+w-2^m] for idempotent ops or by the binary digits of w.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -22,6 +23,11 @@ namespace mzs {
 namespace {
 
 // elements of one staged P or S array: L plus 16 B of padding per 128 B (and one spare vector)
+inline bool env_flag(const char* name) {  // tests / A-B timing only
+  const char* v = getenv(name);
+  return v && v[0] == '1';
+}
+
 template <class T>
 constexpr uint32_t slsum_smem_len(uint32_t L) {
   return L + (16 / sizeof(T)) * (L / (128 / sizeof(T)) + 1);
@@ -238,10 +244,85 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_kernel(const typename Op::
   }
 }
 
+
+// GENERIC path for small power-of-two w (W | E): the same block decomposition (Alg. 2, blocks
+// of W aligned at the warp tile), but a block never straddles two lanes, so P and S are pure
+// register strips and the only exchange is the W-1 prefix values the last outputs of a lane
+// need from the next lane (shuffles).  Each warp owns a tile of 32E inputs and emits the first
+// 31E outputs (the last lane is the halo), so there is no shared memory and no barrier.
+template <class Op, int W>
+__global__ void __launch_bounds__(256) slsum_generic_warp_kernel(const typename Op::T* __restrict__ x,
+                                                                typename Op::T* __restrict__ y, uint64_t n,
+                                                                uint64_t nout) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  static_assert(E % W == 0 && W <= E, "blocks inside a lane");
+  constexpr uint64_t kOut = 31ull * E;  // outputs per warp
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t t0 = warp * kOut;            // first input (and output) of the warp's tile
+  if (t0 >= nout) return;                     // uniform per warp
+  const uint64_t g = t0 + (uint64_t)lane * E;
+  T v[E];
+  if (g + E <= n && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(v + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+  }
+  // P: prefix fold from the start of the block; S: suffix fold to its end (blocks of W)
+  T P[E], S[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) P[j] = (j % W == 0) ? v[j] : Op::op(P[j - (j % W == 0 ? 0 : 1)], v[j]);
+#pragma unroll
+  for (int j = E - 1; j >= 0; --j) S[j] = (j % W == W - 1) ? v[j] : Op::op(v[j], S[j + (j % W == W - 1 ? 0 : 1)]);
+  // the next lane's first W-1 prefix values
+  T Pn[W > 1 ? W - 1 : 1];
+#pragma unroll
+  for (int q = 0; q < W - 1; ++q) Pn[q] = shfl_down(P[q], 1);
+  if (lane == 31) return;                     // the halo lane has no outputs of its own
+  T o[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    if (j % W == 0) o[j] = S[j];
+    else o[j] = Op::op(S[j], (j + W - 1 < E) ? P[(j + W - 1) % E] : Pn[(j + W - 1 - E) % (W > 1 ? W - 1 : 1)]);
+  }
+  if (g + E <= nout && ((reinterpret_cast<uintptr_t>(y + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (g + j < nout) y[g + j] = o[j];
+  }
+}
+
+template <class Op, int W>
+int launch_generic_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  const uint64_t nout = n - w + 1;
+  const uint64_t warps = (nout + 31ull * E - 1) / (31ull * E);
+  const uint64_t grid = (warps + 7) / 8;
+  slsum_generic_warp_kernel<Op, W><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n,
+                                                                  nout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
   constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  // small power-of-two w: the warp-tiled, shared-memory-free variant of the same decomposition
+  if (!env_flag("MZS_SLSUM_NO_WARP")) {
+    if (w == 2) return launch_generic_warp<Op, 2>(xv, yv, n, w, st);
+    if (w == 4) return launch_generic_warp<Op, 4>(xv, yv, n, w, st);
+    if (w == 8) return launch_generic_warp<Op, 8>(xv, yv, n, w, st);
+    if (w == 16 && E >= 16) return launch_generic_warp<Op, E >= 16 ? 16 : 8>(xv, yv, n, w, st);
+  }
   const uint64_t nout = n - w + 1;
   // smallest CTA whose tile keeps the halo (w-1) under 1/8 of it; 1024 threads max
   int tpb = 256;
