@@ -312,6 +312,92 @@ int launch_generic_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaSt
   return SLSUM_OK;
 }
 
+
+// GENERIC path for w = M*E (M in {2,4,8} lanes per block): blocks span M aligned lanes of a
+// warp.  P and S are in-lane prefix / suffix strips plus an M-lane exclusive scan across the
+// block's lanes (order-preserving: the left operand is always the earlier part); the combine
+// takes P[i+w-1] from lanes l+M and l+M-1 by shuffles.  A warp emits (32-M)*E outputs (the
+// last M lanes are the halo); no shared memory, no barrier.
+template <class Op, int M>
+__global__ void __launch_bounds__(256) slsum_generic_warpm_kernel(const typename Op::T* __restrict__ x,
+                                                                 typename Op::T* __restrict__ y, uint64_t n,
+                                                                 uint64_t nout) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  static_assert(M >= 2 && M <= 16 && (M & (M - 1)) == 0, "M lanes per block");
+  constexpr uint64_t kOut = (uint64_t)(32 - M) * E;  // outputs per warp
+  const uint32_t lane = threadIdx.x & 31, gl = lane & (M - 1);  // lane inside its block
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t t0 = warp * kOut;
+  if (t0 >= nout) return;  // uniform per warp
+  const uint64_t g = t0 + (uint64_t)lane * E;
+  T v[E];
+  if (g + E <= n && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(v + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+  }
+  T P[E], S[E];
+  P[0] = v[0];
+#pragma unroll
+  for (int j = 1; j < E; ++j) P[j] = Op::op(P[j - 1], v[j]);
+  S[E - 1] = v[E - 1];
+#pragma unroll
+  for (int j = E - 2; j >= 0; --j) S[j] = Op::op(v[j], S[j + 1]);
+  // exclusive fold of the lanes to the left inside the block (forward), to the right (backward)
+  T lt = P[E - 1], rt = S[0];   // running inclusive folds
+#pragma unroll
+  for (int o = 1; o < M; o <<= 1) {
+    const T a = shfl_up(lt, o);
+    const T b = shfl_down(rt, o);
+    if (gl >= (uint32_t)o) lt = Op::op(a, lt);
+    if (gl + o < (uint32_t)M) rt = Op::op(rt, b);
+  }
+  const T le = shfl_up(lt, 1), re = shfl_down(rt, 1);  // exclusive: the neighbour's inclusive fold
+  if (gl > 0) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) P[j] = Op::op(le, P[j]);
+  }
+  if (gl < (uint32_t)(M - 1)) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) S[j] = Op::op(S[j], re);
+  }
+  // y_i = S[i] (+) P[i+w-1]: element j >= 1 takes lane l+M's P[j-1], element 0 lane l+M-1's P[E-1]
+  T Pm[E];
+#pragma unroll
+  for (int j = 0; j < E - 1; ++j) Pm[j] = shfl_down(P[j], M);
+  Pm[E - 1] = shfl_down(P[E - 1], M - 1);
+  if (lane >= 32 - M) return;  // halo lanes
+  T o[E];
+  o[0] = (gl == 0) ? S[0] : Op::op(S[0], Pm[E - 1]);  // a block head is its own window start
+#pragma unroll
+  for (int j = 1; j < E; ++j) o[j] = Op::op(S[j], Pm[j - 1]);
+  if (g + E <= nout && ((reinterpret_cast<uintptr_t>(y + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (g + j < nout) y[g + j] = o[j];
+  }
+}
+
+template <class Op, int M>
+int launch_generic_warpm(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  const uint64_t nout = n - w + 1;
+  const uint64_t warps = (nout + (uint64_t)(32 - M) * E - 1) / ((uint64_t)(32 - M) * E);
+  const uint64_t grid = (warps + 7) / 8;
+  slsum_generic_warpm_kernel<Op, M><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv),
+                                                                   n, nout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
@@ -322,6 +408,9 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 4) return launch_generic_warp<Op, 4>(xv, yv, n, w, st);
     if (w == 8) return launch_generic_warp<Op, 8>(xv, yv, n, w, st);
     if (w == 16 && E >= 16) return launch_generic_warp<Op, E >= 16 ? 16 : 8>(xv, yv, n, w, st);
+    if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
+    if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
+    if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);
   }
   const uint64_t nout = n - w + 1;
   // smallest CTA whose tile keeps the halo (w-1) under 1/8 of it; 1024 threads max
