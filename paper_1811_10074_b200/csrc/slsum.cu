@@ -398,6 +398,135 @@ int launch_generic_warpm(const void* xv, void* yv, uint64_t n, uint32_t w, cudaS
   return SLSUM_OK;
 }
 
+
+// GENERIC path for w = M*E with M >= 16 lanes per block (w = 256 .. 2048 for 4-byte types):
+// the warp-tiled decomposition at CTA scale.  In-lane P/S strips, shuffle scans across the
+// block's lanes inside a warp, a shared-memory step across warps when a block spans several
+// warps (M > 32); P is then staged in shared memory (16 B of padding per 128 B) so that every
+// lane can read the P[i+w-1] of the block M lanes ahead.  A CTA of TPB lanes emits (TPB-M)*E
+// outputs (the last M lanes are the halo).
+template <class Op, int TPB, int M>
+__global__ void __launch_bounds__(TPB) slsum_generic_cta_kernel(const typename Op::T* __restrict__ x,
+                                                                typename Op::T* __restrict__ y, uint64_t n,
+                                                                uint64_t nout) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  constexpr uint32_t G = 128 / sizeof(T);
+  constexpr int L = TPB * E;
+  constexpr int NW = TPB / 32;
+  constexpr int MW = M < 32 ? M : 32;  // lanes of one block inside one warp
+  static_assert(M >= 16 && (M & (M - 1)) == 0 && M < TPB, "M lanes per block");
+  constexpr uint64_t kOut = (uint64_t)(TPB - M) * E;
+  auto sidx = [](uint32_t i) { return i + OV * (i / G); };
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sP = reinterpret_cast<T*>(smem_raw);
+  __shared__ T wl[NW], wr[NW];  // per-warp left / right folds of its part of a block
+  const uint32_t t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const uint32_t gl = t & (M - 1);          // lane inside its block
+  const uint32_t gw = lane & (MW - 1);      // lane inside its block's part of this warp
+  const uint64_t t0 = (uint64_t)blockIdx.x * kOut;
+  const uint64_t g = t0 + (uint64_t)t * E;
+  T v[E];
+  if (g + E <= n && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(v + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+  }
+  T P[E], S[E];
+  P[0] = v[0];
+#pragma unroll
+  for (int j = 1; j < E; ++j) P[j] = Op::op(P[j - 1], v[j]);
+  S[E - 1] = v[E - 1];
+#pragma unroll
+  for (int j = E - 2; j >= 0; --j) S[j] = Op::op(v[j], S[j + 1]);
+  T lt = P[E - 1], rt = S[0];  // inclusive folds across the block's lanes in this warp
+#pragma unroll
+  for (int o = 1; o < MW; o <<= 1) {
+    const T a = shfl_up(lt, o);
+    const T b = shfl_down(rt, o);
+    if (gw >= (uint32_t)o) lt = Op::op(a, lt);
+    if (gw + o < (uint32_t)MW) rt = Op::op(rt, b);
+  }
+  T le = shfl_up(lt, 1), re = shfl_down(rt, 1);  // exclusive, inside the warp
+  bool has_le = gw > 0, has_re = gw + 1 < (uint32_t)MW;
+  if (M > 32) {
+    // blocks span M/32 warps: fold in the totals of the block's earlier / later warps
+    if (lane == 31) wl[wid] = lt;
+    if (lane == 0) wr[wid] = rt;
+    __syncthreads();
+    constexpr int BW = M > 32 ? M / 32 : 1;  // warps per block
+    const int wb = (int)(wid & (BW - 1));     // warp index inside the block
+    if (wb > 0) {
+      T c = wl[wid - wb];
+      for (int q = 1; q < wb; ++q) c = Op::op(c, wl[wid - wb + q]);
+      le = has_le ? Op::op(c, le) : c;
+      has_le = true;
+    }
+    if (wb < BW - 1) {
+      T c = wr[wid + BW - 1 - wb];
+      for (int q = BW - 2 - wb; q >= 1; --q) c = Op::op(wr[wid + q], c);
+      re = has_re ? Op::op(re, c) : c;
+      has_re = true;
+    }
+  }
+  if (has_le) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) P[j] = Op::op(le, P[j]);
+  }
+  if (has_re) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) S[j] = Op::op(S[j], re);
+  }
+  {
+    const uint32_t b0 = sidx(t * E);
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(sP + b0 + q) = *reinterpret_cast<const uint4*>(P + q);
+  }
+  __syncthreads();
+  if (t >= (uint32_t)(TPB - M)) return;  // halo lanes
+  // y_i = S[i] (+) P[i+w-1]; for this lane i+w-1 = (t+M)*E - 1 + j
+  T Pw[E];
+  Pw[0] = sP[sidx((t + M) * E - 1)];
+  {
+    T nx[E];
+    const uint32_t b1 = sidx((t + M) * E);
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(nx + q) = *reinterpret_cast<const uint4*>(sP + b1 + q);
+#pragma unroll
+    for (int j = 1; j < E; ++j) Pw[j] = nx[j - 1];
+  }
+  T o[E];
+  o[0] = (gl == 0) ? S[0] : Op::op(S[0], Pw[0]);
+#pragma unroll
+  for (int j = 1; j < E; ++j) o[j] = Op::op(S[j], Pw[j]);
+  if (g + E <= nout && ((reinterpret_cast<uintptr_t>(y + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (g + j < nout) y[g + j] = o[j];
+  }
+}
+
+template <class Op, int TPB, int M>
+int launch_generic_cta(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  const uint64_t nout = n - w + 1;
+  const uint64_t kOut = (uint64_t)(TPB - M) * E;
+  const uint64_t grid = (nout + kOut - 1) / kOut;
+  const size_t smem = sizeof(T) * slsum_smem_len<T>(TPB * E);
+  auto k = slsum_generic_cta_kernel<Op, TPB, M>;
+  MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, nout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
@@ -411,6 +540,9 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);
+    if (w == 16 * E) return launch_generic_cta<Op, 256, 16>(xv, yv, n, w, st);
+    if (w == 32 * E) return launch_generic_cta<Op, 512, 32>(xv, yv, n, w, st);
+    if (w == 64 * E) return launch_generic_cta<Op, 1024, 64>(xv, yv, n, w, st);
   }
   const uint64_t nout = n - w + 1;
   // smallest CTA whose tile keeps the halo (w-1) under 1/8 of it; 1024 threads max
