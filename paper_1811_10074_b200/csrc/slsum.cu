@@ -540,9 +540,9 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);
-    if (w == 16 * E) return launch_generic_cta<Op, 256, 16>(xv, yv, n, w, st);
+    if (w == 16 * E) return launch_generic_cta<Op, 256, 16>(xv, yv, n, w, st);  // 256 > 512 lanes (75 vs 68 %)
     if (w == 32 * E) return launch_generic_cta<Op, 512, 32>(xv, yv, n, w, st);
-    if (w == 64 * E) return launch_generic_cta<Op, 1024, 64>(xv, yv, n, w, st);
+    if (w == 64 * E) return launch_generic_cta<Op, 512, 64>(xv, yv, n, w, st);  // 512 > 1024 lanes (61 vs 54 %)
   }
   const uint64_t nout = n - w + 1;
   // smallest CTA whose tile keeps the halo (w-1) under 1/8 of it; 1024 threads max
