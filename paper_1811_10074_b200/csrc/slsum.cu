@@ -570,10 +570,90 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
   return SLSUM_OK;
 }
 
+
+// COMMUTATIVE path for power-of-two w <= 64: the ceil(log2 w) doubling rounds
+// t_{r+1}[i] = t_r[i] (+) t_r[i + 2^r] on a warp tile held in registers (E consecutive values
+// per lane).  A round with 2^r < E pulls the next lane's first 2^r values by shuffles, one
+// with 2^r >= E pulls whole registers from lane + 2^r/E.  For w = 2^m, t_m is the window
+// fold itself (no finishing combine).  Each warp emits the outputs whose windows fit in its
+// 32E inputs; no shared memory, no barrier.
+template <class Op, int W>
+__global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename Op::T* __restrict__ x,
+                                                                 typename Op::T* __restrict__ y, uint64_t n,
+                                                                 uint64_t nout) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  static_assert((W & (W - 1)) == 0 && W >= 2 && W <= 4 * E, "power-of-two w, halo within a warp");
+  constexpr int HL = (W - 1 + E - 1) / E;             // halo lanes
+  constexpr uint64_t kOut = (uint64_t)(32 - HL) * E;  // outputs per warp
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t t0 = warp * kOut;
+  if (t0 >= nout) return;  // uniform per warp
+  const uint64_t g = t0 + (uint64_t)lane * E;
+  T t[E];
+  if (g + E <= n && ((reinterpret_cast<uintptr_t>(x + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(t + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) t[j] = (g + j < n) ? x[g + j] : Op::id();
+  }
+#pragma unroll
+  for (int d = 1; d < W; d <<= 1) {
+    T u[E];
+    if (d < E) {
+      T nx[E];
+#pragma unroll
+      for (int j = 0; j < d; ++j) nx[j] = shfl_down(t[j], 1);
+#pragma unroll
+      for (int j = 0; j < E; ++j) u[j] = Op::op(t[j], j + d < E ? t[(j + d) % E] : nx[(j + d - E) % E]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < E; ++j) u[j] = Op::op(t[j], shfl_down(t[j], d / E));
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j) t[j] = u[j];
+  }
+  if (lane >= 32 - HL) return;  // halo lanes
+  if (g + E <= nout && ((reinterpret_cast<uintptr_t>(y + g) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(t + q);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+      if (g + j < nout) y[g + j] = t[j];
+  }
+}
+
+template <class Op, int W>
+int launch_doubling_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr int HL = (W - 1 + E - 1) / E;
+  const uint64_t nout = n - w + 1;
+  const uint64_t kOut = (uint64_t)(32 - HL) * E;
+  const uint64_t warps = (nout + kOut - 1) / kOut;
+  slsum_doubling_warp_kernel<Op, W><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
+      static_cast<const T*>(xv), static_cast<T*>(yv), n, nout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
   constexpr int TPB = 512;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  if (!env_flag("MZS_SLSUM_NO_WARP")) {  // power-of-two w <= 4E: registers and shuffles only
+    if (w == 2) return launch_doubling_warp<Op, 2>(xv, yv, n, w, st);
+    if (w == 4) return launch_doubling_warp<Op, 4>(xv, yv, n, w, st);
+    if (w == 8) return launch_doubling_warp<Op, 8>(xv, yv, n, w, st);
+    if (w == 16) return launch_doubling_warp<Op, 16>(xv, yv, n, w, st);
+    if (w == 32) return launch_doubling_warp<Op, 32>(xv, yv, n, w, st);
+    if (w == 4 * E) return launch_doubling_warp<Op, 4 * E>(xv, yv, n, w, st);
+  }
   const uint64_t nout = n - w + 1;
   // tile: tout = 8*TPB outputs (register accumulators) from L = tout + w - 1 inputs held in
   // two ping-pong shared-memory buffers (<= 200 KB)
