@@ -93,8 +93,8 @@ def test_unaligned_inputs():
     for m, span in ((70_001, 10 ** 6), (70_001, 10 ** 11)):
         key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
         pos = np.sort(rng.choice(span, size=m, replace=False)).astype(np.uint64)
-        kt = _dev(np.concatenate([[0], key]).astype(np.uint64))[1:]
-        pt = _dev(np.concatenate([[0], pos]).astype(np.uint64))[1:]
+        kt = _dev(np.concatenate([np.zeros(1, np.uint64), key]))[1:]
+        pt = _dev(np.concatenate([np.zeros(1, np.uint64), pos]))[1:]
         assert kt.data_ptr() % 16 == 8
         off, po, fp = P.seedtable_build(kt, pt, 19, 24)
         wo, wf, wp = O.seedtable(key, pos, 19, 24)

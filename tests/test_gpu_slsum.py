@@ -116,6 +116,22 @@ def test_recurrent_rejects_non_invertible(op):
     assert e.value.rc == P.SLSUM_EUNSUPPORTED
 
 
+@pytest.mark.parametrize("w", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("path", ["generic", "commutative"])
+def test_unaligned_and_ragged_views(w, path):
+    """The warp- and CTA-tiled kernels fall back to scalar loads/stores for views 4 or 8 bytes
+    off a 16-byte boundary, and handle ragged tails; bit-exact vs the oracle (u32 / u64)."""
+    pth = P.SLSUM_PATH_GENERIC if path == "generic" else P.SLSUM_PATH_COMMUTATIVE
+    rng = np.random.default_rng(w * 3 + len(path))
+    for op, dt in ((P.SLSUM_MIN_U32, np.uint32), (P.SLSUM_ADD_U32, np.uint32), (P.SLSUM_MIN_U64, np.uint64)):
+        for n in (w, w + 3, 3 * 512 + 7, 40_003):
+            x = rng.integers(0, 2 ** 32 if dt == np.uint32 else 2 ** 63, size=n, dtype=np.uint64).astype(dt)
+            xt = torch.from_numpy(np.concatenate([np.zeros(1, dt), x])).cuda()[1:]
+            yb = torch.empty(n - w + 2, dtype=xt.dtype, device="cuda")
+            y = P.slsum_run(op, w, xt, y=yb[1:], path=pth)
+            assert np.array_equal(y.cpu().numpy(), O.slsum(dict(OPS)[op], w, x)), (op, n)
+
+
 def test_affine_rejected_by_commutative_path():
     x = torch.zeros((100, 2), dtype=torch.uint32, device="cuda")
     with pytest.raises(P.SlsumError) as e:
