@@ -45,6 +45,9 @@ SEEDTABLE_BYTES_PER_REC = 8 + 12 + 12   # histogram reads 8 B, the scatter reads
 # algorithmic 32-bit integer operations per base of the fused minimizer kernel
 # (k=19, w=10): roll 3 + H_38 28 + key 2 + three 64-bit minima 12 + change/emit 3
 MZ_INT_OPS_PER_BASE = {19: 48, 15: 30}
+# N>1 seed-table exchange: "p2p" = partition fused with the all-to-all over symmetric memory
+# (dist.exchange_seedtable_p2p, the product); "nccl" = partition + NCCL all_to_all_single
+EXCHANGE = os.environ.get("MZS_EXCHANGE", "p2p")
 SM_COUNT, INT32_LANES_PER_SM_CLK = 148, 128   # 4 SMSPs x 32 lanes issue (B200_PROFILING / B300_MICROARCH)
 
 
@@ -505,7 +508,8 @@ def main():
             res = (bf.offsets, bf.pos_out)
         else:
             m = int(bf.d_count.view(torch.int64).item())
-            res = D.exchange_seedtable(bf.out_h[:m], bf.out_p[:m], m, k, bits, D.CudaPhases())
+            xchg = D.exchange_seedtable_p2p if EXCHANGE == "p2p" else D.exchange_seedtable
+            res = xchg(bf.out_h[:m], bf.out_p[:m], m, k, bits, D.CudaPhases())
         if record:
             e[3].record(st)
             ev["encode"].append((e[0], e[1]))
@@ -516,7 +520,10 @@ def main():
     # encode + mz + seed table: path-select kernel, 3 narrow passes x (upsweep, chunk scan, digit
     # scan, downsweep), 3 wide passes (enqueued, gated off at entry), 4 pointer-table kernels
     table_launches = 1 + 12 + 12 + 4
-    launches_per_step = 1 + 1 + (table_launches if world == 1 else 1 + (1 + 4 + 4) + (1 + 12 + 12 + 4))
+    # N>1: count, partition (NCCL: ctl + 4 narrow + 4 wide; p2p: ctl + 3 scan kernels + the fused
+    # nsweep writing into the peers), finalize (ctl + 2 passes x 12 + 4)
+    part = 5 if EXCHANGE == "p2p" else 1 + 4 + 4
+    launches_per_step = 1 + 1 + (table_launches if world == 1 else 1 + part + (1 + 12 + 12 + 4))
 
     def barrier():
         if world > 1:
@@ -618,7 +625,7 @@ def main():
         del host_in, host_off, host_pos, seqd, B1
     elif not args.no_e2e and world > 1:
         # N GPUs: every rank copies its shard's ASCII in (H2D), runs the step (extraction, then
-        # the seed-table exchange over NCCL) and reads its slice of the table back (D2H); the
+        # the seed-table exchange, fused p2p or NCCL) and reads its slice of the table back (D2H); the
         # time is the max over ranks (no cross-step pipelining here)
         host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         host_in.copy_(seq)
@@ -704,7 +711,8 @@ def main():
                        + (" (canonical minimizers)" if args.canonical else ""),
                        "k": k, "w": w, "bucket_bits": bits, "bases": n_total, "records": m_rec if world == 1 else None,
                        "density": m_rec / max(1, nwin_local) if world == 1 else None,
-                       "l2": "inputs (3.1 GB) >> L2 (126 MB); no flush needed", "parallelism": f"shards{world}"},
+                       "l2": "inputs (3.1 GB) >> L2 (126 MB); no flush needed", "parallelism": f"shards{world}",
+                       "exchange": EXCHANGE if world > 1 else None},
             "roofline": roof,
             "roofline_table": roof_table,
             "hbm_step": step_hbm,

@@ -217,6 +217,21 @@ size_t seedtable_partition_workspace_bytes(uint64_t m, int nranks);
 int seedtable_partition(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
                         int k, int bucket_bits, int nranks, uint32_t* send_fp, uint64_t* send_pos,
                         uint64_t* send_counts, void* ws, size_t ws_bytes, void* stream);
+/* seedtable_partition_p2p: the partition FUSED with the all-to-all.  The stable
+ *   pass on the owner digit writes each entry directly into its owner's receive buffers
+ *   (peer_fp[o] uint32 / peer_pos[o] uint64: device pointers, typically peer-mapped symmetric
+ *   memory over NVLink), starting at peer_base[o], the number of entries for owner o held by
+ *   the senders of lower rank.  peer_fp/peer_pos/peer_base are HOST arrays of nranks values.
+ *   Requires nranks >= 2 and pos ascending with pos[m-1] - pos[0] < 2^32 (one shard of < 4.29
+ *   Gbases); returns SLSUM_EUNSUPPORTED otherwise (use partition + NCCL all_to_all).  Reads the
+ *   device count and two positions (a short synchronization), then runs asynchronously and
+ *   synchronizes the stream before returning.  The caller barriers across ranks before the
+ *   owners read their buffers. */
+size_t seedtable_partition_p2p_workspace_bytes(uint64_t m, int nranks);
+int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
+                            int k, int bucket_bits, int nranks, const uint64_t* peer_fp,
+                            const uint64_t* peer_pos, const uint64_t* peer_base, void* ws,
+                            size_t ws_bytes, void* stream);
 size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bits, int nranks);
 int seedtable_finalize(const uint32_t* recv_fp, const uint64_t* recv_pos, uint64_t m_recv,
                        const uint32_t* global_counts, int bucket_bits, int rank, int nranks,

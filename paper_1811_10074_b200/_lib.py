@@ -74,6 +74,8 @@ _st_build = _sig("seedtable_build", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _vp, 
 _st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
 _st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
 _st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+_st_p2p_ws = _sig("seedtable_partition_p2p_workspace_bytes", _sz, _u64, _i32)
+_st_p2p = _sig("seedtable_partition_p2p", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _st_fin_ws = _sig("seedtable_finalize_workspace_bytes", _sz, _u64, _i32, _i32)
 _st_lk_ws = _sig("seedtable_lookup_workspace_bytes", _sz, _u64)
 _st_lk = _sig("seedtable_lookup", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _sz, _vp)
@@ -82,7 +84,8 @@ _st_fin = _sig("seedtable_finalize", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32
 EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_encode", "mz_workspace_bytes",
            "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_count",
            "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
-           "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup"]
+           "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup",
+           "seedtable_partition_p2p_workspace_bytes", "seedtable_partition_p2p"]
 
 
 def strerror(rc: int) -> str:
@@ -269,6 +272,25 @@ def seedtable_partition(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: in
     _check(_st_part(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, nranks, _ptr(send_fp), _ptr(send_pos),
                     _ptr(send_counts), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_partition")
     return send_fp, send_pos, send_counts
+
+
+def seedtable_partition_p2p(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, peer_fp: list[int],
+                            peer_pos: list[int], peer_base: list[int], *, m: int | None = None, d_m=None, ws=None,
+                            stream=None) -> int:
+    """Partition fused with the all-to-all: entries go straight into the owners' receive
+    buffers (device pointers, e.g. peer-mapped symmetric memory).  Returns the status code:
+    SLSUM_OK, or SLSUM_EUNSUPPORTED when the narrow precondition fails (use the NCCL path)."""
+    if m is None:
+        m = hash_.numel()
+    nranks = len(peer_fp)
+    if ws is None:
+        ws = _ws(_st_p2p_ws(max(1, m), nranks), hash_.device)
+    arr = ctypes.c_uint64 * nranks
+    rc = _st_p2p(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, nranks, arr(*peer_fp), arr(*peer_pos),
+                 arr(*peer_base), _ptr(ws), ws.numel(), _stream(stream))
+    if rc not in (SLSUM_OK, SLSUM_EUNSUPPORTED):
+        _check(rc, "seedtable_partition_p2p")
+    return rc
 
 
 def seedtable_finalize(recv_fp: torch.Tensor, recv_pos: torch.Tensor, m_recv: int, global_counts, bits: int,

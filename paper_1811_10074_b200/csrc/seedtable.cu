@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -425,28 +426,17 @@ __device__ __forceinline__ uint64_t make_item(const NIn<IN, T>& r, uint32_t j, i
 }
 
 
-// Peers of this lane's digit d < 256 among the 32 lanes (bitwise ballot multi-split; a
-// digit narrower than 8 bits has zero high bits in every lane, so its extra ballots are
-// no-ops).  Measured on B200 at ~1.5 items/clk/SM (tools/microbench_rank.cu), half the
-// cost of MATCH.ANY.
-__device__ __forceinline__ unsigned peers8(uint32_t d) {
-  unsigned peers = 0xffffffffu;
-#pragma unroll
-  for (int bb = 0; bb < 8; ++bb) {
-    const bool bit = (d & (1u << bb)) != 0u;
-    const unsigned mb = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? mb : ~mb;
-  }
-  return peers;
-}
-
 template <int IN, int OUT, int TPB, int IPT>
 __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uint64_t* __restrict__ p_in,
                                                        void* a_out, uint64_t* __restrict__ p_out, const uint64_t* d_m,
                                                        uint64_t m_cap, int k, int shift, int dbits,
                                                        const uint64_t* __restrict__ offsets,
                                                        const unsigned long long* __restrict__ dbase, uint64_t nchunks,
-                                                       uint64_t* ctl, int use_tma) {
+                                                       uint64_t* ctl, int use_tma,
+                                                       uint32_t* const* __restrict__ dfp = nullptr,
+                                                       uint64_t* const* __restrict__ dpos = nullptr) {
+  // dfp/dpos (OUT == kOutFpPos only): per-digit destination arrays, e.g. the peer-mapped receive
+  // buffers of the owner ranks (seedtable_partition_p2p); digit d's entries go to dfp[d][g]
   constexpr int T = TPB * IPT;
   constexpr int NW = TPB / 32;
   static_assert(kChunk % T == 0, "chunk must hold whole tiles");
@@ -636,6 +626,10 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
       if constexpr (OUT == kOutPk) {
         static_cast<uint64_t*>(a_out)[g] = v;
+      } else if (dfp) {
+        const uint32_t d = (uint32_t)(v >> dsh) & dmask;
+        dfp[d][g] = (uint32_t)(v >> 32);  // a plain store: over NVLink when the buffer is a peer's
+        dpos[d][g] = p0 + (uint32_t)v;
       } else {
         static_cast<uint32_t*>(a_out)[g] = (uint32_t)(v >> 32);
         p_out[g] = p0 + (uint32_t)v;
@@ -902,7 +896,7 @@ int launch_nsweep(const void* a_in, const uint64_t* p_in, void* a_out, uint64_t*
   const size_t sm = nsweep_smem<IN, TPB, IPT>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   kern<<<(unsigned)nch, TPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                       use_tma);
+                                       use_tma, nullptr, nullptr);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -1143,6 +1137,81 @@ MZS_API int seedtable_partition(const uint64_t* hash, const uint64_t* pos, uint6
   if (rc) return rc;
   u32_to_u64_kernel<<<1, 256, 0, st>>>(s.totals, send_counts, nranks);
   MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
+MZS_API size_t seedtable_partition_p2p_workspace_bytes(uint64_t m, int nranks) {
+  Sizer z;
+  size_sort_ws(z, m, 1, false);
+  z.take<uint64_t>(2 * (size_t)nranks);  // device copies of the destination pointer tables
+  return z.used;
+}
+
+// Partition fused with the all-to-all: the stable pass on the owner digit writes
+// every entry straight into its owner's receive buffer (peer memory over NVLink), at the offset
+// peer_base[o] this sender owns there.  Narrow path only (positions of the call within 2^32 of
+// pos[0]); returns SLSUM_EUNSUPPORTED otherwise, and the caller uses partition + NCCL.
+MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,
+                                    int bucket_bits, int nranks, const uint64_t* peer_fp, const uint64_t* peer_pos,
+                                    const uint64_t* peer_base, void* ws, size_t ws_bytes, void* stream) {
+  if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
+  if (!is_pow2(nranks) || nranks < 2 || nranks > 256 || log2i(nranks) > bucket_bits || !peer_fp || !peer_pos ||
+      !peer_base)
+    return SLSUM_EINVAL;
+  if (m == 0) return SLSUM_OK;
+  if (!hash || !pos) return SLSUM_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  TempWs tmp;
+  const size_t need = seedtable_partition_p2p_workspace_bytes(m, nranks);
+  if (!ws) {
+    MZS_CUDA(cudaMallocAsync(&tmp.p, need, st));
+    tmp.s = st;
+    ws = tmp.p;
+    ws_bytes = need;
+  }
+  if (ws_bytes < need) return SLSUM_ENOMEM;
+  Carve c(ws, ws_bytes);
+  SortWs s;
+  if (!carve_sort_ws(c, m, 1, false, s)) return SLSUM_ENOMEM;
+  uint64_t* dptr = c.take<uint64_t>(2 * (size_t)nranks);
+  if (!c.ok) return SLSUM_ENOMEM;
+  const int g = log2i(nranks);
+  const uint64_t nch = (m + kChunk - 1) / kChunk;
+  // the narrow precondition, decided here on the host (one small read)
+  uint64_t h[3] = {m, 0, 0};
+  if (d_m) MZS_CUDA(cudaMemcpyAsync(&h[0], d_m, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  MZS_CUDA(cudaStreamSynchronize(st));
+  const uint64_t mm = std::min(h[0], m);
+  if (mm == 0) return SLSUM_OK;
+  MZS_CUDA(cudaMemcpy(&h[1], pos, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  MZS_CUDA(cudaMemcpy(&h[2], pos + mm - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (h[2] < h[1] || h[2] - h[1] > 0xffffffffull) return SLSUM_EUNSUPPORTED;
+  ctl_kernel<<<1, 32, 0, st>>>(pos, d_m, m, s.ctl);
+  MZS_LAUNCHED();
+  const int nb = g;
+  const int sh = 32 - nb;
+  int rc = count_pass<0>(hash, d_m, m, k, sh, nb, nch, s, 1, st);
+  if (rc) return rc;
+  // destinations: digit o -> owner o's buffers, from this sender's base there (replacing the
+  // digit scan's bases; digits >= nranks carry no entries)
+  std::vector<uint64_t> hp(2 * (size_t)nranks), hb(256, 0);
+  for (int o = 0; o < nranks; ++o) {
+    hp[o] = peer_fp[o];
+    hp[nranks + o] = peer_pos[o];
+    hb[o] = peer_base[o];
+  }
+  MZS_CUDA(cudaMemcpyAsync(dptr, hp.data(), sizeof(uint64_t) * 2 * nranks, cudaMemcpyHostToDevice, st));
+  MZS_CUDA(cudaMemcpyAsync(s.dbase, hb.data(), sizeof(unsigned long long) * 256, cudaMemcpyHostToDevice, st));
+  const int tma_in = ((reinterpret_cast<uintptr_t>(hash) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0;
+  auto kern = nsweep_kernel<kInHashPos, kOutFpPos, 256, 8>;
+  const size_t smem = nsweep_smem<kInHashPos, 256, 8>();
+  MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)nch, 256, smem, st>>>(hash, pos, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                         tma_in, reinterpret_cast<uint32_t* const*>(dptr),
+                                         reinterpret_cast<uint64_t* const*>(dptr + nranks));
+  MZS_LAUNCHED();
+  // the host vectors above were read by the async copies; make them complete before returning
+  MZS_CUDA(cudaStreamSynchronize(st));
   return SLSUM_OK;
 }
 

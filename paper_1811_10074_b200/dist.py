@@ -68,6 +68,9 @@ class Phases:
     def finalize(self, recv_fp, recv_pos, m_recv, global_counts, bits, rank, nranks):
         raise NotImplementedError  # -> (offsets_local int64[nbl+1], pos int64[m_recv], fp int32[m_recv])
 
+    def partition_p2p(self, hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base):  # -> status code
+        raise NotImplementedError
+
 
 class CudaPhases(Phases):
     """The product: every phase is a libmzslsum call on the current stream."""
@@ -88,6 +91,10 @@ class CudaPhases(Phases):
         off, p, fp = self.L.seedtable_finalize(recv_fp.view(torch.uint32), recv_pos.view(torch.uint64), m_recv,
                                                global_counts.view(torch.uint32), bits, rank, nranks)
         return off.view(torch.int64), p[:m_recv].view(torch.int64), fp[:m_recv].view(torch.int32)
+
+    def partition_p2p(self, hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base):
+        return self.L.seedtable_partition_p2p(hash_.view(torch.uint64), pos.view(torch.uint64), k, bits,
+                                              peer_fp, peer_pos, peer_base, m=m)
 
 
 # ---------------------------------------------------------------- the exchange
@@ -120,3 +127,95 @@ def exchange_seedtable(hash_, pos, m: int, k: int, bits: int, phases: Phases, gr
     nbl = (1 << bits) // G
     base = int((counts.to(torch.int64) & 0xFFFFFFFF)[: rank * nbl].sum().item())
     return off, pl, fl, base
+
+
+# ---------------------------------------------------------------- the fused exchange (peer memory)
+def p2p_plan(owner_counts, span_ok):
+    """Host logic of the fused exchange, identical on every rank (it sees the same gathered
+    matrix).  owner_counts[s][o] = entries sender s holds for owner o; span_ok[s] = sender s's
+    positions span < 2^32 (the narrow-item precondition of seedtable_partition_p2p).
+    Returns (use_p2p, peer_base[s][o] = where sender s starts writing in owner o's buffer,
+    recv[o] = entries owner o receives, cap = the common symmetric-buffer capacity)."""
+    G = len(owner_counts)
+    recv = [sum(owner_counts[s][o] for s in range(G)) for o in range(G)]
+    base = [[sum(owner_counts[t][o] for t in range(s)) for o in range(G)] for s in range(G)]
+    cap = max(1, max(recv) if recv else 1)
+    return all(bool(x) for x in span_ok), base, recv, cap
+
+
+class SymmPeerMem:
+    """The product's peer memory: one torch symmetric-memory buffer per (group, device), cap u64
+    positions then cap u32 fingerprints, mapped into every peer over NVLink.  Grow-only with
+    1/8 headroom; every rank takes the same decision (cap is agreed).  get() returns
+    (c, local recv_pos int64[c], local recv_fp int32[c], fp pointers[G], pos pointers[G])."""
+
+    def __init__(self):
+        self._ent = {}
+
+    def get(self, cap: int, dev, group):
+        import torch.distributed._symmetric_memory as symm_mem
+        key = (id(group), dev.index)
+        ent = self._ent.get(key)
+        if ent is None or ent[0] < cap:
+            c = cap + cap // 8 + 1024
+            buf = symm_mem.empty(c + (c + 1) // 2, dtype=torch.uint64, device=dev)
+            hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+            G = dist.get_world_size(group)
+            ptrs = [hdl.get_buffer(o, (1,), torch.uint8, 0).data_ptr() for o in range(G)]
+            ent = (c, buf, hdl, ptrs)
+            self._ent[key] = ent
+        c, buf, _, ptrs = ent
+        return (c, buf[:c].view(torch.int64), buf[c:].view(torch.uint32)[:c].view(torch.int32),
+                [p + 8 * c for p in ptrs], list(ptrs))
+
+
+_PEER_MEM = SymmPeerMem()
+
+
+def exchange_seedtable_p2p(hash_, pos, m: int, k: int, bits: int, phases: Phases, group=None, peer_mem=None):
+    """C5 with the partition fused into the all-to-all: each sender's last radix pass writes
+    its (fingerprint, position) entries straight into the owners' symmetric buffers over
+    NVLink (include/mzslsum.h seedtable_partition_p2p), so no send buffer and no NCCL
+    all_to_all exist.  Collectives left: all_reduce of the bucket counts and one all_gather of
+    G x G owner counts (to place each sender's run), plus two barriers around the writes.
+    Same result as exchange_seedtable; falls back to it when a rank's positions span >= 2^32
+    (decided uniformly from the gathered flags).  `peer_mem` is injectable for the CPU tests."""
+    rank = dist.get_rank(group)
+    G = dist.get_world_size(group)
+    if G & (G - 1) or G < 2:
+        raise ValueError("fused exchange needs a power-of-two world size >= 2")
+    peer_mem = peer_mem or _PEER_MEM
+    dev = hash_.device
+    counts = phases.count(hash_, m, k, bits)
+    nbl = (1 << bits) // G
+    own = (counts.to(torch.int64) & 0xFFFFFFFF).view(G, nbl).sum(1)
+    span_ok = 1
+    if m > 0:
+        ends = torch.stack([pos[0], pos[m - 1]]).view(torch.int64).cpu().tolist()
+        span_ok = int(((ends[1] - ends[0]) & ((1 << 64) - 1)) < (1 << 32))
+    row = torch.cat([own, torch.tensor([span_ok], dtype=torch.int64, device=dev)])
+    rows = [torch.empty_like(row) for _ in range(G)]
+    dist.all_gather(rows, row, group=group)
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    mat = [r.cpu().tolist() for r in rows]
+    use, base, recv, cap = p2p_plan([r[:G] for r in mat], [r[G] for r in mat])
+    if not use:
+        return exchange_seedtable(hash_, pos, m, k, bits, phases, group)
+    try:
+        got = peer_mem.get(cap, dev, group)
+        ok = 1
+    except Exception:                              # no peer mapping on this box (no NVLink / IPC)
+        got, ok = None, 0
+    flag = torch.tensor([ok], dtype=torch.int64, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if not int(flag.item()):
+        return exchange_seedtable(hash_, pos, m, k, bits, phases, group)
+    c, recv_pos, recv_fp, fp_ptrs, pos_ptrs = got
+    dist.barrier(group=group)                      # every owner is done with its previous contents
+    rc = phases.partition_p2p(hash_, pos, m, k, bits, fp_ptrs, pos_ptrs, base[rank])
+    if rc != 0:
+        raise RuntimeError(f"seedtable_partition_p2p failed: {rc}")
+    dist.barrier(group=group)                      # every sender's writes have landed (it synced)
+    off, pl, fl = phases.finalize(recv_fp, recv_pos, recv[rank], counts, bits, rank, G)
+    b0 = int((counts.to(torch.int64) & 0xFFFFFFFF)[: rank * nbl].sum().item())
+    return off, pl, fl, b0

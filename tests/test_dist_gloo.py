@@ -58,7 +58,54 @@ class OraclePhases:
                 torch.from_numpy(fpo.view(np.int32).copy()))
 
 
-def _worker(rank, world, port, q):
+    def partition_p2p(self, hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base):
+        """Writes each owner's run at peer_base[o] of that owner's (file-backed) buffers,
+        in position order, as the kernel does over NVLink."""
+        fp, ps, counts = self.partition(hash_, pos, m, k, bits, len(peer_fp))
+        a = 0
+        for o, n in enumerate(counts):
+            f = np.memmap(peer_fp[o], dtype=np.int32, mode="r+")
+            p = np.memmap(peer_pos[o], dtype=np.int64, mode="r+")
+            f[peer_base[o]: peer_base[o] + n] = fp.numpy()[a: a + n]
+            p[peer_base[o]: peer_base[o] + n] = ps.numpy()[a: a + n]
+            f.flush()
+            p.flush()
+            a += n
+        return 0
+
+
+class FilePeerMem:
+    """Test-only stand-in for the symmetric buffers: one shared file pair per rank; the
+    'pointers' handed to partition_p2p are the peers' file paths."""
+
+    def __init__(self, root, rank, world):
+        self.root, self.rank, self.world = root, rank, world
+
+    def _paths(self, o):
+        return os.path.join(self.root, f"fp{o}"), os.path.join(self.root, f"pos{o}")
+
+    def get(self, cap, dev, group):
+        c = cap + 7
+        fpp, psp = self._paths(self.rank)
+        np.memmap(fpp, dtype=np.int32, mode="w+", shape=(c,)).flush()
+        np.memmap(psp, dtype=np.int64, mode="w+", shape=(c,)).flush()
+        dist.barrier(group=group)
+        self.local = (np.memmap(fpp, dtype=np.int32, mode="r"), np.memmap(psp, dtype=np.int64, mode="r"))
+        return (c, _LazyFile(psp, np.int64), _LazyFile(fpp, np.int32),
+                [self._paths(o)[0] for o in range(self.world)], [self._paths(o)[1] for o in range(self.world)])
+
+
+class _LazyFile:
+    """Reads the file when finalize slices it (after the second barrier)."""
+
+    def __init__(self, path, dt):
+        self.path, self.dt = path, dt
+
+    def __getitem__(self, sl):
+        return torch.from_numpy(np.array(np.memmap(self.path, dtype=self.dt, mode="r"))[sl])
+
+
+def _worker(rank, world, port, q, p2p_root=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -69,20 +116,26 @@ def _worker(rank, world, port, q):
         sub = seq[sh.base_lo: sh.base_hi]
         key, pos = O.mz(sub, K, W, pos_base=sh.base_lo, win_lo=sh.win_lo, win_hi=sh.win_hi)
         m = len(key)
-        off, pl, fl, base = D.exchange_seedtable(torch.from_numpy(key.view(np.int64).copy()),
-                                                 torch.from_numpy(pos.view(np.int64).copy()), m, K, BITS,
-                                                 OraclePhases())
+        args = (torch.from_numpy(key.view(np.int64).copy()), torch.from_numpy(pos.view(np.int64).copy()),
+                m, K, BITS, OraclePhases())
+        if p2p_root is None:
+            off, pl, fl, base = D.exchange_seedtable(*args)
+        else:
+            off, pl, fl, base = D.exchange_seedtable_p2p(*args, peer_mem=FilePeerMem(p2p_root, rank, world))
         q.put((rank, key, pos, off.numpy(), pl.numpy(), fl.numpy(), base))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_extraction_and_exchange(world):
+@pytest.mark.parametrize("world,p2p", [(2, False), (4, False), (2, True), (4, True)])
+def test_sharded_extraction_and_exchange(world, p2p, tmp_path):
+    """p2p=True runs exchange_seedtable_p2p (the fused partition-to-peers path) with
+    file-backed peer buffers in place of NVLink-mapped symmetric memory."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    root = str(tmp_path) if p2p else None
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, root)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
@@ -115,6 +168,16 @@ def test_plan_shards_covers_windows():
             if s.win_b > s.win_a:
                 assert s.base_lo == max(0, s.win_a - 1) and s.base_hi == s.win_b + k + w - 2
                 assert s.win_hi - s.win_lo == s.win_b - s.win_a
+
+
+def test_p2p_plan():
+    from paper_1811_10074_b200 import dist as D
+    oc = [[3, 0, 5], [1, 2, 0], [4, 4, 4]]          # [sender][owner]
+    use, base, recv, cap = D.p2p_plan(oc, [1, 1, 1])
+    assert use and recv == [8, 6, 9] and cap == 9
+    assert base == [[0, 0, 0], [3, 0, 5], [4, 2, 5]]
+    assert not D.p2p_plan(oc, [1, 0, 1])[0]
+    assert D.p2p_plan([[0, 0], [0, 0]], [1, 1])[3] == 1
 
 
 def test_plan_reads_balanced():

@@ -167,3 +167,54 @@ def test_multi_rank_phases_emulated(nranks):
         base += mr
     assert np.array_equal(np.concatenate(all_pos), wp)
     assert np.array_equal(np.concatenate(all_fp), wf)
+
+
+@pytest.mark.parametrize("nranks", [2, 4, 8])
+def test_partition_p2p_emulated(nranks):
+    """The partition fused with the all-to-all (seedtable_partition_p2p), with the ranks
+    emulated in one process on one GPU: every sender writes straight into all owners' receive
+    buffers (here plain device buffers; peer-mapped symmetric memory on a real box) at its base
+    offsets; each owner then finalizes.  The concatenated slices must equal the oracle table."""
+    k, bits = 19, 24
+    c3 = G.C3(n=3_000_000)
+    key, pos = O.mz(c3.ascii(), k, 10)
+    m = len(key)
+    cuts = [m * g // nranks for g in range(nranks + 1)]
+    nbl = (1 << bits) // nranks
+    shards, per_owner, gcounts = [], [], None
+    for g in range(nranks):
+        kt, pt = _dev(key[cuts[g]:cuts[g + 1]]), _dev(pos[cuts[g]:cuts[g + 1]])
+        c = P.seedtable_count(kt, k, bits).view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        gcounts = c if gcounts is None else gcounts + c
+        per_owner.append(c.view(nranks, nbl).sum(1).cpu().numpy())
+        shards.append((kt, pt))
+    cnt = np.stack(per_owner)                       # [sender, owner]
+    recv = cnt.sum(0)
+    bufs = [(torch.empty(max(1, int(recv[o])), dtype=torch.uint32, device="cuda"),
+             torch.empty(max(1, int(recv[o])), dtype=torch.uint64, device="cuda")) for o in range(nranks)]
+    for g, (kt, pt) in enumerate(shards):
+        base = [int(cnt[:g, o].sum()) for o in range(nranks)]
+        rc = P.seedtable_partition_p2p(kt, pt, k, bits, [b[0].data_ptr() for b in bufs],
+                                       [b[1].data_ptr() for b in bufs], base)
+        assert rc == P.SLSUM_OK
+    torch.cuda.synchronize()
+    gc32 = gcounts.to(torch.int32).view(torch.uint32)
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    all_pos, all_fp, b0 = [], [], 0
+    for r in range(nranks):
+        mr = int(recv[r])
+        off, po, fp = P.seedtable_finalize(bufs[r][0], bufs[r][1], mr, gc32, bits, r, nranks)
+        assert np.array_equal(off.cpu().numpy() + np.uint64(b0), wo[r * nbl: (r + 1) * nbl + 1])
+        all_pos.append(po[:mr].cpu().numpy())
+        all_fp.append(fp[:mr].cpu().numpy())
+        b0 += mr
+    assert np.array_equal(np.concatenate(all_pos), wp)
+    assert np.array_equal(np.concatenate(all_fp), wf)
+
+
+def test_partition_p2p_rejects_wide_spans():
+    kt = _dev(np.arange(100, dtype=np.uint64))
+    pt = _dev((np.arange(100, dtype=np.uint64) * np.uint64(10 ** 9)))    # spans > 2^32
+    b = torch.empty(100, dtype=torch.uint64, device="cuda")
+    rc = P.seedtable_partition_p2p(kt, pt, 19, 24, [b.data_ptr()] * 2, [b.data_ptr()] * 2, [0, 0])
+    assert rc == P.SLSUM_EUNSUPPORTED
