@@ -38,10 +38,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-MIN_U32, MAX_U32, ADD_U32, ADD_F32, AFFINE_U32X2, MIN_U64 = range(6)
+MIN_U32, MAX_U32, ADD_U32, ADD_F32, AFFINE_U32X2, MIN_U64, CONCAT_U32X2 = range(7)
 KEY_HASH, KEY_RAW, KEY_CANON, KEY_CANON_RAW = 0, 1, 2, 3
 _DTYPE = {MIN_U32: np.uint32, MAX_U32: np.uint32, ADD_U32: np.uint32, ADD_F32: np.float32,
-          AFFINE_U32X2: np.uint32, MIN_U64: np.uint64}
+          AFFINE_U32X2: np.uint32, MIN_U64: np.uint64, CONCAT_U32X2: np.uint32}
 
 _lib = None
 
@@ -105,7 +105,8 @@ def as_bytes(seq) -> np.ndarray:
 
 # ---------------------------------------------------------------- sliding sums
 def slsum(op: int, w: int, x: np.ndarray) -> np.ndarray:
-    """Eq. 2 by the naive O(wN) strict left fold.  AFFINE_U32X2 takes x of shape (n, 2)."""
+    """Eq. 2 by the naive O(wN) strict left fold.  AFFINE_U32X2 and CONCAT_U32X2 take x of
+    shape (n, 2)."""
     x = np.ascontiguousarray(x, dtype=_DTYPE[op])
     n = x.shape[0]
     shape = (max(0, n - w + 1),) + x.shape[1:]

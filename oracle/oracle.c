@@ -47,7 +47,7 @@
 
 /* operator ids -- same numeric values as the public ABI so tests can pass one id */
 enum { ORC_MIN_U32 = 0, ORC_MAX_U32 = 1, ORC_ADD_U32 = 2, ORC_ADD_F32 = 3,
-       ORC_AFFINE_U32X2 = 4, ORC_MIN_U64 = 5 };
+       ORC_AFFINE_U32X2 = 4, ORC_MIN_U64 = 5, ORC_CONCAT_U32X2 = 6 };
 
 int orc_num_threads(void) {
 #ifdef _OPENMP
@@ -81,10 +81,25 @@ static void op_affine(const uint32_t* l, const uint32_t* r, uint32_t* out) {
     out[1] = a * d + b;
 }
 
+/* string concatenation of base-s numerals ("k-mers of R as a sliding sum ...
+ * string concatenation operator"): an element (v, s) is a string with value v and weight
+ * s = sigma^length; (v1,s1) (+) (v2,s2) = (v1 s2 + v2, s1 s2) over Z/2^32.  For symbols
+ * (b, sigma) the w-fold is (sum_t b_t sigma^(w-1-t), sigma^w) mod 2^32. */
+static void op_concat(const uint32_t* l, const uint32_t* r, uint32_t* out) {
+    uint32_t v1 = l[0], s1 = l[1], v2 = r[0], s2 = r[1];
+    out[0] = v1 * s2 + v2;
+    out[1] = s1 * s2;
+}
+
+static void op_pair(int op, const uint32_t* l, const uint32_t* r, uint32_t* out) {
+    if (op == ORC_AFFINE_U32X2) op_affine(l, r, out);
+    else op_concat(l, r, out);
+}
+
 static size_t elem_size(int op) {
     switch (op) {
     case ORC_MIN_U32: case ORC_MAX_U32: case ORC_ADD_U32: case ORC_ADD_F32: return 4;
-    case ORC_AFFINE_U32X2: case ORC_MIN_U64: return 8;
+    case ORC_AFFINE_U32X2: case ORC_MIN_U64: case ORC_CONCAT_U32X2: return 8;
     default: return 0;
     }
 }
@@ -122,11 +137,11 @@ int orc_slsum(int op, uint32_t w, const void* x, void* y, uint64_t n) {
             ((uint64_t*)y)[i] = acc;
             break;
         }
-        case ORC_AFFINE_U32X2: {
+        case ORC_AFFINE_U32X2: case ORC_CONCAT_U32X2: {
             const uint32_t* xs = (const uint32_t*)x;
             uint32_t acc[2] = { xs[2 * i], xs[2 * i + 1] }, t[2];
             for (uint32_t j = 1; j < w; j++) {
-                op_affine(acc, xs + 2 * (i + j), t);
+                op_pair(op, acc, xs + 2 * (i + j), t);
                 acc[0] = t[0]; acc[1] = t[1];
             }
             ((uint32_t*)y)[2 * i] = acc[0];
@@ -165,12 +180,12 @@ int orc_prefix(int op, const void* x, void* y, uint64_t n) {
         for (uint64_t i = 1; i < n; i++) { acc = op_min_u64(acc, xs[i]); ys[i] = acc; }
         break;
     }
-    case ORC_AFFINE_U32X2: {
+    case ORC_AFFINE_U32X2: case ORC_CONCAT_U32X2: {
         const uint32_t* xs = (const uint32_t*)x; uint32_t* ys = (uint32_t*)y;
         uint32_t acc[2] = { xs[0], xs[1] }, t[2];
         ys[0] = acc[0]; ys[1] = acc[1];
         for (uint64_t i = 1; i < n; i++) {
-            op_affine(acc, xs + 2 * i, t); acc[0] = t[0]; acc[1] = t[1];
+            op_pair(op, acc, xs + 2 * i, t); acc[0] = t[0]; acc[1] = t[1];
             ys[2 * i] = acc[0]; ys[2 * i + 1] = acc[1];
         }
         break;

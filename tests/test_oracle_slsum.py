@@ -130,3 +130,37 @@ def test_prefix_matches_cumsum_and_accumulate():
     x = rng.integers(0, 2 ** 32, size=1000, dtype=np.uint64).astype(np.uint32)
     assert np.array_equal(O.prefix(O.ADD_U32, x), (np.cumsum(x.astype(np.uint64)) & np.uint64(0xFFFFFFFF)).astype(np.uint32))
     assert np.array_equal(O.prefix(O.MIN_U32, x), np.minimum.accumulate(x))
+
+
+# ---------------------------------------------------------------- concatenation
+@pytest.mark.parametrize("sigma,w", [(4, 15), (4, 16), (20, 7), (20, 9), (256, 4), (256, 6), (3, 1)])
+def test_concat_is_base_sigma_numeral(sigma, w):
+    """k-mers "as a sliding sum ... string concatenation" (P:L67): folding (b, sigma) over
+    w symbols gives the base-sigma numeral of the w-mer and sigma^w, mod 2^32.  Pinned to
+    Python big-integer arithmetic (exact, then reduced)."""
+    rng = np.random.default_rng(sigma * 100 + w)
+    n = 300
+    b = rng.integers(0, sigma, size=n, dtype=np.uint64).astype(np.uint32)
+    x = np.stack([b, np.full(n, sigma, np.uint32)], axis=1)
+    y = O.slsum(O.CONCAT_U32X2, w, x)
+    for i in range(n - w + 1):
+        v = sum(int(b[i + t]) * sigma ** (w - 1 - t) for t in range(w))
+        assert int(y[i, 0]) == v % 2 ** 32
+        assert int(y[i, 1]) == sigma ** w % 2 ** 32
+
+
+def test_concat_dna_equals_kmer_codes():
+    """For DNA (sigma = 4, k <= 16) the concatenation fold is the k-mer code of a2."""
+    seq = b"ACGTTGCAACGGTACCATGCAAGT" * 5
+    codes, valid = O.encode(seq)
+    assert valid.all()
+    x = np.stack([codes.astype(np.uint32), np.full(len(codes), 4, np.uint32)], axis=1)
+    for k in (3, 11, 16):
+        y = O.slsum(O.CONCAT_U32X2, k, x)
+        assert [int(v) for v in y[:, 0]] == [O.kmer(codes, i, k) for i in range(len(seq) - k + 1)]
+
+
+def test_concat_not_commutative_fixture():
+    x = np.array([[1, 10], [2, 10]], np.uint32)     # "1" then "2" in base 10
+    assert O.slsum(O.CONCAT_U32X2, 2, x).tolist() == [[12, 100]]
+    assert O.slsum(O.CONCAT_U32X2, 2, x[::-1].copy()).tolist() == [[21, 100]]
