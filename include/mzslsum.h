@@ -66,6 +66,12 @@ int slsum_version(void);
  *                       (a,b) (+) (c,d) = (a c, a d + b).  Associative and NOT
  *                       commutative: proves that a path preserves operand order.
  *   SLSUM_MIN_U64       uint64 min (e.g. (key << 32 | pos) argmin keys)
+ *   SLSUM_CONCAT_U32X2  pairs (v, s) of uint32: a string with base-sigma value v and weight
+ *                       s = sigma^length; (v1,s1) (+) (v2,s2) = (v1 s2 + v2, s1 s2) mod 2^32,
+ *                       string concatenation (L67: "k-mers of R as a sliding sum ... string
+ *                       concatenation").  With x_i = (symbol_i, sigma) and w = k, y_i is the
+ *                       k-mer code of any alphabet (exact while sigma^k <= 2^32) and sigma^k.
+ *                       Not commutative (GENERIC, SCALAR; COMMUTATIVE -> EUNSUPPORTED).
  * path:
  *   SLSUM_PATH_GENERIC      Algorithm 2's decomposition with blocks of length w:
  *                           y_i = S[i] (+) P[i+w-1] (S = suffix fold to the end of i's
@@ -95,7 +101,8 @@ enum {
   SLSUM_ADD_U32 = 2,
   SLSUM_ADD_F32 = 3,
   SLSUM_AFFINE_U32X2 = 4,
-  SLSUM_MIN_U64 = 5
+  SLSUM_MIN_U64 = 5,
+  SLSUM_CONCAT_U32X2 = 6
 };
 enum {
   SLSUM_PATH_GENERIC = 0,

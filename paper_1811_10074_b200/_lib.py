@@ -17,14 +17,15 @@ LIB_PATH = os.environ.get("MZS_LIB") or os.path.join(HERE, "libmzslsum.so")
 
 # ---------------------------------------------------------------- constants (mzslsum.h)
 SLSUM_OK, SLSUM_EINVAL, SLSUM_EUNSUPPORTED, SLSUM_ECAPACITY, SLSUM_ECUDA, SLSUM_ENOMEM = 0, -1, -2, -3, -4, -5
-SLSUM_MIN_U32, SLSUM_MAX_U32, SLSUM_ADD_U32, SLSUM_ADD_F32, SLSUM_AFFINE_U32X2, SLSUM_MIN_U64 = range(6)
+SLSUM_MIN_U32, SLSUM_MAX_U32, SLSUM_ADD_U32, SLSUM_ADD_F32, SLSUM_AFFINE_U32X2, SLSUM_MIN_U64, SLSUM_CONCAT_U32X2 = range(7)
 SLSUM_PATH_GENERIC, SLSUM_PATH_COMMUTATIVE, SLSUM_PATH_AUTO, SLSUM_PATH_RECURRENT, SLSUM_PATH_SCALAR = range(5)
 MZ_IN_ASCII, MZ_IN_PACKED2 = 0, 1
 MZ_KEY_HASH, MZ_KEY_RAW, MZ_KEY_CANON, MZ_KEY_CANON_RAW = 0, 1, 2, 3
 U64_MAX = 2 ** 64 - 1
 
 OP_DTYPE = {SLSUM_MIN_U32: torch.uint32, SLSUM_MAX_U32: torch.uint32, SLSUM_ADD_U32: torch.uint32,
-            SLSUM_ADD_F32: torch.float32, SLSUM_AFFINE_U32X2: torch.uint32, SLSUM_MIN_U64: torch.uint64}
+            SLSUM_ADD_F32: torch.float32, SLSUM_AFFINE_U32X2: torch.uint32, SLSUM_MIN_U64: torch.uint64,
+            SLSUM_CONCAT_U32X2: torch.uint32}
 
 
 class SlsumError(RuntimeError):
@@ -124,7 +125,8 @@ def _ws(nbytes: int, device) -> torch.Tensor:
 # ---------------------------------------------------------------- sliding sums (Eq. 2)
 def slsum_run(op: int, w: int, x: torch.Tensor, y: torch.Tensor | None = None, path: int = SLSUM_PATH_GENERIC,
               stream=None) -> torch.Tensor:
-    """y_i = x_i (+) ... (+) x_{i+w-1} on the device.  AFFINE_U32X2 takes x of shape (n, 2)."""
+    """y_i = x_i (+) ... (+) x_{i+w-1} on the device.  AFFINE_U32X2 and CONCAT_U32X2 take x of
+    shape (n, 2)."""
     n = x.shape[0]
     nout = max(0, n - w + 1)
     if y is None:

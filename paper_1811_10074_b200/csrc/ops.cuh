@@ -46,6 +46,14 @@ struct OpAffine {
   __device__ __forceinline__ static T id() { return make_uint2(1u, 0u); }
   __device__ __forceinline__ static T op(T l, T r) { return make_uint2(l.x * r.x, l.x * r.y + l.y); }
 };
+// string concatenation of base-sigma numerals (L67: k-mers as a sliding sum under
+// concatenation): (v1,s1) (+) (v2,s2) = (v1 s2 + v2, s1 s2) over Z/2^32; the empty string (0,1).
+struct OpConcat {
+  using T = uint2;  // x = value, y = weight sigma^length
+  static constexpr bool kCommutative = false, kIdempotent = false;
+  __device__ __forceinline__ static T id() { return make_uint2(0u, 1u); }
+  __device__ __forceinline__ static T op(T l, T r) { return make_uint2(l.x * r.y + r.x, l.y * r.y); }
+};
 
 // ---------------------------------------------------------------- shuffles
 __device__ __forceinline__ uint32_t shfl_up(uint32_t v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }

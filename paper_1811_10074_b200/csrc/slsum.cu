@@ -858,7 +858,7 @@ int launch_scalar(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t
 using namespace mzs;
 
 MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n, int path, void* stream) {
-  if (w == 0 || op < SLSUM_MIN_U32 || op > SLSUM_MIN_U64) return SLSUM_EINVAL;
+  if (w == 0 || op < SLSUM_MIN_U32 || op > SLSUM_CONCAT_U32X2) return SLSUM_EINVAL;
   if (path < SLSUM_PATH_GENERIC || path > SLSUM_PATH_SCALAR) return SLSUM_EINVAL;
   if (n < w) return SLSUM_OK;  // zero outputs (not an error)
   if (!x || !y) return SLSUM_EINVAL;
@@ -871,6 +871,7 @@ MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n,
       case SLSUM_ADD_U32: return launch_scalar<OpAddU32>(x, y, n, w, st);
       case SLSUM_ADD_F32: return launch_scalar<OpAddF32>(x, y, n, w, st);
       case SLSUM_AFFINE_U32X2: return launch_scalar<OpAffine>(x, y, n, w, st);
+      case SLSUM_CONCAT_U32X2: return launch_scalar<OpConcat>(x, y, n, w, st);
       case SLSUM_MIN_U64: return launch_scalar<OpMinU64>(x, y, n, w, st);
     }
     return SLSUM_EINVAL;
@@ -888,6 +889,7 @@ MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n,
       case SLSUM_ADD_U32: return launch_generic<OpAddU32>(x, y, n, w, st);
       case SLSUM_ADD_F32: return launch_generic<OpAddF32>(x, y, n, w, st);
       case SLSUM_AFFINE_U32X2: return launch_generic<OpAffine>(x, y, n, w, st);
+      case SLSUM_CONCAT_U32X2: return launch_generic<OpConcat>(x, y, n, w, st);
       case SLSUM_MIN_U64: return launch_generic<OpMinU64>(x, y, n, w, st);
     }
   } else {
@@ -896,7 +898,8 @@ MZS_API int slsum_run_ex(int op, uint32_t w, const void* x, void* y, uint64_t n,
       case SLSUM_MAX_U32: return launch_doubling<OpMaxU32>(x, y, n, w, st);
       case SLSUM_ADD_U32: return launch_doubling<OpAddU32>(x, y, n, w, st);
       case SLSUM_ADD_F32: return launch_doubling<OpAddF32>(x, y, n, w, st);
-      case SLSUM_AFFINE_U32X2: return SLSUM_EUNSUPPORTED;  // not commutative (abstract L8, D15)
+      case SLSUM_AFFINE_U32X2:
+      case SLSUM_CONCAT_U32X2: return SLSUM_EUNSUPPORTED;  // not commutative (abstract L8, D15)
       case SLSUM_MIN_U64: return launch_doubling<OpMinU64>(x, y, n, w, st);
     }
   }

@@ -13,7 +13,9 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_1811_10074_b200")
 
 OPS = [(P.SLSUM_MIN_U32, O.MIN_U32), (P.SLSUM_MAX_U32, O.MAX_U32), (P.SLSUM_ADD_U32, O.ADD_U32),
-       (P.SLSUM_ADD_F32, O.ADD_F32), (P.SLSUM_AFFINE_U32X2, O.AFFINE_U32X2), (P.SLSUM_MIN_U64, O.MIN_U64)]
+       (P.SLSUM_ADD_F32, O.ADD_F32), (P.SLSUM_AFFINE_U32X2, O.AFFINE_U32X2), (P.SLSUM_MIN_U64, O.MIN_U64),
+       (P.SLSUM_CONCAT_U32X2, O.CONCAT_U32X2)]
+PAIR_OPS = (P.SLSUM_AFFINE_U32X2, P.SLSUM_CONCAT_U32X2)    # (n, 2) uint32, not commutative
 WS = [1, 2, 3, 4, 5, 7, 10, 16, 17, 31, 32, 33, 64, 100, 255, 256, 1000, 1024]
 
 
@@ -24,6 +26,12 @@ def _input(op, n, rng):
         return rng.integers(0, 2 ** 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
     if op == P.SLSUM_MIN_U64:
         return rng.integers(0, 2 ** 63, size=n, dtype=np.uint64)
+    if op == P.SLSUM_CONCAT_U32X2:     # symbols of a sigma-letter alphabet (L67), else any pairs
+        sigma = int(rng.choice([4, 20, 256, 0]))
+        if sigma == 0:
+            return rng.integers(0, 2 ** 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+        b = rng.integers(0, sigma, size=n, dtype=np.uint64).astype(np.uint32)
+        return np.stack([b, np.full(n, sigma, np.uint32)], axis=1)
     hi = 2 ** 32 if rng.random() < 0.7 else 5  # small alphabets force ties
     return rng.integers(0, hi, size=n, dtype=np.uint64).astype(np.uint32)
 
@@ -55,7 +63,7 @@ def test_generic_vs_oracle(op, w):
         _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_GENERIC))
 
 
-@pytest.mark.parametrize("op", [o for o, _ in OPS if o != P.SLSUM_AFFINE_U32X2])
+@pytest.mark.parametrize("op", [o for o, _ in OPS if o not in PAIR_OPS])
 @pytest.mark.parametrize("w", WS)
 def test_commutative_vs_oracle(op, w):
     rng = np.random.default_rng(op * 777 + w)
@@ -108,7 +116,7 @@ def test_scalar_rejects_w_over_1024():
 
 @pytest.mark.parametrize("op", [o for o, _ in OPS if o != P.SLSUM_ADD_U32])
 def test_recurrent_rejects_non_invertible(op):
-    x = torch.zeros((100, 2) if op == P.SLSUM_AFFINE_U32X2 else (100,),
+    x = torch.zeros((100, 2) if op in PAIR_OPS else (100,),
                     dtype={P.SLSUM_ADD_F32: torch.float32, P.SLSUM_MIN_U64: torch.uint64}.get(op, torch.uint32),
                     device="cuda")
     with pytest.raises(P.SlsumError) as e:
@@ -132,11 +140,29 @@ def test_unaligned_and_ragged_views(w, path):
             assert np.array_equal(y.cpu().numpy(), O.slsum(dict(OPS)[op], w, x)), (op, n)
 
 
-def test_affine_rejected_by_commutative_path():
+@pytest.mark.parametrize("op", PAIR_OPS)
+def test_pair_ops_rejected_by_commutative_path(op):
     x = torch.zeros((100, 2), dtype=torch.uint32, device="cuda")
     with pytest.raises(P.SlsumError) as e:
-        P.slsum_run(P.SLSUM_AFFINE_U32X2, 4, x, path=P.SLSUM_PATH_COMMUTATIVE)
+        P.slsum_run(op, 4, x, path=P.SLSUM_PATH_COMMUTATIVE)
     assert e.value.rc == P.SLSUM_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("path", [P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_SCALAR])
+def test_concat_kmer_codes_any_alphabet(path):
+    """k-mers as a sliding sum under concatenation (L67) for alphabets that are not 2-bit
+    packable: a 20-letter (protein) alphabet with k = 7 (20^7 < 2^32, exact codes) and DNA
+    with k = 16 (= the 2-bit k-mer codes); checked against Python big-integer numerals."""
+    rng = np.random.default_rng(67)
+    for sigma, k in ((20, 7), (4, 16), (256, 4)):
+        n = 50_001
+        b = rng.integers(0, sigma, size=n, dtype=np.uint64).astype(np.uint32)
+        x = np.stack([b, np.full(n, sigma, np.uint32)], axis=1)
+        y = _run(P.SLSUM_CONCAT_U32X2, k, x, path)
+        assert np.all(y[:, 1] == np.uint32(sigma ** k % 2 ** 32))
+        pw = np.array([sigma ** (k - 1 - t) for t in range(k)], dtype=np.uint64)
+        want = (np.lib.stride_tricks.sliding_window_view(b.astype(np.uint64), k) * pw).sum(axis=1)
+        assert np.array_equal(y[:, 0].astype(np.uint64), want)       # exact: sigma^k <= 2^32
 
 
 def test_degenerate():
