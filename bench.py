@@ -86,6 +86,17 @@ def load_peaks():
     return 6650.0, "fallback", 1965.0
 
 
+def load_int_peak():
+    """The INT32 issue roof measured by tools/microbench_int.cu (profiles/r01/int_peak.json):
+    a 1:1 ALU/FMA-pipe mix, reported beside the derived peak (which stays the denominator)."""
+    p = os.path.join(ROOT, "profiles", "r01", "int_peak.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return {"tops": d.get("mixed_imm_tops"), "alu_pipe_only_tops": d.get("lop3_tops"),
+            "source": "profiles/r01/int_peak.json (tools/microbench_int.cu)"}
+
+
 # ------------------------------------------------------------------ clocks sampler
 class Clocks:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -681,6 +692,7 @@ def main():
             "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01/traffic_c3.json); algorithmic "
                             f"{per_phase_bytes['extract']:.3e} B",
             "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
+            "peak_measured": load_int_peak(),
             "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"]}
     tab_ach = per_phase_bytes["table"] / (phase_ms["table"] * 1e-3) / 1e9
     roof_table = {"bound": "hbm", "kernel": "seed table (3 packed-item LSD radix passes + pointer table)",
