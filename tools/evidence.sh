@@ -17,18 +17,23 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # full sections of the top kernels of the C3 step (after 3 warm-up steps) and of slsum (C2)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mz_fast|^nsweep|encode_kernel|upsweep" \
   -s 33 -c 11 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/full_c3.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 19 -c 1 \
-  -o $O/full_c2_generic_w16 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2a.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 11 -c 1 \
-  -o $O/full_c2_doubling_w4 python bench.py --config c2 --steps 5 --warmup 3 --no-cpu-baseline > $O/full_c2b.log 2>&1
+# one named C2 configuration per capture (tools/slsum_one.py launches exactly 4 slsum kernels;
+# the 4th, warm one is captured)
+for cfg in "min 16 generic" "min 1024 generic" "min 4 commutative" "min 1024 commutative" "add 64 recurrent"; do
+  set -- $cfg
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 3 -c 1 \
+    -o $O/full_c2_$3_$1_w$2 python tools/slsum_one.py --op $1 --w $2 --path $3 --reps 4 > $O/full_c2_$3_$1_w$2.log 2>&1
+done
 timeout 600 python bench.py --config lookup --steps 5 > $O/bench_lookup.json 2> $O/bench_lookup.err
 # summaries are made here (gpurun copies back at most 64 MiB): launch list, --set full table,
 # per-kernel DRAM traffic; the large reports are then dropped
 python tools/ncu_summary.py launches $O/launches_c3.csv --last-step encode_kernel > $O/summary_launches.md
-for r in full_c3 full_c2_generic_w16 full_c2_doubling_w4; do
-  python tools/ncu_summary.py report $O/$r.ncu-rep --bases 3.1e9 > $O/summary_$r.md 2>&1
+python tools/ncu_summary.py report $O/full_c3.ncu-rep --bases 3.1e9 > $O/summary_full_c3.md 2>&1
+for r in $O/full_c2_*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  python tools/ncu_summary.py report $r --bases 268435456 > $O/summary_$b.md 2>&1
 done
 python tools/ncu_summary.py traffic $O/full_c3.ncu-rep > $O/traffic_c3.json
 python tools/src_hot.py $O/full_c3.ncu-rep mz_fast --per 3.1e9 --top 40 > $O/srchot_mz.txt 2>&1
-rm -f $O/full_c3.ncu-rep
+rm -f $O/*.ncu-rep
 echo done
