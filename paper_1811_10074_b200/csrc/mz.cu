@@ -252,7 +252,16 @@ __device__ __forceinline__ PackedKey kmin(PackedKey a, PackedKey b) { return a.v
 struct DKey {
   unsigned long long v;
   __device__ __forceinline__ static DKey make(uint64_t h, uint32_t slot) {
-    return DKey{0x4330000000000000ull | (h << kSlotBits) | slot};
+    // = 0x43300000'00000000 | h << 14 | slot, as two multiply-adds on the FMA pipe (the bit
+    // fields do not overlap, so + is |): IMAD.WIDE.U32 of the low word with {slot, exponent}
+    // as addend, then IMAD of the high word into the upper half.
+    static_assert(kSlotBits == 14, "multiplier below assumes 14 slot bits");
+    unsigned long long lo;
+    uint32_t hi;
+    const unsigned long long c = (0x43300000ull << 32) | slot;
+    asm("mad.wide.u32 %0, %1, 16384, %2;" : "=l"(lo) : "r"((uint32_t)h), "l"(c));
+    asm("mad.lo.u32 %0, %1, 16384, %2;" : "=r"(hi) : "r"((uint32_t)(h >> 32)), "r"((uint32_t)(lo >> 32)));
+    return DKey{((unsigned long long)hi << 32) | (uint32_t)lo};
   }
   __device__ __forceinline__ uint32_t slot() const { return (uint32_t)(v & kSlotMask); }
   __device__ __forceinline__ uint64_t hash() const { return (v & 0x000FFFFFFFFFFFFFull) >> kSlotBits; }
