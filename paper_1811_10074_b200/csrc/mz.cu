@@ -166,9 +166,22 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
     constexpr bool RAW = KM & 1, CANON = KM & 2;
     uint64_t code = X >> (64 - kk);
     uint64_t rc = CANON ? revcomp64(code, k) : 0;
+    // DIRECT (compile-time k, hashed forward keys): every code is cut straight out of the
+    // aligned 128-bit stream X:Y with two constant funnel shifts instead of rolling 2 bits per
+    // base.  The high word keeps the stream bits above the code (garbage above bit 2k), which
+    // the hash's first step, (x (2^21-1) - 1) mod 2^2k, discards.
+    constexpr bool DIRECT = KK > 0 && KM == 0 && 2 * (Q - 1) + 2 * KK <= 128;
+    const uint32_t sw[5] = {0u, (uint32_t)(X >> 32), (uint32_t)X, (uint32_t)(Y >> 32), (uint32_t)Y};
+    // the 32 stream bits starting at stream bit b (b >= -32; bits before the stream read as 0)
+    auto cut = [&](int b) -> uint32_t {
+      const int j = (b + 32) >> 5, r = (b + 32) & 31;
+      return r ? __funnelshift_l(sw[j + 1], sw[j], r) : sw[j];
+    };
 #pragma unroll
     for (int s = 0; s < Q; ++s) {
-      if (s > 0) {
+      if (DIRECT) {
+        code = ((uint64_t)cut(2 * s + 2 * KK - 64) << 32) | cut(2 * s + 2 * KK - 32);
+      } else if (s > 0) {
         if (CANON) rc = (rc >> 2) | ((uint64_t)(3u - (uint32_t)(Z >> 62)) << (kk - 2));
         code = ((code << 2) | (Z >> 62)) & km;
         Z <<= 2;
