@@ -206,9 +206,19 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
     constexpr bool RAW = KM & 1, CANON = KM & 2;
     uint32_t code = (uint32_t)(X >> (64 - kk));
     uint32_t rc = CANON ? revcomp32(code, k) : 0u;
+    // DIRECT as in the 64-bit branch: one constant funnel shift per code (garbage above bit
+    // 2k is discarded by the hash's first step)
+    constexpr bool DIRECT = KK > 0 && KM == 0 && 2 * (Q - 1) + 2 * KK <= 128;
+    const uint32_t sw[5] = {0u, (uint32_t)(X >> 32), (uint32_t)X, (uint32_t)(Y >> 32), (uint32_t)Y};
+    auto cut = [&](int b) -> uint32_t {
+      const int j = (b + 32) >> 5, r = (b + 32) & 31;
+      return r ? __funnelshift_l(sw[j + 1], sw[j], r) : sw[j];
+    };
 #pragma unroll
     for (int s = 0; s < Q; ++s) {
-      if (s > 0) {
+      if (DIRECT) {
+        code = cut(2 * s + 2 * KK - 32);
+      } else if (s > 0) {
         if (CANON) rc = (rc >> 2) | ((3u - (uint32_t)(Z >> 62)) << (kk - 2));
         code = ((code << 2) | (uint32_t)(Z >> 62)) & km;
         Z <<= 2;
@@ -228,7 +238,10 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
       const uint32_t h = RAW ? c : hash_b32(c, km);
       if constexpr (std::is_same<Key, DKey>::value) {
         // h * 2^14 + slot as one 32x32->64 multiply-add (FMA pipe), then the exponent bits
-        keys[s0 + s] = Key{0x4330000000000000ull | ((uint64_t)h * (1ull << kSlotBits) + (s0 + s))};
+        unsigned long long v;
+        const unsigned long long c = (0x43300000ull << 32) | (s0 + s);
+        asm("mad.wide.u32 %0, %1, 16384, %2;" : "=l"(v) : "r"(h), "l"(c));
+        keys[s0 + s] = Key{v};
       } else {
         keys[s0 + s] = Key::make(h, s0 + s);
       }
