@@ -83,7 +83,11 @@ struct MzArgs {
   uint32_t* tile_counter;
   uint64_t ntiles;
   uint32_t tw;               // windows per tile
+  const uint64_t* ridx;      // coarse read index (kRidxShift), or nullptr
 };
+// ridx[b] = first read r in [0, nreads+1] with read_off[r] >= b * 2^kRidxShift: brackets every
+// read-start search to the reads of one 8 kbp block (a few loads instead of ~20 dependent ones)
+constexpr int kRidxShift = 13;
 
 __device__ __forceinline__ uint64_t ldw(const MzArgs& a, int64_t i) {
   return (i >= 0 && (uint64_t)i < a.nwords) ? __ldg(a.words + i) : 0ull;
@@ -99,9 +103,20 @@ __device__ __forceinline__ uint64_t inv_window64(const MzArgs& a, int64_t lo) {
   const uint64_t c = ldi(a, wi + 2);
   return sh ? (ab >> sh) | (c << (64 - sh)) : ab;
 }
-// first index r in [0, nreads] with read_off[r] > x  (read_off[nreads] = n)
+// first index r in [0, nreads+1] with read_off[r] > x  (read_off[nreads] = n)
 __device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
   uint64_t lo = 0, hi = a.nreads + 1;
+  if (a.ridx) {
+    if (x < 0) {
+      hi = __ldg(a.ridx);                 // reads starting at 0 .. : none <= x
+    } else if ((uint64_t)x >= a.n) {
+      lo = a.nreads + 1;                  // read_off[nreads] = n <= x
+    } else {
+      const uint64_t b = (uint64_t)x >> kRidxShift;
+      lo = __ldg(a.ridx + b);             // read_off[r] < b 2^S <= x for r < lo
+      hi = __ldg(a.ridx + b + 1);         // read_off[hi] >= (b+1) 2^S > x
+    }
+  }
   while (lo < hi) {
     uint64_t mid = (lo + hi) >> 1;
     if ((int64_t)__ldg(a.read_off + mid) > x) hi = mid; else lo = mid + 1;
@@ -110,6 +125,16 @@ __device__ __forceinline__ uint64_t upper_read(const MzArgs& a, int64_t x) {
 }
 
 // ------------------------------------------------------------------ phase 1
+// OR the bits of v into the shared bitmask m starting at bit s0
+__device__ __forceinline__ void or_bits(uint32_t* m, uint32_t s0, uint64_t v) {
+  const uint32_t w0 = s0 >> 5, sh = s0 & 31;
+  const uint32_t lo = (uint32_t)(v << sh), mid = (uint32_t)(v >> (32 - sh));
+  const uint32_t hi = sh ? (uint32_t)(v >> (64 - sh)) : 0u;
+  if (lo) atomicOr(&m[w0], lo);
+  if (mid) atomicOr(&m[w0 + 1], mid);
+  if (hi) atomicOr(&m[w0 + 2], hi);
+}
+
 // Keys of k-mers q0 .. q0+Q-1 into slots s0 .. s0+Q-1.  If CHECK, bit `slot` of the shared
 // bitmask wvb (zeroed by the caller) is set iff the window whose LAST k-mer is that slot's
 // k-mer is valid (run of valid same-read bases ending at the k-mer's last base >= k+w-1).
@@ -136,7 +161,32 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   int64_t next_rs = INT64_MAX;
   uint64_t ri = 0;
   const int span = k + a.w - 1;
-  if (CHECK) {
+  // BULK validity (the strip's windows and their bases fit one 64-bit mask): window s (last
+  // k-mer q0+s) covers bases [L+s, L+s+span), L = q0-w+1.  It is invalid iff an invalid base
+  // lies in that range -- the OR of the invalid bits over span positions, by doubling and one
+  // overlapping OR (the idempotent-op trick of the sliding sums themselves) -- or a read
+  // starts in (L+s, L+s+span).  Same result as the run counter below, without a walk.
+  const bool bulk = CHECK && Q + span - 1 <= 64;
+  if (bulk) {
+    const int64_t L = q0 - (a.w - 1);
+    uint64_t T = inv_window64(a, L);  // bit j <-> base L+j invalid
+    int p = 1;
+    while (2 * p <= span) {
+      T |= T >> p;
+      p *= 2;
+    }
+    uint64_t bad = T | (T >> (span - p));
+    if (a.read_off) {
+      const int64_t last = L + Q + span - 2;  // last base of the strip's last window
+      for (uint64_t r_i = upper_read(a, L); r_i <= a.nreads; ++r_i) {
+        const int64_t r = (int64_t)__ldg(a.read_off + r_i);  // > L
+        if (r > last) break;
+        const int64_t hi = min(r - L - 1, (int64_t)63), lo = max(r - L - span + 1, (int64_t)0);
+        if (hi >= lo) bad |= ((2ull << (hi - lo)) - 1ull) << lo;
+      }
+    }
+    vbits = ~bad & ((1ull << Q) - 1ull);
+  } else if (CHECK) {
     // run length at base x0 = q0 + k - 2 (capped at span), then walk base by base
     const int64_t x0 = q0 + k - 2;
     // last invalid base in [x0-span+1, x0], scanning back 64 bases at a time (span may exceed 64)
@@ -186,7 +236,7 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
         code = ((code << 2) | (Z >> 62)) & km;
         Z <<= 2;
       }
-      if (CHECK) {
+      if (CHECK && !bulk) {
         const int64_t x = q0 + s + k - 1;
         const uint32_t inv = (uint32_t)(iv >> s) & 1u;
         if (x == next_rs) {
@@ -223,7 +273,7 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
         code = ((code << 2) | (uint32_t)(Z >> 62)) & km;
         Z <<= 2;
       }
-      if (CHECK) {
+      if (CHECK && !bulk) {
         const int64_t x = q0 + s + k - 1;
         const uint32_t inv = (uint32_t)(iv >> s) & 1u;
         if (x == next_rs) {
@@ -247,17 +297,16 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
       }
     }
   }
-  if (CHECK && vbits) {
-    const uint32_t w0 = s0 >> 5, sh = s0 & 31;
-    const uint32_t lo = (uint32_t)(vbits << sh), mid = (uint32_t)(vbits >> (32 - sh));
-    const uint32_t hi = sh ? (uint32_t)(vbits >> (64 - sh)) : 0u;
-    if (lo) atomicOr(&wvb[w0], lo);
-    if (mid) atomicOr(&wvb[w0 + 1], mid);
-    if (hi) atomicOr(&wvb[w0 + 2], hi);
-  }
+  if (CHECK && vbits) or_bits(wvb, s0, vbits);
 }
 
 __device__ __forceinline__ bool wv_bit(const uint32_t* wvb, int s) { return (wvb[s >> 5] >> (s & 31)) & 1u; }
+// bits b .. b+63 of a shared bitmask (the words up to (b >> 5) + 2 must exist)
+__device__ __forceinline__ uint64_t bits64(const uint32_t* m, int b) {
+  const int w0 = b >> 5, sh = b & 31;
+  const uint64_t v = ((uint64_t)m[w0 + 1] << 32) | m[w0];
+  return sh ? (v >> sh) | ((uint64_t)m[w0 + 2] << (64 - sh)) : v;
+}
 
 // Packed key: (hash << 14) | slot -- lexicographic (hash, position) order in one u64.
 struct PackedKey {
@@ -361,6 +410,48 @@ __device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int
   if (a.read_off && threadIdx.x == 0) {
     const uint64_t r = upper_read(a, b_lo);  // first read start > b_lo
     if (r <= a.nreads && (int64_t)__ldg(a.read_off + r) < b_hi) dirty = 1;
+  }
+  return !__syncthreads_or(dirty);
+}
+
+// Sub-tile dirty map: bit u of dwm <-> packed word W0 + u (W0 = b_lo >> 5) holds an invalid
+// base or a read start inside [b_lo, b_hi) (b_lo itself excluded for read starts, as a read
+// may start at the first base).  Returns true iff the whole sub-tile is clean; warps of a
+// dirty sub-tile test their own range of words (warp_dirty) and take the validity-free
+// phase 1 when it is clean -- with ~1 read start per 10 kbp (C4) most warps are.
+template <int TPB, int DW>
+__device__ __forceinline__ bool subtile_dirty_map(const MzArgs& a, int64_t b_lo, int64_t b_hi, uint32_t* dwm,
+                                                  const uint32_t* pre) {
+  const int64_t W0 = b_lo >> 5;
+  int dirty = 0;
+  if (a.invalid) {
+    const int64_t w0 = max((int64_t)0, W0), w1 = min((int64_t)a.nwords - 1, (b_hi - 1) >> 5);
+    for (int64_t wi = w0 + threadIdx.x; wi <= w1; wi += TPB) {
+      uint32_t m = (pre && wi == w0 + (int64_t)threadIdx.x) ? *pre : __ldg(a.invalid + wi);
+      const int64_t base = wi << 5;
+      if (base < b_lo) m &= 0xffffffffu << (uint32_t)(b_lo - base);
+      if (base + 32 > b_hi) m &= (b_hi - base >= 32) ? 0xffffffffu : ((1u << (uint32_t)(b_hi - base)) - 1u);
+      if (m) {
+        dirty = 1;
+        const uint32_t u = (uint32_t)(wi - W0);
+        atomicOr(&dwm[u >> 5], 1u << (u & 31));
+      }
+    }
+  }
+  if (a.read_off && threadIdx.x < 32) {
+    // read starts r with b_lo < r < b_hi: warp 0 walks them 32 at a time
+    uint64_t r0 = 0;
+    if (threadIdx.x == 0) r0 = upper_read(a, b_lo);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+    for (uint64_t r = r0 + threadIdx.x;; r += 32) {
+      const bool in = r <= a.nreads && (int64_t)__ldg(a.read_off + r) < b_hi;
+      if (in) {
+        dirty = 1;
+        const uint32_t u = (uint32_t)(((int64_t)__ldg(a.read_off + r) >> 5) - W0);
+        atomicOr(&dwm[u >> 5], 1u << (u & 31));
+      }
+      if (!__all_sync(0xffffffffu, in)) break;
+    }
   }
   return !__syncthreads_or(dirty);
 }
@@ -612,6 +703,10 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   Key* keys = reinterpret_cast<Key*>(smem_raw);
   __shared__ uint32_t emit[2][NSWT + 2];
   __shared__ uint32_t wvb[G::NSW + 3];
+  // dirty-word maps of the sub-tile's packed words (double-buffered: the next one is zeroed
+  // while the current one is in use); DW words cover NS + k + 64 bases
+  constexpr int DW = (G::NS + 64 + 64) / 1024 + 3;
+  __shared__ uint32_t dwm[2][DW];
   __shared__ uint64_t warp_sums[G::TPB / 32];
   __shared__ uint64_t bcast;
   __shared__ uint32_t s_tile;
@@ -622,6 +717,7 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   while (true) {
     if (t == 0) s_tile = atomicAdd(a.tile_counter, 1u);
     for (int u = t; u < NSWT + 2; u += G::TPB) emit[cur][u] = 0;
+    if (t < 2 * DW) dwm[t / DW][t % DW] = 0;
     __syncthreads();
     const uint64_t tile = s_tile;
     if (tile >= a.ntiles) break;
@@ -645,18 +741,32 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       const int64_t b_lo = tile_lo - 1, b_hi = tile_lo - 1 + G::NS + a.k;  // bases touched
       for (int u = t; u < G::NSW + 3; u += G::TPB) wvb[u] = 0;
       const uint32_t inv0 = pinv;
-      const bool clean = tile_is_clean<G::TPB>(a, b_lo, b_hi, &inv0);  // (also the barrier for wvb)
+      uint32_t* dm = dwm[sub & 1];
+      const bool clean = subtile_dirty_map<G::TPB, DW>(a, b_lo, b_hi, dm, &inv0);  // (also the barrier for wvb)
+      if (t < DW) dwm[(sub + 1) & 1][t] = 0;  // next sub-tile's map (unused until then)
       const int64_t q0 = tile_lo - 1 + (int64_t)t * G::Q;
       const uint32_t s0 = (uint32_t)(t * G::Q);
+      // a warp whose windows touch no dirty word skips the validity walk: the windows with
+      // their last k-mer in its slots cover bases [wq + 1 - W, wq + 32 Q + k - 2], wq = its first k-mer
+      bool wclean = clean;
+      if (!clean) {
+        const int64_t wq = tile_lo - 1 + (int64_t)(t & ~31) * G::Q;
+        const int64_t lo = max(b_lo, wq + 1 - W), hi = min(b_hi - 1, wq + 32 * G::Q + a.k - 2);
+        const int u0 = (int)((lo >> 5) - (b_lo >> 5)), u1 = (int)((hi >> 5) - (b_lo >> 5));
+        const int nb = u1 - u0 + 1;  // <= 64 (32 Q + k + W bases)
+        const uint64_t m = bits64(dm, u0) & (nb >= 64 ? ~0ull : ((1ull << nb) - 1));
+        wclean = m == 0;
+      }
       const uint64_t w3[3] = {pw[0], pw[1], pw[2]};
       constexpr int KMC = CN ? 2 : 0;  // canonical keys: a separate kernel instantiation
       if (!a.raw) {
-        if (clean) phase1_keys<Key, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
+        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
         else phase1_keys<Key, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb, w3);
       } else {
-        if (clean) phase1_keys<Key, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
+        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
         else phase1_keys<Key, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
       }
+      if (!clean && wclean) or_bits(wvb, s0, (1ull << G::Q) - 1);  // every window ending here is valid
       if (sub + 1 < G::SUBS) prefetch(tile_lo + G::TW);
       __syncthreads();
       // window ranges relative to the sub-tile
@@ -668,7 +778,11 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       const int elo = (int)wl, ehi = (int)max(wh, wl);
       // vlo may be -1: the window before the sub-tile exists and feeds the change rule
       const int jb = t * G::R;
-      const bool full = clean && vlo <= jb - 1 && jb + G::R <= vhi && elo <= jb && jb + G::R <= ehi;
+      // FULL: windows jb-1 .. jb+R-1 all valid (bits jb-1+W .. jb+R-1+W of wvb when the
+      // sub-tile is dirty) and inside the emission range
+      const bool inr = vlo <= jb - 1 && jb + G::R <= vhi && elo <= jb && jb + G::R <= ehi;
+      const uint64_t vm = (1ull << (G::R + 1)) - 1;
+      const bool full = inr && (clean || (bits64(wvb, jb - 1 + W) & vm) == vm);
       uint32_t* em = emit[cur] + sub * G::NSW;
       if (full) fast_phase2<W, false, true>(keys, wvb, vlo, vhi, elo, ehi, em);
       else if (clean) fast_phase2<W, false, false>(keys, wvb, vlo, vhi, elo, ehi, em);
@@ -797,6 +911,20 @@ __global__ void __launch_bounds__(kGenTPB) mz_generic_kernel(MzArgs a) {
 }
 
 // ------------------------------------------------------------------ host side
+__global__ void __launch_bounds__(256) ridx_kernel(const uint64_t* __restrict__ read_off, uint64_t nreads,
+                                                   uint64_t* __restrict__ ridx, uint64_t nb) {
+  const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t x = b << kRidxShift;
+  uint64_t lo = 0, hi = nreads + 1;   // first r with read_off[r] >= x
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (__ldg(read_off + mid) >= x) hi = mid; else lo = mid + 1;
+  }
+  ridx[b] = lo;
+}
+uint64_t ridx_entries(uint64_t n) { return (n >> kRidxShift) + 2; }
+
 int launch_mz(MzArgs a, int path, cudaStream_t st) {
   const int k = a.k, w = a.w;
   const bool h64 = 2 * k > 32;
@@ -871,6 +999,7 @@ MZS_API size_t mz_workspace_bytes(uint64_t n, int k, int w, int kind) {
   Sizer z;
   z.take<uint32_t>(1);                  // tile counter
   z.take<uint64_t>(max_tiles(n));       // look-back status
+  z.take<uint64_t>(ridx_entries(n));    // coarse read index (segmented input)
   if (kind == MZ_IN_ASCII) {
     z.take<uint64_t>((n + 31) / 32 + 1);
     z.take<uint32_t>((n + 31) / 32 + 1);
@@ -907,6 +1036,7 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   MzArgs a{};
   a.tile_counter = c.take<uint32_t>(1);
   a.status = c.take<uint64_t>(max_tiles(n));
+  uint64_t* ridx = c.take<uint64_t>(ridx_entries(n));
   a.nwords = (n + 31) / 32;
   if (in->kind == MZ_IN_ASCII) {
     uint64_t* words = c.take<uint64_t>(a.nwords + 1);
@@ -923,6 +1053,12 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   a.nwin = n - span + 1;
   a.read_off = in->read_off;
   a.nreads = in->read_off ? in->nreads : 0;
+  if (in->read_off) {
+    const uint64_t nb = ridx_entries(n);
+    ridx_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(in->read_off, a.nreads, ridx, nb);
+    MZS_LAUNCHED();
+    a.ridx = ridx;
+  }
   a.pos_base = in->pos_base;
   a.win_lo = in->win_lo;
   a.win_hi = in->win_hi;

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--skip", type=int, default=0)
     ap.add_argument("--per", type=float, default=1.0)
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--by-stall", action="store_true", help="sort by stall samples instead of instructions")
     a = ap.parse_args()
     out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k",
                           f"regex:{a.kernel}", "--launch-skip", str(a.skip), "--launch-count", "1"],
@@ -47,7 +48,8 @@ def main():
     tot_s = sum(x[1] for x in agg) or 1
     print(f"thread-inst {tot_i:,} = {tot_i / a.per:.1f} per unit")
     print(f"{'inst/unit':>9} {'inst%':>6} {'stall%':>6}  line")
-    for ti, smp, loc, src in sorted(agg, reverse=True)[:a.top]:
+    key = (lambda x: x[1]) if a.by_stall else (lambda x: x[0])
+    for ti, smp, loc, src in sorted(agg, key=key, reverse=True)[:a.top]:
         print(f"{ti / a.per:9.2f} {ti / tot_i * 100:6.1f} {smp / tot_s * 100:6.1f}  {loc:18s} {src[:80]}")
 
 
