@@ -142,9 +142,11 @@ __device__ __forceinline__ void or_bits(uint32_t* m, uint32_t s0, uint64_t v) {
 // xor-shift work on the always-zero high bits); KM bit 0 (RAW): keys are the codes themselves;
 // KM bit 1 (CANON): the code is min(forward, reverse complement), the reverse complement
 // rolled alongside (the entering base's complement enters at the top, R32).
-template <class Key, int Q, bool H64, bool CHECK, int KK = 0, int KM = 0>
+template <class Key, int Q, bool H64, bool CHECK, int KK = 0, int KM = 0, int WC = 0>
 __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_t s0, Key* keys, uint32_t* wvb,
-                                            const uint64_t* pre = nullptr) {
+                                            const uint64_t* pre = nullptr, const int64_t* rs = nullptr,
+                                            int nrs = -1) {
+  // rs[0 .. nrs): every read start the caller's tile range holds (shared memory), or nrs < 0
   static_assert(Q <= 33, "validity bits of one strip fit in a u64 shifted by < 32");
   uint64_t vbits = 0;
   const int k = KK ? KK : a.k;
@@ -160,7 +162,7 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   uint64_t iv = 0;
   int64_t next_rs = INT64_MAX;
   uint64_t ri = 0;
-  const int span = k + a.w - 1;
+  const int span = k + (WC ? WC : a.w) - 1;  // compile-time with KK and WC (w) both given
   // BULK validity (the strip's windows and their bases fit one 64-bit mask): window s (last
   // k-mer q0+s) covers bases [L+s, L+s+span), L = q0-w+1.  It is invalid iff an invalid base
   // lies in that range -- the OR of the invalid bits over span positions, by doubling and one
@@ -168,7 +170,7 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
   // starts in (L+s, L+s+span).  Same result as the run counter below, without a walk.
   const bool bulk = CHECK && Q + span - 1 <= 64;
   if (bulk) {
-    const int64_t L = q0 - (a.w - 1);
+    const int64_t L = q0 - (span - k);
     uint64_t T = inv_window64(a, L);  // bit j <-> base L+j invalid
     int p = 1;
     while (2 * p <= span) {
@@ -178,11 +180,21 @@ __device__ __forceinline__ void phase1_keys(const MzArgs& a, int64_t q0, uint32_
     uint64_t bad = T | (T >> (span - p));
     if (a.read_off) {
       const int64_t last = L + Q + span - 2;  // last base of the strip's last window
-      for (uint64_t r_i = upper_read(a, L); r_i <= a.nreads; ++r_i) {
-        const int64_t r = (int64_t)__ldg(a.read_off + r_i);  // > L
-        if (r > last) break;
+      auto drop = [&](int64_t r) {            // windows with a read start in (first, last base]
         const int64_t hi = min(r - L - 1, (int64_t)63), lo = max(r - L - span + 1, (int64_t)0);
         if (hi >= lo) bad |= ((2ull << (hi - lo)) - 1ull) << lo;
+      };
+      if (nrs >= 0) {
+        for (int i = 0; i < nrs; ++i) {
+          const int64_t r = rs[i];
+          if (r > L && r <= last) drop(r);
+        }
+      } else {
+        for (uint64_t r_i = upper_read(a, L); r_i <= a.nreads; ++r_i) {
+          const int64_t r = (int64_t)__ldg(a.read_off + r_i);  // > L
+          if (r > last) break;
+          drop(r);
+        }
       }
     }
     vbits = ~bad & ((1ull << Q) - 1ull);
@@ -421,7 +433,7 @@ __device__ __forceinline__ bool tile_is_clean(const MzArgs& a, int64_t b_lo, int
 // phase 1 when it is clean -- with ~1 read start per 10 kbp (C4) most warps are.
 template <int TPB, int DW>
 __device__ __forceinline__ bool subtile_dirty_map(const MzArgs& a, int64_t b_lo, int64_t b_hi, uint32_t* dwm,
-                                                  const uint32_t* pre) {
+                                                  const uint32_t* pre, const int64_t* rs, const int* p_nrs) {
   const int64_t W0 = b_lo >> 5;
   int dirty = 0;
   if (a.invalid) {
@@ -438,7 +450,18 @@ __device__ __forceinline__ bool subtile_dirty_map(const MzArgs& a, int64_t b_lo,
       }
     }
   }
-  if (a.read_off && threadIdx.x < 32) {
+  const int nrs = (a.read_off && p_nrs && threadIdx.x < 32) ? *p_nrs : -1;  // (warp 0 wrote it)
+  if (a.read_off && threadIdx.x < 32 && nrs >= 0) {
+    // the super-tile's read starts are in shared memory
+    for (int i = threadIdx.x; i < nrs; i += 32) {
+      const int64_t r = rs[i];
+      if (r > b_lo && r < b_hi) {
+        dirty = 1;
+        const uint32_t u = (uint32_t)((r >> 5) - (b_lo >> 5));
+        atomicOr(&dwm[u >> 5], 1u << (u & 31));
+      }
+    }
+  } else if (a.read_off && threadIdx.x < 32) {
     // read starts r with b_lo < r < b_hi: warp 0 walks them 32 at a time
     uint64_t r0 = 0;
     if (threadIdx.x == 0) r0 = upper_read(a, b_lo);
@@ -550,9 +573,13 @@ struct FastGeom {
 // [vlo, vhi): windows that exist; [elo, ehi): windows allowed to emit (shard range).
 // FULL: every window of the strip (and the one before it) is valid and may emit -- the
 // common case -- so the per-window work is the 3 minima plus the change test.
-template <int W, bool CHECK, bool FULL, class Key>
+template <int W, bool CHECK, bool FULL, class Key, bool MASKED = false>
 __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb, int vlo, int vhi, int elo,
-                                            int ehi, uint32_t* emit) {
+                                            int ehi, uint32_t* emit, uint64_t vm = ~0ull) {
+  // MASKED (with FULL): the strip lies inside the emission range but some of its windows are
+  // invalid (a read start or an N nearby); vm bit i = window jb-1+i is valid.  The argmin of
+  // every valid window is marked: the same set as the change rule, since the argmin of two
+  // valid windows can only coincide when every window between them is valid (D3).
   using G = FastGeom<W>;
   const int jb = threadIdx.x * G::R;
   Key S[W], kb[W];
@@ -571,7 +598,8 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
       // every window's argmin is marked (argmins never decrease, so a repeat hits the same
       // bit); the carried-in argmin of window jb-1, owned by the strip on the left, is cleared
       // once after the strip (R3)
-      em |= 1ull << (s - (uint32_t)(jb + 1));
+      if (MASKED) em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
+      else em |= 1ull << (s - (uint32_t)(jb + 1));
     } else {
       const bool v = valid_of(j);
       const bool e = v && (!vprev || s != sprev) && ((unsigned)(j - elo) < (unsigned)(ehi - elo));
@@ -611,7 +639,7 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
 #pragma unroll
     for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
   }
-  if (FULL) {
+  if (FULL && (!MASKED || (vm & 1u))) {  // (an invalid window jb-1 carries no record)
     const uint32_t rel = s_carry - (uint32_t)(jb + 1);  // wraps (large) when the carry is left of the strip
     if (rel < 64u) em &= ~(1ull << rel);
   }
@@ -710,6 +738,10 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   __shared__ uint64_t warp_sums[G::TPB / 32];
   __shared__ uint64_t bcast;
   __shared__ uint32_t s_tile;
+  // the read starts inside the current super-tile's bases (segmented input), found once per
+  // super-tile by warp 0; s_nrs < 0: more than 31 (the sub-tiles search global memory)
+  __shared__ int64_t s_rs[32];
+  __shared__ int s_nrs;
   const int t = threadIdx.x;
   int64_t pend = -1;           // previous super-tile awaiting output
   uint32_t pend_excl = 0, pend_total = 0;
@@ -735,6 +767,18 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       pinv = ldi(a, w0);
     };
     prefetch(super_lo);
+    if (a.read_off && t < 32) {
+      const int64_t lo_b = super_lo - 1, hi_b = super_lo - 1 + (int64_t)(G::SUBS - 1) * G::TW + G::NS + a.k;
+      uint64_t r0 = 0;
+      if (t == 0) r0 = upper_read(a, lo_b);   // first read start > lo_b
+      r0 = __shfl_sync(0xffffffffu, r0, 0);
+      const uint64_t r = r0 + t;
+      const int64_t v = r <= a.nreads ? (int64_t)__ldg(a.read_off + r) : INT64_MAX;
+      const uint32_t in = __ballot_sync(0xffffffffu, v < hi_b);
+      if (v < hi_b) s_rs[t] = v;
+      if (t == 0) s_nrs = (in == 0xffffffffu) ? -1 : __popc(in);
+      __syncwarp();
+    }
     for (int sub = 0; sub < G::SUBS; ++sub) {
       const int64_t tile_lo = super_lo + (int64_t)sub * G::TW;
       if (tile_lo >= (int64_t)a.nwin) break;
@@ -742,7 +786,8 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       for (int u = t; u < G::NSW + 3; u += G::TPB) wvb[u] = 0;
       const uint32_t inv0 = pinv;
       uint32_t* dm = dwm[sub & 1];
-      const bool clean = subtile_dirty_map<G::TPB, DW>(a, b_lo, b_hi, dm, &inv0);  // (also the barrier for wvb)
+      const bool clean = subtile_dirty_map<G::TPB, DW>(a, b_lo, b_hi, dm, &inv0, s_rs, &s_nrs);  // (also the barrier for wvb)
+      const int nrs = a.read_off ? s_nrs : 0;  // every warp reads the list after that barrier
       if (t < DW) dwm[(sub + 1) & 1][t] = 0;  // next sub-tile's map (unused until then)
       const int64_t q0 = tile_lo - 1 + (int64_t)t * G::Q;
       const uint32_t s0 = (uint32_t)(t * G::Q);
@@ -760,11 +805,11 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       const uint64_t w3[3] = {pw[0], pw[1], pw[2]};
       constexpr int KMC = CN ? 2 : 0;  // canonical keys: a separate kernel instantiation
       if (!a.raw) {
-        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC>(a, q0, s0, keys, wvb, w3);
-        else phase1_keys<Key, G::Q, H64, true, KK, KMC>(a, q0, s0, keys, wvb, w3);
+        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC, W>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<Key, G::Q, H64, true, KK, KMC, W>(a, q0, s0, keys, wvb, w3, s_rs, nrs);
       } else {
-        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
-        else phase1_keys<Key, G::Q, H64, true, KK, KMC | 1>(a, q0, s0, keys, wvb, w3);
+        if (wclean) phase1_keys<Key, G::Q, H64, false, KK, KMC | 1, W>(a, q0, s0, keys, wvb, w3);
+        else phase1_keys<Key, G::Q, H64, true, KK, KMC | 1, W>(a, q0, s0, keys, wvb, w3, s_rs, nrs);
       }
       if (!clean && wclean) or_bits(wvb, s0, (1ull << G::Q) - 1);  // every window ending here is valid
       if (sub + 1 < G::SUBS) prefetch(tile_lo + G::TW);
@@ -781,12 +826,17 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
       // FULL: windows jb-1 .. jb+R-1 all valid (bits jb-1+W .. jb+R-1+W of wvb when the
       // sub-tile is dirty) and inside the emission range
       const bool inr = vlo <= jb - 1 && jb + G::R <= vhi && elo <= jb && jb + G::R <= ehi;
-      const uint64_t vm = (1ull << (G::R + 1)) - 1;
-      const bool full = inr && (clean || (bits64(wvb, jb - 1 + W) & vm) == vm);
       uint32_t* em = emit[cur] + sub * G::NSW;
-      if (full) fast_phase2<W, false, true>(keys, wvb, vlo, vhi, elo, ehi, em);
-      else if (clean) fast_phase2<W, false, false>(keys, wvb, vlo, vhi, elo, ehi, em);
-      else fast_phase2<W, true, false>(keys, wvb, vlo, vhi, elo, ehi, em);
+      if (clean) {
+        if (inr) fast_phase2<W, false, true>(keys, wvb, vlo, vhi, elo, ehi, em);
+        else fast_phase2<W, false, false>(keys, wvb, vlo, vhi, elo, ehi, em);
+      } else {
+        // dirty sub-tile: every in-range strip takes the masked FULL path (no divergence
+        // between strips with and without invalid windows)
+        const uint64_t vm = bits64(wvb, jb - 1 + W) & ((1ull << (G::R + 1)) - 1);
+        if (inr) fast_phase2<W, false, true, Key, true>(keys, wvb, vlo, vhi, elo, ehi, em, vm);
+        else fast_phase2<W, true, false>(keys, wvb, vlo, vhi, elo, ehi, em);
+      }
       __syncthreads();
     }
     // count this super-tile's records and publish the count right away
