@@ -701,8 +701,11 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
       const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
       const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
       q[u] = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
-      A[u] = i < lim ? ldw(a, q[u] >> 5) : 0ull;
-      B[u] = i < lim ? ldw(a, (q[u] >> 5) + 1) : 0ull;
+      // an emitted k-mer lies in [0, n), so its first word exists; the next one is needed only
+      // when the k-mer crosses into it, so clamping its index (instead of a bounds test) is safe
+      const uint64_t wq = (uint64_t)max(q[u] >> 5, (int64_t)0);
+      A[u] = i < lim ? __ldg(a.words + wq) : 0ull;
+      B[u] = i < lim ? __ldg(a.words + min(wq + 1, a.nwords - 1)) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
