@@ -139,6 +139,25 @@ def test_segments_reads(path):
         _same(s, k, w, path=path, read_off=ro)
 
 
+@pytest.mark.parametrize("lens", [(900, 1100), (60, 140), (8192, 8192), (20000, 40000)])
+def test_read_start_density(lens):
+    """Read-start handling of the fast kernel: ~31 starts per super-tile (the shared-memory
+    list's capacity edge), very short reads (list overflow -> global search), reads starting
+    exactly on the 8 kbp blocks of the coarse read index, and long reads; N-runs mixed in.
+    Bit-exact vs the oracle, ASCII and packed input."""
+    rng = np.random.default_rng(lens[0])
+    n = 400_003
+    s = _rand_seq(rng, n, pn=0.0005)
+    lo, hi = lens
+    ln = rng.integers(lo, hi + 1, size=n // lo + 2)
+    st = np.concatenate([[0], np.cumsum(ln)])
+    st = st[st < n]
+    ro = np.concatenate([st, [n]]).astype(np.uint64)
+    for k, w in [(15, 10), (19, 10)]:
+        _same(s, k, w, read_off=ro)
+        _same(s, k, w, read_off=ro, packed=True)
+
+
 def test_c4_like_batch():
     c4 = G.C4(nreads=300)
     s = c4.ascii_range(0, c4.n)
