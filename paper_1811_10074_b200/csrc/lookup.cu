@@ -78,28 +78,45 @@ __global__ void __launch_bounds__(kLTPB) lookup_kernel(const uint64_t* __restric
 
 // One thread per query (no ballots): 32 independent random lookups in flight per warp, for
 // tables whose buckets are short (the scan of a bucket is a serial loop in the thread).
+// The count step also records each query's first matching entry (first[i]); the emit step
+// then skips the queries without hits and starts at that entry -- no second pointer-table
+// read and no second scan of the leading entries (one dependent random access fewer).
 template <bool EMIT>
 __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restrict__ q, uint64_t nq_cap,
                                                         const uint64_t* d_nq, int k, int bits,
                                                         const uint64_t* __restrict__ offsets,
                                                         const uint32_t* __restrict__ fp,
                                                         const uint64_t* __restrict__ pos_tab, uint64_t* hit_off,
-                                                        uint64_t* __restrict__ hit_pos, uint64_t hit_cap) {
+                                                        uint64_t* __restrict__ hit_pos, uint64_t hit_cap,
+                                                        uint64_t* __restrict__ first) {
   const uint64_t nq = query_count(d_nq, nq_cap);
   for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
-    const uint32_t f = fp_of(q[i], k);
-    const uint64_t b = f >> (32 - bits);
-    const uint64_t lo = offsets[b], hi = offsets[b + 1];
-    uint64_t o = EMIT ? hit_off[i] : 0;
-    uint64_t cnt = 0;
-    for (uint64_t e = lo; e < hi; ++e) {
-      if (fp[e] == f) {
-        if (EMIT && o < hit_cap) hit_pos[o] = pos_tab[e];
-        ++o;
-        ++cnt;
+    if (EMIT) {
+      uint64_t o = hit_off[i];
+      const uint64_t o_end = hit_off[i + 1];
+      if (o == o_end) continue;
+      const uint32_t f = fp_of(q[i], k);
+      // the hits are the first o_end - o entries from first[i] on whose fingerprint is f
+      for (uint64_t e = first[i]; o < o_end; ++e) {
+        if (fp[e] == f) {
+          if (o < hit_cap) hit_pos[o] = pos_tab[e];
+          ++o;
+        }
       }
+    } else {
+      const uint32_t f = fp_of(q[i], k);
+      const uint64_t b = f >> (32 - bits);
+      const uint64_t lo = offsets[b], hi = offsets[b + 1];
+      uint64_t cnt = 0, e0 = lo;
+      for (uint64_t e = lo; e < hi; ++e) {
+        if (fp[e] == f) {
+          if (cnt == 0) e0 = e;
+          ++cnt;
+        }
+      }
+      hit_off[i] = cnt;
+      first[i] = e0;
     }
-    if (!EMIT) hit_off[i] = cnt;
   }
 }
 
@@ -173,6 +190,7 @@ MZS_API size_t seedtable_lookup_workspace_bytes(uint64_t nq) {
   Sizer z;
   z.take<uint64_t>((nq + kSB - 1) / kSB + 1);
   z.take<uint64_t>(1);
+  z.take<uint64_t>(nq);  // first matching entry per query (one-lane kernel)
   return z.used;
 }
 
@@ -201,6 +219,8 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
   Carve c(ws, ws_bytes);
   const uint64_t nb = (nq + kSB - 1) / kSB;
   uint64_t* bsum = c.take<uint64_t>(nb + 1);
+  c.take<uint64_t>(1);
+  uint64_t* first = c.take<uint64_t>(nq);
   if (!c.ok) return SLSUM_ENOMEM;
   // lanes per query: 1 (a thread per query, the most lookups in flight) when buckets are short
   // (>= 2^26 buckets for the tables measured), else 8; MZS_LOOKUP_LANES overrides (tuning)
@@ -217,7 +237,8 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
     uint64_t* hp = E ? hit_pos : nullptr;
     const uint64_t hc = E ? hit_cap : 0;
     if (lanes == 1)
-      lookup1_kernel<E><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+      lookup1_kernel<E><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc,
+                                               first);
     else if (lanes == 8)
       lookup_kernel<E, 8><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
     else if (lanes == 32)
