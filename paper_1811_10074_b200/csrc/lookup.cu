@@ -95,9 +95,13 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
       uint64_t o = hit_off[i];
       const uint64_t o_end = hit_off[i + 1];
       if (o == o_end) continue;
+      // the hits are the first o_end - o entries from first[i] on whose fingerprint is f;
+      // first[i] itself is one (no need to read its fingerprint again)
+      const uint64_t e0 = first[i];
+      if (o < hit_cap) hit_pos[o] = pos_tab[e0];
+      if (++o == o_end) continue;
       const uint32_t f = fp_of(q[i], k);
-      // the hits are the first o_end - o entries from first[i] on whose fingerprint is f
-      for (uint64_t e = first[i]; o < o_end; ++e) {
+      for (uint64_t e = e0 + 1; o < o_end; ++e) {
         if (fp[e] == f) {
           if (o < hit_cap) hit_pos[o] = pos_tab[e];
           ++o;
