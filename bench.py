@@ -360,7 +360,7 @@ def bench_lookup(args):
     hbm_peak, peak_kind, _ = load_peaks()
     # 2^28 buckets (offsets 2 GiB): minimizer hashes are skewed low, so with 2^24 buckets a query
     # scans ~120 fingerprints of its (size-biased) bucket; at 2^28 about 8 (R30)
-    k, w, bits = 15, 10, 28
+    k, w, bits = 15, 10, int(os.environ.get("MZS_LOOKUP_BITS", "28"))  # 24: the C5 table geometry
     nq_reads = 100_000
     c4 = H.C4()
     tn = c4.tlen

@@ -31,48 +31,76 @@ __device__ __forceinline__ uint64_t query_count(const uint64_t* d_nq, uint64_t n
   return d_nq ? min(*d_nq, nq) : nq;
 }
 
-// EMIT = false: hit_off[i] = number of hits of query i.  EMIT = true: write them at hit_off[i].
+// EMIT = false: hit_off[i] = number of hits of query i, first[i] = its first matching entry.
+// EMIT = true: write them at hit_off[i] (exclusive offsets), scanning from first[i] until all
+// hit_off[i+1] - hit_off[i] hits are found (hitless queries read nothing of the table).
 template <bool EMIT, int kG>
 __global__ void __launch_bounds__(kLTPB) lookup_kernel(const uint64_t* __restrict__ q, uint64_t nq_cap,
                                                        const uint64_t* d_nq, int k, int bits,
                                                        const uint64_t* __restrict__ offsets,
                                                        const uint32_t* __restrict__ fp,
                                                        const uint64_t* __restrict__ pos_tab, uint64_t* hit_off,
-                                                       uint64_t* __restrict__ hit_pos, uint64_t hit_cap) {
+                                                       uint64_t* __restrict__ hit_pos, uint64_t hit_cap,
+                                                       uint64_t* __restrict__ first) {
   const uint64_t nq = query_count(d_nq, nq_cap);
   const unsigned lane = lane_id();
   const unsigned gl = lane & (kG - 1);                   // lane inside the group
   const unsigned gshift = lane & ~(unsigned)(kG - 1);    // group's first lane
   const unsigned gmask = (kG == 32 ? 0xffffffffu : ((1u << kG) - 1u)) << gshift;
   const uint64_t groups = (uint64_t)gridDim.x * (kLTPB / kG);
+  const uint64_t m_tab = EMIT ? offsets[(uint64_t)1 << bits] : 0;  // table entries (reads stay below)
   for (uint64_t i0 = ((uint64_t)blockIdx.x * kLTPB + threadIdx.x) / kG; i0 < ((nq + groups - 1) / groups) * groups;
        i0 += groups) {
     const bool live = i0 < nq;
     uint32_t f = 0;
-    uint64_t lo = 0, hi = 0, o = 0;
+    uint64_t lo = 0, hi = 0, o = 0, o_end = 0;
     if (live) {
-      f = fp_of(q[i0], k);
-      const uint64_t b = f >> (32 - bits);
-      lo = offsets[b];
-      hi = offsets[b + 1];
-      if (EMIT) o = hit_off[i0];
-    }
-    uint64_t cnt = 0;
-    // all groups of the warp iterate together (ballots need the full warp)
-    uint64_t len = hi - lo;
-    uint64_t steps = (len + kG - 1) / kG;
-    for (int o2 = kG; o2 < 32; o2 <<= 1) steps = max(steps, (uint64_t)__shfl_xor_sync(0xffffffffu, steps, o2));
-    for (uint64_t s = 0; s < steps; ++s) {
-      const uint64_t e = lo + s * kG + gl;
-      const bool hit = e < hi && fp[e] == f;
-      const unsigned bal = __ballot_sync(0xffffffffu, hit) & gmask;
-      if (EMIT && hit) {
-        const uint64_t r = o + cnt + __popc(bal & ((1u << lane) - 1u));
-        if (r < hit_cap) hit_pos[r] = pos_tab[e];
+      if (EMIT) {
+        o = hit_off[i0];
+        o_end = hit_off[i0 + 1];
+        if (o < o_end) {
+          f = fp_of(q[i0], k);
+          lo = first[i0];
+          hi = m_tab;
+        }
+      } else {
+        f = fp_of(q[i0], k);
+        const uint64_t b = f >> (32 - bits);
+        lo = offsets[b];
+        hi = offsets[b + 1];
       }
-      cnt += __popc(bal);
     }
-    if (!EMIT && live && gl == 0) hit_off[i0] = cnt;
+    uint64_t cnt = 0, e0 = lo;
+    // all groups of the warp iterate together (ballots need the full warp)
+    if (EMIT) {
+      for (uint64_t s = 0;; ++s) {
+        const bool pending = o + cnt < o_end;
+        if (!__any_sync(0xffffffffu, pending)) break;
+        const uint64_t e = lo + s * kG + gl;
+        const bool hit = pending && e < hi && fp[e] == f;
+        const unsigned bal = __ballot_sync(0xffffffffu, hit) & gmask;
+        if (hit) {
+          const uint64_t r = o + cnt + __popc(bal & ((1u << lane) - 1u));
+          if (r < o_end && r < hit_cap) hit_pos[r] = pos_tab[e];
+        }
+        cnt += __popc(bal);
+      }
+    } else {
+      uint64_t len = hi - lo;
+      uint64_t steps = (len + kG - 1) / kG;
+      for (int o2 = kG; o2 < 32; o2 <<= 1) steps = max(steps, (uint64_t)__shfl_xor_sync(0xffffffffu, steps, o2));
+      for (uint64_t s = 0; s < steps; ++s) {
+        const uint64_t e = lo + s * kG + gl;
+        const bool hit = e < hi && fp[e] == f;
+        const unsigned bal = __ballot_sync(0xffffffffu, hit) & gmask;
+        if (cnt == 0 && bal) e0 = lo + s * kG + (__ffs(bal >> gshift) - 1);
+        cnt += __popc(bal);
+      }
+      if (live && gl == 0) {
+        hit_off[i0] = cnt;
+        first[i0] = e0;
+      }
+    }
   }
 }
 
@@ -244,11 +272,14 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
       lookup1_kernel<E><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc,
                                                first);
     else if (lanes == 8)
-      lookup_kernel<E, 8><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+      lookup_kernel<E, 8><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc,
+                                                   first);
     else if (lanes == 32)
-      lookup_kernel<E, 32><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+      lookup_kernel<E, 32><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc,
+                                                   first);
     else
-      lookup_kernel<E, 16><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc);
+      lookup_kernel<E, 16><<<grid, kLTPB, 0, st>>>(qkey, nq, d_nq, k, bucket_bits, offsets, fp, pos_tab, hit_off, hp, hc,
+                                                   first);
     MZS_LAUNCHED();
     return SLSUM_OK;
   };
