@@ -52,8 +52,8 @@ constexpr int kDIPT = 8;                    // downsweep items per thread per su
 constexpr int kDTile = kDTPB * kDIPT;       // 4096 entries per downsweep sub-tile
 constexpr int kStages = 2;                  // TMA ring depth (sub-tiles in flight per CTA)
 constexpr int kGrp = 8;                     // write granularity: 8 entries = 32 B fp, 64 B pos
-constexpr int kChunk = 131072;              // entries per chunk
-constexpr int kSubs = kChunk / kDTile;      // 32 sub-tiles per chunk
+constexpr int kChunk = 131072;              // entries per chunk (at most; see chunk_for)
+constexpr int kMinChunk = 4096;             // and at least: whole tiles of every kernel
 
 // Peers of this lane's digit d within the warp (lanes with the same d; d == 256 for
 // invalid lanes), by a bitwise ballot multi-split: nbits+1 ballots, no match.any.
@@ -88,7 +88,7 @@ __device__ __forceinline__ uint32_t load_key(const void* keys, uint64_t i, int k
 template <int IN>
 __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const uint64_t* d_m, uint64_t m_cap, int k,
                                                        int shift, int dbits, uint32_t* counts, uint64_t nchunks,
-                                                       const uint64_t* ctl, int want) {
+                                                       const uint64_t* ctl, int want, uint32_t chunk) {
   if (gate_off(ctl, want)) return;
   __shared__ uint32_t h[kNW][256];
   const unsigned lane = lane_id(), wid = warp_id();
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(kTPB) upsweep_kernel(const void* keys, const u
   for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {  // grid-stride over chunks
     for (int i = lane; i < 256; i += 32) h[wid][i] = 0;
     __syncthreads();
-    const uint64_t base = c * (uint64_t)kChunk;
-    const uint64_t end = min(m, base + kChunk);
+    const uint64_t base = c * (uint64_t)chunk;
+    const uint64_t end = min(m, base + chunk);
     {
       uint64_t i = base + threadIdx.x;
       for (; i + 3 * kTPB < end; i += 4 * kTPB) {  // 4 loads in flight per thread
@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
                                                          const uint64_t* d_m, uint64_t m_cap, int k, int shift,
                                                          int dbits, const uint64_t* __restrict__ offsets,
                                                          const unsigned long long* __restrict__ dbase,
-                                                         uint64_t nchunks, const uint64_t* ctl, int use_tma) {
+                                                         uint64_t nchunks, const uint64_t* ctl, int use_tma,
+                                                         uint32_t chunk) {
   if (gate_off(ctl, 0)) return;
   using SM = DownSmem<FROM_HASH>;
   using KT = typename SM::KT;
@@ -207,8 +208,8 @@ __global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in
     S.carry_lo[td] = r;
   }
   __syncthreads();
-  const uint64_t cbase = c * (uint64_t)kChunk;
-  const int nsubs = (int)min((uint64_t)kSubs, (m - min(m, cbase) + kDTile - 1) / kDTile);
+  const uint64_t cbase = c * (uint64_t)chunk;
+  const int nsubs = (int)min((uint64_t)(chunk / kDTile), (m - min(m, cbase) + kDTile - 1) / kDTile);
   auto full = [&](int sub) { return use_tma && cbase + (uint64_t)(sub + 1) * kDTile <= m; };
   auto issue = [&](int sub) {
     if (threadIdx.x == 0 && sub < nsubs && full(sub)) {
@@ -432,14 +433,14 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
                                                        uint64_t m_cap, int k, int shift, int dbits,
                                                        const uint64_t* __restrict__ offsets,
                                                        const unsigned long long* __restrict__ dbase, uint64_t nchunks,
-                                                       uint64_t* ctl, int use_tma,
+                                                       uint64_t* ctl, int use_tma, uint32_t chunk,
                                                        uint32_t* const* __restrict__ dfp = nullptr,
                                                        uint64_t* const* __restrict__ dpos = nullptr) {
   // dfp/dpos (OUT == kOutFpPos only): per-digit destination arrays, e.g. the peer-mapped receive
   // buffers of the owner ranks (seedtable_partition_p2p); digit d's entries go to dfp[d][g]
   constexpr int T = TPB * IPT;
   constexpr int NW = TPB / 32;
-  static_assert(kChunk % T == 0, "chunk must hold whole tiles");
+  static_assert(kChunk % T == 0 && kMinChunk % T == 0, "chunks hold whole tiles");
   static_assert(TPB >= 256, "digit threads");
   using SM = NSmem<IN, TPB, T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
   const unsigned lane = lane_id(), wid = warp_id(), lt = (1u << lane) - 1u;
   const uint32_t dmask = (1u << dbits) - 1u;
   const int dsh = 32 + shift;
-  const uint64_t c = blockIdx.x, cbase = c * (uint64_t)kChunk;
+  const uint64_t c = blockIdx.x, cbase = c * (uint64_t)chunk;
   if (cbase >= m) return;
   if (td < 256) S.run_off[td] = dbase[td] + offsets[(uint64_t)td * nchunks + c];
   for (uint32_t i = td; i < NW * 256; i += TPB) (&S.wcnt[0][0])[i] = 0;
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
     fence_mbar_init();
   }
   __syncthreads();
-  const int nsubs = (int)min((uint64_t)(kChunk / T), (m - cbase + T - 1) / T);
+  const int nsubs = (int)min((uint64_t)(chunk / T), (m - cbase + T - 1) / T);
   auto tma_ok = [&](int sub) { return use_tma && cbase + (uint64_t)(sub + 1) * T <= m; };
   auto issue = [&](int sub) {
     if (td == 0 && sub < nsubs && tma_ok(sub)) {
@@ -819,6 +820,7 @@ __global__ void u32_to_u64_kernel(const unsigned long long* in, uint64_t* out, i
 
 // ---------------------------------------------------------------- host helpers
 struct SortWs {
+  uint32_t chunk;             // entries per chunk (chunk_for(m))
   uint32_t* counts;           // [256 * nchunks]
   uint64_t* offs;             // [256 * nchunks]
   unsigned long long* totals; // [256]
@@ -831,7 +833,16 @@ struct SortWs {
   uint32_t* fpF;              // final fingerprints when the caller gave none
 };
 
-uint64_t chunks_for(uint64_t m) { return (m + kChunk - 1) / kChunk + 1; }
+// Chunk size: kChunk entries, but small inputs take smaller chunks (a multiple of 4096) so that
+// about 296 CTAs (2 per SM) share the passes instead of a handful working through 128K
+// entries each (C1's 1.9e5 entries were 2 chunks).  A function of m only (no device query), so
+// the workspace size and the carve agree.
+uint32_t chunk_for(uint64_t m) {
+  const uint64_t want = (m + 295) / 296;
+  const uint64_t c = (want + kMinChunk - 1) / kMinChunk * kMinChunk;
+  return (uint32_t)std::min<uint64_t>(kChunk, std::max<uint64_t>(kMinChunk, c));
+}
+uint64_t chunks_for(uint64_t m) { return (m + chunk_for(m) - 1) / chunk_for(m) + 1; }
 
 template <class C>
 void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
@@ -853,6 +864,7 @@ void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
 
 bool carve_sort_ws(Carve& c, uint64_t m, int npass, bool need_fp, SortWs& s) {
   s = SortWs{};
+  s.chunk = chunk_for(m);
   s.counts = c.take<uint32_t>(256 * chunks_for(m));
   s.offs = c.take<uint64_t>(256 * chunks_for(m));
   s.totals = c.take<unsigned long long>(256);
@@ -880,7 +892,7 @@ template <int IN>
 int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s,
                int want, cudaStream_t st) {
   const unsigned grid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms() * 8);
-  upsweep_kernel<IN><<<grid, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want);
+  upsweep_kernel<IN><<<grid, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want, s.chunk);
   MZS_LAUNCHED();
   chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals, s.ctl, want);
   MZS_LAUNCHED();
@@ -896,7 +908,7 @@ int launch_nsweep(const void* a_in, const uint64_t* p_in, void* a_out, uint64_t*
   const size_t sm = nsweep_smem<IN, TPB, IPT>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   kern<<<(unsigned)nch, TPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                       use_tma, nullptr, nullptr);
+                                       use_tma, s.chunk, nullptr, nullptr);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -922,7 +934,7 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st) {
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
-  const uint64_t nch = (m + kChunk - 1) / kChunk;
+  const uint64_t nch = (m + s.chunk - 1) / s.chunk;
   if (nch == 0) return SLSUM_OK;
   int rc;
   static const int force = env_int("MZS_RADIX_PATH", -1);  // tests/tuning: 0 forces the wide path
@@ -975,10 +987,10 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       const unsigned wgrid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms());
       if (kin_hash)
         ds1<<<wgrid, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                                p == 0 ? tma_in : 1);
+                                                p == 0 ? tma_in : 1, s.chunk);
       else
         ds0<<<wgrid, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                                p == 0 ? tma_in : 1);
+                                                p == 0 ? tma_in : 1, s.chunk);
       MZS_LAUNCHED();
       kin = fo;
       pin = po;
@@ -1176,7 +1188,7 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   uint64_t* dptr = c.take<uint64_t>(2 * (size_t)nranks);
   if (!c.ok) return SLSUM_ENOMEM;
   const int g = log2i(nranks);
-  const uint64_t nch = (m + kChunk - 1) / kChunk;
+  const uint64_t nch = (m + s.chunk - 1) / s.chunk;
   // the narrow precondition, decided here on the host (one small read)
   uint64_t h[3] = {m, 0, 0};
   if (d_m) MZS_CUDA(cudaMemcpyAsync(&h[0], d_m, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
@@ -1207,7 +1219,7 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   const size_t smem = nsweep_smem<kInHashPos, 256, 8>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)nch, 256, smem, st>>>(hash, pos, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                         tma_in, reinterpret_cast<uint32_t* const*>(dptr),
+                                         tma_in, s.chunk, reinterpret_cast<uint32_t* const*>(dptr),
                                          reinterpret_cast<uint64_t* const*>(dptr + nranks));
   MZS_LAUNCHED();
   // the host vectors above were read by the async copies; make them complete before returning
