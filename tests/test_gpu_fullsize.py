@@ -122,3 +122,25 @@ def test_c4_bench_path_full_size_sampled():
         hi = int(torch.searchsorted(pi, torch.tensor([b], dtype=torch.int64, device="cuda")).item())
         assert np.array_equal(pi[li:hi].cpu().numpy().astype(np.uint64), op_), r
         assert np.array_equal(h[li:hi].cpu().numpy(), ok), r
+
+
+@pytest.mark.parametrize("w", [16, 100, 1024])
+def test_slsum_beyond_2_32_elements(w):
+    """64-bit indexing of the sliding-sum kernels: n = 2^32 + 4099 u32 elements (16 GiB in,
+    16 GiB out), GENERIC and COMMUTATIVE paths, outputs sampled around the 2^32 boundary and
+    at the end vs the oracle on the same elements (regenerated on the host)."""
+    from synthgen import device as D
+    import paper_1811_10074_b200 as P
+    n = (1 << 32) + 4099
+    x = D.c2_u32(n)
+    idx = np.array([0, (1 << 32) - w - 3, (1 << 32) - w + 1, (1 << 32) - 1, 1 << 32, n - w - 7, n - w], np.int64)
+    it = torch.from_numpy(idx).cuda()
+    for path in (P.SLSUM_PATH_GENERIC, P.SLSUM_PATH_COMMUTATIVE):
+        y = P.slsum_run(P.SLSUM_MIN_U32, w, x, path=path)
+        assert y.numel() == n - w + 1
+        ys = y.view(torch.int32)[it].cpu().numpy().view(np.uint32)
+        for j, i in enumerate(idx):
+            assert ys[j] == O.slsum(O.MIN_U32, w, G.c2_u32(w, lo=int(i)))[0], (path, int(i))
+        del y
+    del x
+    torch.cuda.empty_cache()
