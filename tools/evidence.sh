@@ -11,6 +11,7 @@ timeout 600 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --config c2 --steps 10 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 900 python bench.py --config c4 --steps 5 > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+timeout 600 python bench.py --config c1 --steps 20 > $O/bench_c1.json 2> $O/bench_c1.err
 # launch list of one timed C3 step (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_c3.log 2>&1
