@@ -43,31 +43,12 @@ __device__ __forceinline__ uint64_t block_count(const uint64_t* d_m, uint64_t m_
 // ---------------------------------------------------------------- stable LSD radix pass
 // Reduce-then-scan (no serial look-back chains): the m entries are cut into chunks of
 // kChunk; (U) counts per (digit, chunk); (S) exclusive scan over chunks per digit, then
-// over digits; (D) every chunk re-reads its entries sub-tile by sub-tile, ranks them
-// stably (ballot multi-split + per-warp counters), stages them in digit order in shared
-// memory and writes each digit run contiguously.
-constexpr int kDTPB = 512;                  // downsweep threads per CTA (16 warps, 1 CTA per SM)
-constexpr int kDNW = kDTPB / 32;
-constexpr int kDIPT = 8;                    // downsweep items per thread per sub-tile
-constexpr int kDTile = kDTPB * kDIPT;       // 4096 entries per downsweep sub-tile
+// over digits; (D) every chunk re-reads its entries tile by tile, ranks them stably
+// (per-warp peer bit tables + per-warp counters, nsweep_kernel), stages them in digit order
+// in shared memory and writes each digit run contiguously.
 constexpr int kStages = 2;                  // TMA ring depth (sub-tiles in flight per CTA)
-constexpr int kGrp = 8;                     // write granularity: 8 entries = 32 B fp, 64 B pos
 constexpr int kChunk = 131072;              // entries per chunk (at most; see chunk_for)
 constexpr int kMinChunk = 4096;             // and at least: whole tiles of every kernel
-
-// Peers of this lane's digit d within the warp (lanes with the same d; d == 256 for
-// invalid lanes), by a bitwise ballot multi-split: nbits+1 ballots, no match.any.
-__device__ __forceinline__ unsigned warp_peers(uint32_t d, int nbits) {
-  unsigned peers = 0xffffffffu;
-  for (int b = 0; b < nbits; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const unsigned m = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? m : ~m;
-  }
-  const bool inv = d >= 256u;
-  const unsigned mi = __ballot_sync(0xffffffffu, inv);
-  return peers & (inv ? mi : ~mi);
-}
 
 // Path gate: the narrow (packed u64) and wide (u32 fp + u64 pos) passes are both enqueued;
 // each kernel runs only if ctl[0] selects its path (ctl == nullptr: always run).  ctl[0] is
@@ -151,185 +132,6 @@ __global__ void digit_scan_kernel(const unsigned long long* totals, unsigned lon
   base[threadIdx.x] = block_exclusive_sum<256, unsigned long long>(totals[threadIdx.x], ws, &tot);
 }
 
-// Shared memory of one downsweep CTA: two input buffers filled by TMA bulk copies (the
-// next sub-tile streams in while the current one is ranked and scattered); the current
-// buffer is then reused in place as the digit-sorted staging area for coalesced writes.
-template <bool FROM_HASH>
-struct DownSmem {
-  using KT = typename std::conditional<FROM_HASH, uint64_t, uint32_t>::type;
-  KT kin[kStages][kDTile];
-  uint64_t pin[kStages][kDTile];
-  uint64_t mbar[kStages];
-  uint32_t cfp[256][kGrp];   // carried run tails, slot = global index & 7
-  uint64_t cpos[256][kGrp];
-  uint64_t run_off[256];     // next global index of digit d
-  uint64_t carry_lo[256];    // digit d's carried entries are [carry_lo, run_off)
-  uint64_t wlim[256];        // this sub-tile writes digit d's indices < wlim (8-aligned)
-  uint64_t gbase[256];       // run_off[d] - dstart[d]: staged entry j of digit d goes to gbase + j
-  uint16_t wcnt[kDNW][256];
-  uint16_t dstart[256];
-  uint16_t tcount[256];
-  unsigned long long ws2[kDNW];
-};
-
-// One chunk per CTA, streamed through a TMA ring of sub-tiles.  Per sub-tile: stable rank
-// by digit (ballot multi-split), stage in digit order (in place), then write every digit's
-// run in whole 8-entry groups; the ragged tail of each run is carried in shared memory to
-// the next sub-tile, so DRAM sees full sectors except at the chunk's edges.
-template <bool FROM_HASH, bool MATCH>
-__global__ void __launch_bounds__(kDTPB, 1) downsweep_kernel(const void* keys_in, const uint64_t* __restrict__ pos_in,
-                                                         uint32_t* __restrict__ fp_out, uint64_t* __restrict__ pos_out,
-                                                         const uint64_t* d_m, uint64_t m_cap, int k, int shift,
-                                                         int dbits, const uint64_t* __restrict__ offsets,
-                                                         const unsigned long long* __restrict__ dbase,
-                                                         uint64_t nchunks, const uint64_t* ctl, int use_tma,
-                                                         uint32_t chunk) {
-  if (gate_off(ctl, 0)) return;
-  using SM = DownSmem<FROM_HASH>;
-  using KT = typename SM::KT;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  SM& S = *reinterpret_cast<SM*>(smem_raw);
-  const unsigned lane = lane_id(), wid = warp_id();
-  const uint64_t m = block_count(d_m, m_cap);
-  const uint32_t dmask = (1u << dbits) - 1u;
-  const unsigned lt = (1u << lane) - 1u;
-  const KT* kg = static_cast<const KT*>(keys_in);
-  const uint32_t td = threadIdx.x;  // digit owned by this thread when td < 256
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
-    fence_mbar_init();
-  }
-  uint32_t parity = 0;
-  // grid-stride over chunks (a small grid: the gated-off launch costs a few us, not 40 waves)
-  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-  if (td < 256) {
-    const uint64_t r = dbase[td] + offsets[(uint64_t)td * nchunks + c];
-    S.run_off[td] = r;
-    S.carry_lo[td] = r;
-  }
-  __syncthreads();
-  const uint64_t cbase = c * (uint64_t)chunk;
-  const int nsubs = (int)min((uint64_t)(chunk / kDTile), (m - min(m, cbase) + kDTile - 1) / kDTile);
-  auto full = [&](int sub) { return use_tma && cbase + (uint64_t)(sub + 1) * kDTile <= m; };
-  auto issue = [&](int sub) {
-    if (threadIdx.x == 0 && sub < nsubs && full(sub)) {
-      const int b = sub % kStages;
-      const uint64_t base = cbase + (uint64_t)sub * kDTile;
-      mbar_arrive_expect_tx(&S.mbar[b], kDTile * (uint32_t)(sizeof(KT) + sizeof(uint64_t)));
-      bulk_g2s(S.kin[b], kg + base, kDTile * sizeof(KT), &S.mbar[b]);
-      bulk_g2s(S.pin[b], pos_in + base, kDTile * sizeof(uint64_t), &S.mbar[b]);
-    }
-  };
-  for (int p = 0; p < kStages - 1; ++p) issue(p);
-  for (int sub = 0; sub < nsubs; ++sub) {
-    const int b = sub % kStages;
-    const uint64_t base = cbase + (uint64_t)sub * kDTile;
-    issue(sub + kStages - 1);
-    if (full(sub)) {
-      mbar_wait(&S.mbar[b], (parity >> b) & 1u);
-      parity ^= 1u << b;
-    } else {
-      for (uint32_t j = threadIdx.x; j < kDTile; j += kDTPB) {
-        const bool v = base + j < m;
-        S.kin[b][j] = v ? kg[base + j] : (KT)0;
-        S.pin[b][j] = v ? pos_in[base + j] : 0ull;
-      }
-      __syncthreads();
-    }
-    for (int i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;
-    __syncwarp();
-    uint32_t key[kDIPT], rank[kDIPT];
-    uint64_t pos[kDIPT];
-#pragma unroll
-    for (int it = 0; it < kDIPT; ++it) {
-      const uint32_t j = wid * (kDIPT * 32) + it * 32 + lane;
-      const bool valid = base + j < m;
-      const KT kv = S.kin[b][j];
-      const uint32_t f = FROM_HASH ? fingerprint((uint64_t)kv, k) : (uint32_t)kv;
-      const uint32_t d = valid ? ((f >> shift) & dmask) : 256u;
-      const unsigned peers = MATCH ? __match_any_sync(0xffffffffu, d) : warp_peers(d, dbits);
-      const uint32_t before = __popc(peers & lt);
-      const uint32_t cc = (d < 256u) ? S.wcnt[wid][d] : 0u;
-      __syncwarp();
-      if (d < 256u && before == 0) S.wcnt[wid][d] = (uint16_t)(cc + __popc(peers));
-      __syncwarp();
-      key[it] = f;
-      pos[it] = S.pin[b][j];
-      rank[it] = (d < 256u) ? cc + before : 0xffffffffu;
-    }
-    __syncthreads();
-    uint32_t run = 0;
-    if (td < 256) {
-#pragma unroll
-      for (int w = 0; w < kDNW; ++w) {
-        const uint32_t cc = S.wcnt[w][td];
-        S.wcnt[w][td] = (uint16_t)run;
-        run += cc;
-      }
-      S.tcount[td] = (uint16_t)run;
-    }
-    {
-      unsigned long long tot;
-      // digits are owned by threads 0..255 (the first 8 warps); the scan runs over them
-      const unsigned long long ex = block_exclusive_sum<kDTPB, unsigned long long>(td < 256 ? run : 0u, S.ws2, &tot);
-      if (td < 256) {
-        S.dstart[td] = (uint16_t)ex;
-        // this sub-tile writes [carry_lo, floor8(run_off + count)); flush the carried part now
-        const uint64_t r0 = S.run_off[td], r1 = r0 + run, g0 = S.carry_lo[td];
-        const uint64_t lim = r1 & ~(uint64_t)(kGrp - 1);
-        S.wlim[td] = lim;
-        S.gbase[td] = r0 - ex;
-        for (uint64_t g = g0; g < min(r0, lim); ++g) {
-          fp_out[g] = S.cfp[td][g & (kGrp - 1)];
-          pos_out[g] = S.cpos[td][g & (kGrp - 1)];
-        }
-      }
-    }
-    __syncthreads();
-    // stage in digit order, in place in ring slot b (fingerprints as u32)
-    uint32_t* sk = reinterpret_cast<uint32_t*>(S.kin[b]);
-#pragma unroll
-    for (int it = 0; it < kDIPT; ++it) {
-      if (rank[it] != 0xffffffffu) {
-        const uint32_t d = (key[it] >> shift) & dmask;
-        const uint32_t j = S.dstart[d] + S.wcnt[wid][d] + rank[it];
-        sk[j] = key[it];
-        S.pin[b][j] = pos[it];
-      }
-    }
-    __syncthreads();
-    const uint32_t nsub = (uint32_t)min((uint64_t)kDTile, m - base);
-    for (uint32_t j = threadIdx.x; j < nsub; j += kDTPB) {
-      const uint32_t f = sk[j];
-      const uint32_t d = (f >> shift) & dmask;
-      const uint64_t g = S.gbase[d] + j;
-      const uint64_t p = S.pin[b][j];
-      if (g < S.wlim[d]) {
-        fp_out[g] = f;
-        pos_out[g] = p;
-      } else {
-        S.cfp[d][g & (kGrp - 1)] = f;
-        S.cpos[d][g & (kGrp - 1)] = p;
-      }
-    }
-    fence_proxy_async();  // ring slot b is refilled by TMA in a later iteration
-    __syncthreads();
-    if (td < 256) {
-      S.carry_lo[td] = max(S.carry_lo[td], S.wlim[td]);
-      S.run_off[td] += S.tcount[td];
-    }
-    __syncthreads();
-  }
-  // flush the carried tails
-  if (td < 256) {
-    for (uint64_t g = S.carry_lo[td]; g < S.run_off[td]; ++g) {
-      fp_out[g] = S.cfp[td][g & (kGrp - 1)];
-      pos_out[g] = S.cpos[td][g & (kGrp - 1)];
-    }
-  }
-  __syncthreads();
-  }
-}
 
 
 // Optional per-phase cycle counters of the narrow downsweep (build with -DMZS_PROF; read via
@@ -427,13 +229,13 @@ __device__ __forceinline__ uint64_t make_item(const NIn<IN, T>& r, uint32_t j, i
 }
 
 
-template <int IN, int OUT, int TPB, int IPT>
+template <int IN, int OUT, int TPB, int IPT, bool WD = false>
 __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uint64_t* __restrict__ p_in,
                                                        void* a_out, uint64_t* __restrict__ p_out, const uint64_t* d_m,
                                                        uint64_t m_cap, int k, int shift, int dbits,
                                                        const uint64_t* __restrict__ offsets,
                                                        const unsigned long long* __restrict__ dbase, uint64_t nchunks,
-                                                       uint64_t* ctl, int use_tma, uint32_t chunk,
+                                                       uint64_t* ctl, int use_tma, uint32_t chunk, int gate,
                                                        uint32_t* const* __restrict__ dfp = nullptr,
                                                        uint64_t* const* __restrict__ dpos = nullptr) {
   // dfp/dpos (OUT == kOutFpPos only): per-digit destination arrays, e.g. the peer-mapped receive
@@ -441,6 +243,11 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
   constexpr int T = TPB * IPT;
   constexpr int NW = TPB / 32;
   static_assert(kChunk % T == 0 && kMinChunk % T == 0, "chunks hold whole tiles");
+  // WD: the wide path (positions spanning >= 2^32, or unsorted): an entry stays (fp, full
+  // position) in registers -- `item` carries fp in its high word for the ranking, `ipos` the
+  // position -- and is staged as two arrays (fp over the ring's key array, positions over
+  // its position array), written as u32 fp + u64 position
+  static_assert(!WD || (IN != kInPk && OUT == kOutFpPos), "wide passes read and write fp + pos");
   static_assert(TPB >= 256, "digit threads");
   using SM = NSmem<IN, TPB, T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -449,7 +256,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
   __shared__ int s_go;
   const uint32_t td = threadIdx.x;
   if (td == 0) {
-    s_go = ld_volatile_u64(ctl) == 1;
+    s_go = ld_volatile_u64(ctl) == (uint64_t)gate;  // 1: packed items, 0: WD (the wide path)
     s_m = min(count_of(d_m, m_cap), m_cap);
     s_p0 = ctl[1];
   }
@@ -516,6 +323,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
     MZS_PROF_MARK(1);
     // ---- stable rank of every item within its digit (warp-major item order)
     uint64_t item[IPT];
+    uint64_t ipos[WD ? IPT : 1];
     uint32_t rank[IPT];
     auto rank_tile = [&](auto whole_tag) {
       constexpr bool kWhole = decltype(whole_tag)::value;
@@ -533,7 +341,15 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
         for (int u = 0; u < kPeerTables; ++u) {
           const int it = g + u;
           const uint32_t j = wid * (IPT * 32) + it * 32 + lane;
-          item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
+          if constexpr (WD) {
+            uint32_t f;
+            if constexpr (IN == kInHashPos) f = fingerprint(S.ring[b].a[j], k);
+            else f = S.ring[b].a[j];
+            item[it] = (uint64_t)f << 32;
+            ipos[it] = S.ring[b].p[j];
+          } else {
+            item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
+          }
           if (kWhole || j < nvalid) atomicOr(&pm[u][(uint32_t)(item[it] >> dsh) & dmask], 1u << lane);
         }
         __syncwarp();
@@ -614,15 +430,32 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
     MZS_PROF_MARK(3);
     // ---- stage in digit order (in place: every item of this tile is in registers)
     uint64_t* stage = stage_of<IN, T>(S.ring[b]);
+    uint32_t* stage_f = reinterpret_cast<uint32_t*>(S.ring[b].a);  // (WD) fingerprints
     const uint32_t* wrow = S.wcnt[wid];
 #pragma unroll
-    for (int it = 0; it < IPT; ++it)
-      if (rank[it] != 0xffffffffu) stage[wrow[(uint32_t)(item[it] >> dsh) & dmask] + rank[it]] = item[it];
+    for (int it = 0; it < IPT; ++it) {
+      if (rank[it] != 0xffffffffu) {
+        const uint32_t sl = wrow[(uint32_t)(item[it] >> dsh) & dmask] + rank[it];
+        if constexpr (WD) {
+          stage_f[sl] = (uint32_t)(item[it] >> 32);
+          stage[sl] = ipos[WD ? it : 0];
+        } else {
+          stage[sl] = item[it];
+        }
+      }
+    }
     __syncthreads();
     for (uint32_t i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;  // own row: read only by this warp above
     MZS_PROF_MARK(4);
     // ---- write every digit run contiguously
     auto put = [&](uint32_t j) {
+      if constexpr (WD) {
+        const uint32_t f = stage_f[j];
+        const uint64_t g = S.gbase[(f >> shift) & dmask] + j;
+        static_cast<uint32_t*>(a_out)[g] = f;
+        p_out[g] = stage[j];
+        return;
+      }
       const uint64_t v = stage[j];
       const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
       if constexpr (OUT == kOutPk) {
@@ -646,7 +479,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
     __syncthreads();
     MZS_PROF_MARK(5);
   }
-  if constexpr (IN != kInPk) {
+  if constexpr (IN != kInPk && !WD) {
     if (__syncthreads_or(bad) && td == 0) st_volatile_u64(ctl, 0);  // precondition broken: wide path redoes it
   }
 }
@@ -901,14 +734,14 @@ int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, 
   return SLSUM_OK;
 }
 
-template <int IN, int OUT, int TPB, int IPT>
+template <int IN, int OUT, int TPB, int IPT, bool WD = false>
 int launch_nsweep(const void* a_in, const uint64_t* p_in, void* a_out, uint64_t* p_out, const uint64_t* d_m,
                   uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s, int use_tma, cudaStream_t st) {
-  auto kern = nsweep_kernel<IN, OUT, TPB, IPT>;
+  auto kern = nsweep_kernel<IN, OUT, TPB, IPT, WD>;
   const size_t sm = nsweep_smem<IN, TPB, IPT>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   kern<<<(unsigned)nch, TPB, sm, st>>>(a_in, p_in, a_out, p_out, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                       use_tma, s.chunk, nullptr, nullptr);
+                                       use_tma, s.chunk, WD ? 0 : 1, nullptr, nullptr);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -966,14 +799,9 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     }
     if (rc) return rc;
   }
-  // ---- wide path: every pass (gated off when the narrow path holds)
+  // ---- wide path: every pass (gated off when the narrow path holds); the same ranking and
+  // staging as the narrow passes with (u32 fp, u64 position) entries (nsweep_kernel WD)
   {
-    const size_t dsm1 = sizeof(DownSmem<true>), dsm0 = sizeof(DownSmem<false>);
-    static const bool use_match = env_int("MZS_RADIX_MATCH", 0) == 1;
-    auto ds1 = use_match ? downsweep_kernel<true, true> : downsweep_kernel<true, false>;
-    auto ds0 = use_match ? downsweep_kernel<false, true> : downsweep_kernel<false, false>;
-    MZS_CUDA(cudaFuncSetAttribute(ds1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm1));
-    MZS_CUDA(cudaFuncSetAttribute(ds0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm0));
     const void* kin = keys;
     const uint64_t* pin = pos;
     bool kin_hash = from_hash;
@@ -984,14 +812,10 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       const int nb = std::min(8, hi_bit - sh);
       rc = kin_hash ? count_pass<0>(kin, d_m, m, k, sh, nb, nch, s, 0, st) : count_pass<1>(kin, d_m, m, k, sh, nb, nch, s, 0, st);
       if (rc) return rc;
-      const unsigned wgrid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms());
-      if (kin_hash)
-        ds1<<<wgrid, kDTPB, dsm1, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                                p == 0 ? tma_in : 1, s.chunk);
-      else
-        ds0<<<wgrid, kDTPB, dsm0, st>>>(kin, pin, fo, po, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                                p == 0 ? tma_in : 1, s.chunk);
-      MZS_LAUNCHED();
+      const int tma = p == 0 ? tma_in : 1;
+      rc = kin_hash ? launch_nsweep<kInHashPos, kOutFpPos, 256, 8, true>(kin, pin, fo, po, d_m, m, k, sh, nb, nch, s, tma, st)
+                    : launch_nsweep<kInFpPos, kOutFpPos, 256, 8, true>(kin, pin, fo, po, d_m, m, k, sh, nb, nch, s, tma, st);
+      if (rc) return rc;
       kin = fo;
       pin = po;
       kin_hash = false;
@@ -1219,7 +1043,7 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   const size_t smem = nsweep_smem<kInHashPos, 256, 8>();
   MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)nch, 256, smem, st>>>(hash, pos, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                         tma_in, s.chunk, reinterpret_cast<uint32_t* const*>(dptr),
+                                         tma_in, s.chunk, 1, reinterpret_cast<uint32_t* const*>(dptr),
                                          reinterpret_cast<uint64_t* const*>(dptr + nranks));
   MZS_LAUNCHED();
   // the host vectors above were read by the async copies; make them complete before returning
