@@ -727,7 +727,9 @@ def main():
     ops = MZ_INT_OPS_PER_BASE.get(k, 48) * n
     ach = ops / (phase_ms["extract"] * 1e-3) / 1e12
     tr = load_traffic("traffic_c3.json") if k == 19 else None
-    mz_traffic = tr.get("mz_fast_kernel<10, 1, 19>", {}).get("dram_bytes") if tr else None
+    # per launch: the capture holds one step's kernels (tools/evidence.sh); mz runs once per step
+    mzk = [v for kk, v in (tr or {}).items() if kk.startswith("mz_fast_kernel<10, 1, 19")]
+    mz_traffic = mzk[0]["dram_bytes"] / max(1, mzk[0].get("launches", 1)) if mzk else None
     tab_traffic = sum(v["dram_bytes"] for kk, v in tr.items() if kk.startswith(("nsweep", "upsweep"))) if tr else None
     roof = {"bound": "alu", "kernel": "mz_fast_kernel (a2-a7 fused, one launch per step)",
             "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": mz_traffic,

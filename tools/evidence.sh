@@ -11,13 +11,15 @@ timeout 600 python bench.py > $O/bench_c3.json 2> $O/bench_c3.err
 timeout 600 python bench.py --config c2 --steps 10 > $O/bench_c2.json 2> $O/bench_c2.err
 timeout 900 python bench.py --config c4 --steps 5 > $O/bench_c4.json 2> $O/bench_c4.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
-timeout 600 python bench.py --config c1 --steps 20 > $O/bench_c1.json 2> $O/bench_c1.err
+timeout 600 python bench.py --config c1 --steps 3000 > $O/bench_c1.json 2> $O/bench_c1.err
 # launch list of one timed C3 step (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_c3.log 2>&1
 # full sections of the top kernels of the C3 step (after 3 warm-up steps) and of slsum (C2)
+# one step matches 14 kernels (encode, mz, 3 packed passes x (upsweep, nsweep), and the wide
+# path's 3 x 2 enqueued-but-gated ones); skip the 3 warm-up steps, capture the timed one
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mz_fast|^nsweep|encode_kernel|upsweep" \
-  -s 33 -c 11 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/full_c3.log 2>&1
+  -s 42 -c 14 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/full_c3.log 2>&1
 # one named C2 configuration per capture (tools/slsum_one.py launches exactly 4 slsum kernels;
 # the 4th, warm one is captured)
 for cfg in "min 16 generic" "min 1024 generic" "min 4 commutative" "min 1024 commutative" "add 64 recurrent"; do

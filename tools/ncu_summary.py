@@ -96,8 +96,9 @@ def launches(path, last_step=None):
 
 
 def traffic(path):
-    """JSON {kernel base name: {"dram_bytes": read + write per launch, "time_ms": ...}} of a
-    --set full capture (first launch of each kernel name) -- bench.py's roofline `traffic`."""
+    """JSON {kernel name: {"dram_bytes": read + write summed over the capture's launches of that
+    name, "launches": n, "time_ms": summed}} of a --set full capture of ONE step's kernels --
+    bench.py's roofline `traffic` (per launch = dram_bytes / launches)."""
     import json
     rows = _csv([path, "--page", "raw"])
     hdr = rows[0]
@@ -105,8 +106,6 @@ def traffic(path):
     for r in rows[2:]:
         name = re.sub(r"\(.*", "", r[hdr.index("Kernel Name")]).replace("(anonymous namespace)::", "")
         name = re.sub(r"^.*unnamed>::", "", name.replace("mzs::", "").replace("void ", "")).strip()
-        if name in out:
-            continue
 
         def val(m, scale):
             i = hdr.index(m)
@@ -115,8 +114,10 @@ def traffic(path):
             return v * scale.get(u, 1.0)
         gb = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
         ms = {"ms": 1.0, "us": 1e-3, "ns": 1e-6, "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}
-        out[name] = {"dram_bytes": val("dram__bytes_read.sum", gb) + val("dram__bytes_write.sum", gb),
-                     "time_ms": val("gpu__time_duration.sum", ms)}
+        e = out.setdefault(name, {"dram_bytes": 0.0, "launches": 0, "time_ms": 0.0})
+        e["dram_bytes"] += val("dram__bytes_read.sum", gb) + val("dram__bytes_write.sum", gb)
+        e["launches"] += 1
+        e["time_ms"] += val("gpu__time_duration.sum", ms)
     print(json.dumps(out, indent=1))
 
 
