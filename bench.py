@@ -616,20 +616,21 @@ def main():
     # D2H of step i overlaps the H2D and compute of step i+1 (PCIe is full duplex).
     e2e = None
     if not args.no_e2e and world == 1:
-        B1 = Bufs()
-        sets = (B0, B1)
+        nset = max(2, int(os.environ.get("MZS_E2E_SETS", "2")))
+        extra = [Bufs() for _ in range(nset - 1)]
+        sets = (B0, *extra)
         host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         host_in.copy_(seq)
-        host_off = [torch.empty((1 << bits) + 1, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
-        host_pos = [torch.empty(cap, dtype=torch.uint64, pin_memory=True) for _ in range(2)]
-        host_cnt = torch.zeros(2, dtype=torch.int64, pin_memory=True)
-        seqd = [torch.empty_like(seq) for _ in range(2)]
+        host_off = [torch.empty((1 << bits) + 1, dtype=torch.uint64, pin_memory=True) for _ in range(nset)]
+        host_pos = [torch.empty(cap, dtype=torch.uint64, pin_memory=True) for _ in range(nset)]
+        host_cnt = torch.zeros(nset, dtype=torch.int64, pin_memory=True)
+        seqd = [torch.empty_like(seq) for _ in range(nset)]
         del seq
         s_h2d, s_cmp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        ev_h2d = [torch.cuda.Event() for _ in range(2)]
-        ev_cmp = [torch.cuda.Event() for _ in range(2)]
-        ev_d2h = [torch.cuda.Event() for _ in range(2)]
-        started = [False, False]
+        ev_h2d = [torch.cuda.Event() for _ in range(nset)]
+        ev_cmp = [torch.cuda.Event() for _ in range(nset)]
+        ev_d2h = [torch.cuda.Event() for _ in range(nset)]
+        started = [False] * nset
 
         def enqueue(b):
             with torch.cuda.stream(s_h2d):
@@ -665,17 +666,17 @@ def main():
         a.record(s_h2d)
         d2h = 0
         for i in range(ke):
-            enqueue(i % 2)
+            enqueue(i % nset)
             if i > 0:
-                d2h = readback((i - 1) % 2)
-        d2h = readback((ke - 1) % 2)
+                d2h = readback((i - 1) % nset)
+        d2h = readback((ke - 1) % nset)
         bev.record(s_d2h)
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(bev) / ke
         e2e = {"value": n_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gbases/s", "h2d_bytes_per_step": n,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
-               "pipeline": "2 buffer sets, streams H2D | compute | D2H; step i's D2H overlaps step i+1"}
-        del host_in, host_off, host_pos, seqd, B1
+               "pipeline": f"{nset} buffer sets, streams H2D | compute | D2H; step i's D2H overlaps step i+1"}
+        del host_in, host_off, host_pos, seqd, extra
     elif not args.no_e2e and world > 1:
         # N GPUs: every rank copies its shard's ASCII in (H2D), runs the step (extraction, then
         # the seed-table exchange, fused p2p or NCCL) and reads its slice of the table back (D2H); the
