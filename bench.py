@@ -160,6 +160,17 @@ def cpu_oracle_run(sample_bases: int):
     return sample_bases / dt / 1e9, dt, O.num_threads(), len(key)
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (record it beside the oracle's core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def reference_main(args, rank, world):
     if rank != 0:
         return 0
@@ -178,7 +189,7 @@ def reference_main(args, rank, world):
         "ms_per_step": sample / (v * 1e9) * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": "C3 sample", "k": K_MER, "w": W_WIN, "bucket_bits": BITS, "bases": sample},
-        "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": O.num_threads(), "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": "Gbases/s", "cores": O.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                          "sample": f"first {sample} bases of C3 (mz + seedtable oracle)"},
         "e2e": {"value": v, "unit": "Gbases/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -248,7 +259,7 @@ def bench_c2(args):
             for w in (4, 16, 64, 256, 1024):
                 O.slsum(oop, w, xs)
         dt = time.perf_counter() - t0
-        cpu = {"value": 15 * ns / dt / 1e9, "unit": "Gelem/s", "cores": O.num_threads(), "kind": "oracle",
+        cpu = {"value": 15 * ns / dt / 1e9, "unit": "Gelem/s", "cores": O.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"the 15 (op, w) runs on the first {ns} C2 elements each ({dt:.1f} s)"}
     line = {
         "metric": "generic sliding window sums (Eq. 2), Gelem/s",
@@ -328,7 +339,7 @@ def bench_c4(args):
         t0 = time.perf_counter()
         O.mz(s, k, w, read_off=c4.read_off[: r1 + 1].astype(np.uint64))
         dt = time.perf_counter() - t0
-        cpu = {"value": hi / dt / 1e9, "unit": "Gbases/s", "cores": O.num_threads(), "kind": "oracle",
+        cpu = {"value": hi / dt / 1e9, "unit": "Gbases/s", "cores": O.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"first {r1} reads ({hi} bases) of C4 ({dt:.1f} s)"}
     line = {
         "metric": "minimizer extraction over a long-read batch, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
@@ -413,7 +424,7 @@ def bench_lookup(args):
         t0 = time.perf_counter()
         O.lookup(qs, k, bits, to, tf, tpt)
         dt = time.perf_counter() - t0
-        cpu = {"value": len(qs) / dt / 1e9, "unit": "Gqueries/s", "cores": O.num_threads(), "kind": "oracle",
+        cpu = {"value": len(qs) / dt / 1e9, "unit": "Gqueries/s", "cores": O.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{len(qs)} of the queries against the oracle's table of a {ts}-base template prefix "
                          f"({dt:.1f} s)"}
     line = {
@@ -745,17 +756,18 @@ def main():
                   "traffic": tab_traffic,
                   "traffic_note": "DRAM bytes of the 3 passes' upsweeps + downsweeps (ncu); the SURVEY's "
                                   "algorithmic model is 32 B/entry, the 3-pass LSD moves 84 B/entry",
-                  "peak_kind": peak_kind, "ms": phase_ms["table"]}
+                  "peak_kind": peak_kind, "frac_vs_nominal_8tbs": tab_ach / 8000.0, "ms": phase_ms["table"]}
     step_bytes = sum(per_phase_bytes.values())
     step_hbm = {"achieved": step_bytes / (ms_step * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                 "frac": step_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak, "peak_kind": peak_kind,
+                "frac_vs_nominal_8tbs": step_bytes / (ms_step * 1e-3) / 1e9 / 8000.0,
                 "phase_ms": phase_ms,
                 "phase_frac": {kk: per_phase_bytes[kk] / (phase_ms[kk] * 1e-3) / 1e9 / hbm_peak for kk in phase_ms}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, cores, mm = cpu_oracle_run(args.cpu_sample_bases)
-        cpu = {"value": v, "unit": "Gbases/s", "cores": cores, "kind": "oracle",
+        cpu = {"value": v, "unit": "Gbases/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"first {args.cpu_sample_bases} bases of C3, k={k} w={w}: oracle mz + seedtable ({dt:.1f} s)"}
 
     if rank == 0:
