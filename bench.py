@@ -579,6 +579,9 @@ def main():
     gbases = n_total / (ms_step * 1e-3) / 1e9
 
     phase_ms = {kk: statistics.mean(a.elapsed_time(b) for a, b in v) for kk, v in ev.items()}
+    # per-step device times (encode start -> table end of each timed step): median and best
+    per_step = [a.elapsed_time(d) for (a, _), (_, d) in zip(ev["encode"], ev["table"])]
+    step_stats = {"median_ms": statistics.median(per_step), "best_ms": min(per_step), "steps": len(per_step)}
 
     # ---------------- C1 (1 Mbp, ~launch-bound): the step captured once in a CUDA graph and
     # replayed.  The inputs fit in L2, so every replay first overwrites a 256 MiB
@@ -774,7 +777,8 @@ def main():
         line = {
             "metric": "minimizer extraction + seed table, Gbases/s (whole job)",
             "value": gbases, "unit": "Gbases/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": ms_step, "step_ms": step_stats,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u64", "data": "synthetic",
             "config": {"workload": ("C3: 3.1 Gbp GC41% 1% N-runs" if c3 is not None else "C1: 1 Mbp uniform")
                        + (" (canonical minimizers)" if args.canonical else ""),
