@@ -250,12 +250,15 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_kernel(const typename Op::
 // register strips and the only exchange is the W-1 prefix values the last outputs of a lane
 // need from the next lane (shuffles).  Each warp owns a tile of 32E inputs and emits the first
 // 31E outputs (the last lane is the halo), so there is no shared memory and no barrier.
-template <class Op, int W>
+template <class Op, int W, int EE = 0>
 __global__ void __launch_bounds__(256) slsum_generic_warp_kernel(const typename Op::T* __restrict__ x,
                                                                 typename Op::T* __restrict__ y, uint64_t n,
                                                                 uint64_t nout) {
   using T = typename Op::T;
-  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  // EE: elements per lane when it is not the default 16 (8 for 8-byte types): a multiple of
+  // both W and the 16-byte vector, so that small w which do not divide 16 (3, 5, 6, 7, 10,
+  // 12, 14) also keep whole blocks inside a lane
+  constexpr int E = EE ? EE : ((sizeof(T) == 4) ? 16 : 8);
   constexpr uint32_t OV = 16 / sizeof(T);
   static_assert(E % W == 0 && W <= E, "blocks inside a lane");
   constexpr uint64_t kOut = 31ull * E;  // outputs per warp
@@ -299,15 +302,15 @@ __global__ void __launch_bounds__(256) slsum_generic_warp_kernel(const typename 
   }
 }
 
-template <class Op, int W>
+template <class Op, int W, int EE = 0>
 int launch_generic_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
-  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr int E = EE ? EE : ((sizeof(T) == 4) ? 16 : 8);
   const uint64_t nout = n - w + 1;
   const uint64_t warps = (nout + 31ull * E - 1) / (31ull * E);
   const uint64_t grid = (warps + 7) / 8;
-  slsum_generic_warp_kernel<Op, W><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n,
-                                                                  nout);
+  slsum_generic_warp_kernel<Op, W, EE><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv),
+                                                                      n, nout);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -537,6 +540,15 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 4) return launch_generic_warp<Op, 4>(xv, yv, n, w, st);
     if (w == 8) return launch_generic_warp<Op, 8>(xv, yv, n, w, st);
     if (w == 16 && E >= 16) return launch_generic_warp<Op, E >= 16 ? 16 : 8>(xv, yv, n, w, st);
+    // small w that do not divide E: lanes of a multiple of lcm(w, 16-byte vector) elements
+    constexpr bool B4 = sizeof(T) == 4;
+    if (w == 3) return launch_generic_warp<Op, 3, B4 ? 24 : 12>(xv, yv, n, w, st);
+    if (w == 5) return launch_generic_warp<Op, 5, B4 ? 20 : 10>(xv, yv, n, w, st);
+    if (w == 6) return launch_generic_warp<Op, 6, B4 ? 24 : 12>(xv, yv, n, w, st);
+    if (w == 7) return launch_generic_warp<Op, 7, B4 ? 28 : 14>(xv, yv, n, w, st);
+    if (w == 10) return launch_generic_warp<Op, 10, B4 ? 20 : 10>(xv, yv, n, w, st);
+    if (w == 12) return launch_generic_warp<Op, 12, B4 ? 24 : 12>(xv, yv, n, w, st);
+    if (w == 14) return launch_generic_warp<Op, 14, B4 ? 28 : 14>(xv, yv, n, w, st);
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);

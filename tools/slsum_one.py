@@ -29,10 +29,16 @@ def main():
     x = D.c2_f32(a.n) if a.op == "addf" else D.c2_u32(a.n)
     y = torch.empty(a.n - a.w + 1, dtype=x.dtype, device="cuda")
     torch.cuda.synchronize()
-    for _ in range(a.reps):
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    P.slsum_run(OPS[a.op], a.w, x, y=y, path=PATHS[a.path])
+    t0.record()
+    for _ in range(a.reps - 1):
         P.slsum_run(OPS[a.op], a.w, x, y=y, path=PATHS[a.path])
+    t1.record()
     torch.cuda.synchronize()
-    print(f"ok {a.op} w={a.w} {a.path} x{a.reps}")
+    ms = t0.elapsed_time(t1) / max(1, a.reps - 1)
+    print(f"ok {a.op} w={a.w} {a.path} x{a.reps}: {ms:.3f} ms/run, {a.n / ms / 1e6:.1f} Gelem/s, "
+          f"{8 * a.n / ms / 1e6:.0f} GB/s")
 
 
 if __name__ == "__main__":
