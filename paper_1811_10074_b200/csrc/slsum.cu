@@ -33,6 +33,32 @@ constexpr uint32_t slsum_smem_len(uint32_t L) {
   return L + (16 / sizeof(T)) * (L / (128 / sizeof(T)) + 1);
 }
 
+template <class T, uint32_t OV, uint32_t R>
+__device__ __forceinline__ void take_shifted(const T (&lo)[OV], const T (&hi)[OV], T (&o)[OV]) {
+#pragma unroll
+  for (uint32_t q = 0; q < OV; ++q) o[q] = (R + q < OV) ? lo[R + q] : hi[R + q - OV];
+}
+// o[q] = A[b + sh + q] for A in the padded layout (sidx), b a multiple of OV, sh < OV uniform
+// across the CTA: the two aligned 16-byte vectors around the run and a select (no divergence)
+template <class T, uint32_t OV, class Idx>
+__device__ __forceinline__ void ld_shifted_pad(const T* A, uint32_t b, uint32_t sh, Idx sidx, T (&o)[OV]) {
+  T lo[OV], hi[OV];
+  *reinterpret_cast<uint4*>(lo) = *reinterpret_cast<const uint4*>(A + sidx(b));
+  if (sh == 0) {
+#pragma unroll
+    for (uint32_t q = 0; q < OV; ++q) o[q] = lo[q];
+    return;
+  }
+  *reinterpret_cast<uint4*>(hi) = *reinterpret_cast<const uint4*>(A + sidx(b + OV));
+  if constexpr (OV == 4) {
+    if (sh == 1) take_shifted<T, OV, 1>(lo, hi, o);
+    else if (sh == 2) take_shifted<T, OV, 2>(lo, hi, o);
+    else take_shifted<T, OV, 3>(lo, hi, o);
+  } else {
+    take_shifted<T, OV, 1>(lo, hi, o);
+  }
+}
+
 // One tile of L = TPB*E inputs per CTA (tout outputs + the w-1 halo).  P and S are staged in
 // shared memory as 16-byte vectors with 16 B of padding every 128 B: the blocked 64-byte
 // writes of 8 consecutive threads then hit 8 distinct bank groups, and the strided output
@@ -86,15 +112,17 @@ __global__ void __launch_bounds__(TPB) slsum_generic_kernel(const typename Op::T
   uint32_t e_scalar = 0;
   if ((reinterpret_cast<uintptr_t>(y + g0) & 15) == 0) {
     const uint32_t step = (TPB * OV) % w;
+    const uint32_t psh = (w - 1) % OV;        // P[e + w - 1 ..] starts psh past an aligned vector
     uint32_t e = t * OV;
     uint32_t r = e % w;
     for (; e + OV <= e_end; e += TPB * OV) {
-      T s[OV], o[OV];
+      T s[OV], o[OV], pw[OV];
       *reinterpret_cast<uint4*>(s) = *reinterpret_cast<const uint4*>(sS + sidx(e));
+      ld_shifted_pad<T, OV>(sP, e + w - 1 - psh, psh, sidx, pw);
       uint32_t rr = r;
 #pragma unroll
       for (uint32_t q = 0; q < OV; ++q) {
-        o[q] = (rr == 0) ? s[q] : Op::op(s[q], sP[sidx(e + q + w - 1)]);
+        o[q] = (rr == 0) ? s[q] : Op::op(s[q], pw[q]);
         rr = (rr + 1 == w) ? 0u : rr + 1;
       }
       *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(o);
@@ -114,11 +142,6 @@ __global__ void __launch_bounds__(TPB) slsum_generic_kernel(const typename Op::T
 // elements (one LDS.128 of A[e..], one of A[e+d..] when d is a multiple of OV, otherwise the
 // shifted vector is assembled from two aligned ones; one STS.128), so a round costs a few
 // instructions per element.  Interior tiles are loaded and stored with 16-byte global accesses.
-template <class T, uint32_t OV, uint32_t R>
-__device__ __forceinline__ void take_shifted(const T (&lo)[OV], const T (&hi)[OV], T (&o)[OV]) {
-#pragma unroll
-  for (uint32_t q = 0; q < OV; ++q) o[q] = (R + q < OV) ? lo[R + q] : hi[R + q - OV];
-}
 // o[q] = A[e + d + q] for e a multiple of OV: one or two aligned 16-byte loads; the shift
 // r = d mod OV is uniform across the CTA, so the switch does not diverge
 template <class T, uint32_t OV>
