@@ -572,6 +572,10 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 10) return launch_generic_warp<Op, 10, B4 ? 20 : 10>(xv, yv, n, w, st);
     if (w == 12) return launch_generic_warp<Op, 12, B4 ? 24 : 12>(xv, yv, n, w, st);
     if (w == 14) return launch_generic_warp<Op, 14, B4 ? 28 : 14>(xv, yv, n, w, st);
+    if (w == 9) return launch_generic_warp<Op, 9, B4 ? 36 : 18>(xv, yv, n, w, st);
+    if (w == 11) return launch_generic_warp<Op, 11, B4 ? 44 : 22>(xv, yv, n, w, st);
+    if (w == 13) return launch_generic_warp<Op, 13, B4 ? 52 : 26>(xv, yv, n, w, st);
+    if (w == 15) return launch_generic_warp<Op, 15, B4 ? 60 : 30>(xv, yv, n, w, st);
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);
