@@ -610,12 +610,23 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
 }
 
 
-// COMMUTATIVE path for power-of-two w <= 64: the ceil(log2 w) doubling rounds
+// COMMUTATIVE path for small w (powers of two up to 4E, and 3..15): the doubling rounds
 // t_{r+1}[i] = t_r[i] (+) t_r[i + 2^r] on a warp tile held in registers (E consecutive values
-// per lane).  A round with 2^r < E pulls the next lane's first 2^r values by shuffles, one
-// with 2^r >= E pulls whole registers from lane + 2^r/E.  For w = 2^m, t_m is the window
-// fold itself (no finishing combine).  Each warp emits the outputs whose windows fit in its
-// 32E inputs; no shared memory, no barrier.
+// per lane).  A shift by s < E pulls the next lane's first s values by shuffles; a shift by
+// s >= E pulls whole registers from lane + s/E.  For w = 2^m, t_m is the window fold itself.
+// Otherwise, with m = floor(log2 w): an idempotent op finishes with t_m[i] (+) t_m[i+w-2^m]
+// (the two halves overlap); add takes the binary digits of w, the smallest piece
+// leftmost, t_{c0}[i] (+) t_{c1}[i+2^c0] (+) ... (every shift is a compile-time constant).
+// Each warp emits the outputs whose windows fit in its 32E inputs; no shared memory, no barrier.
+template <class T, int E, int SH>
+__device__ __forceinline__ void shifted_regs(const T (&t)[E], T (&u)[E]) {
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int src = j + SH;
+    if (src < E) u[j] = t[src];
+    else u[j] = shfl_down(t[src % E], src / E);
+  }
+}
 template <class Op, int W>
 __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename Op::T* __restrict__ x,
                                                                  typename Op::T* __restrict__ y, uint64_t n,
@@ -623,7 +634,9 @@ __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename
   using T = typename Op::T;
   constexpr int E = (sizeof(T) == 4) ? 16 : 8;
   constexpr uint32_t OV = 16 / sizeof(T);
-  static_assert((W & (W - 1)) == 0 && W >= 2 && W <= 4 * E, "power-of-two w, halo within a warp");
+  static_assert(W >= 2 && W <= 4 * E, "halo within a warp");
+  constexpr int M = 31 - __builtin_clz((unsigned)W);  // floor(log2 W)
+  constexpr int P2 = 1 << M;
   constexpr int HL = (W - 1 + E - 1) / E;             // halo lanes
   constexpr uint64_t kOut = (uint64_t)(32 - HL) * E;  // outputs per warp
   const uint32_t lane = threadIdx.x & 31;
@@ -639,30 +652,65 @@ __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename
 #pragma unroll
     for (int j = 0; j < E; ++j) t[j] = (g + j < n) ? x[g + j] : Op::id();
   }
-#pragma unroll
-  for (int d = 1; d < W; d <<= 1) {
+  // non-idempotent, w not a power of two: the binary-digit accumulation (acc, next offset)
+  constexpr bool kDigits = !Op::kIdempotent && W != P2;
+  T acc[E];
+  int off = 0;
+  bool have = false;
+  auto take = [&](auto shift_tag) {  // acc (+)= t shifted left by the tag's value
+    constexpr int SH = decltype(shift_tag)::value;
     T u[E];
-    if (d < E) {
-      T nx[E];
+    shifted_regs<T, E, SH>(t, u);
 #pragma unroll
-      for (int j = 0; j < d; ++j) nx[j] = shfl_down(t[j], 1);
-#pragma unroll
-      for (int j = 0; j < E; ++j) u[j] = Op::op(t[j], j + d < E ? t[(j + d) % E] : nx[(j + d - E) % E]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < E; ++j) u[j] = Op::op(t[j], shfl_down(t[j], d / E));
+    for (int j = 0; j < E; ++j) acc[j] = have ? Op::op(acc[j], u[j]) : u[j];
+    have = true;
+  };
+  auto digit = [&](auto r_tag) {
+    constexpr int R = decltype(r_tag)::value;
+    if constexpr (kDigits && ((W >> R) & 1)) {
+      // offset of this piece = the sum of the smaller pieces = W mod 2^R
+      take(std::integral_constant<int, (W & ((1 << R) - 1))>{});
     }
+  };
+  auto round = [&](auto r_tag) {   // t_r -> t_{r+1}
+    constexpr int D = 1 << decltype(r_tag)::value;
+    T u[E];
+    shifted_regs<T, E, D>(t, u);
 #pragma unroll
-    for (int j = 0; j < E; ++j) t[j] = u[j];
+    for (int j = 0; j < E; ++j) t[j] = Op::op(t[j], u[j]);
+  };
+  auto level = [&](auto r_tag) {
+    constexpr int R = decltype(r_tag)::value;
+    if constexpr (R <= M) {
+      digit(r_tag);
+      if constexpr (R < M) round(r_tag);
+    }
+  };
+  level(std::integral_constant<int, 0>{});
+  level(std::integral_constant<int, 1>{});
+  level(std::integral_constant<int, 2>{});
+  level(std::integral_constant<int, 3>{});
+  level(std::integral_constant<int, 4>{});
+  level(std::integral_constant<int, 5>{});
+  level(std::integral_constant<int, 6>{});
+  static_assert(M <= 6, "levels unrolled above");
+  T* out = t;
+  if constexpr (kDigits) {
+    out = acc;
+  } else if constexpr (W != P2) {  // idempotent: overlap of two 2^M windows
+    T u[E];
+    shifted_regs<T, E, W - P2>(t, u);
+#pragma unroll
+    for (int j = 0; j < E; ++j) t[j] = Op::op(t[j], u[j]);
   }
   if (lane >= 32 - HL) return;  // halo lanes
   if (g + E <= nout && ((reinterpret_cast<uintptr_t>(y + g) & 15) == 0)) {
 #pragma unroll
-    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(t + q);
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(out + q);
   } else {
 #pragma unroll
     for (int j = 0; j < E; ++j)
-      if (g + j < nout) y[g + j] = t[j];
+      if (g + j < nout) y[g + j] = out[j];
   }
 }
 
@@ -692,6 +740,18 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
     if (w == 16) return launch_doubling_warp<Op, 16>(xv, yv, n, w, st);
     if (w == 32) return launch_doubling_warp<Op, 32>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_doubling_warp<Op, 4 * E>(xv, yv, n, w, st);
+    // w = 3..15 outside the powers of two: finishing combine in registers too
+    if (w == 3) return launch_doubling_warp<Op, 3>(xv, yv, n, w, st);
+    if (w == 5) return launch_doubling_warp<Op, 5>(xv, yv, n, w, st);
+    if (w == 6) return launch_doubling_warp<Op, 6>(xv, yv, n, w, st);
+    if (w == 7) return launch_doubling_warp<Op, 7>(xv, yv, n, w, st);
+    if (w == 9) return launch_doubling_warp<Op, 9>(xv, yv, n, w, st);
+    if (w == 10) return launch_doubling_warp<Op, 10>(xv, yv, n, w, st);
+    if (w == 11) return launch_doubling_warp<Op, 11>(xv, yv, n, w, st);
+    if (w == 12) return launch_doubling_warp<Op, 12>(xv, yv, n, w, st);
+    if (w == 13) return launch_doubling_warp<Op, 13>(xv, yv, n, w, st);
+    if (w == 14) return launch_doubling_warp<Op, 14>(xv, yv, n, w, st);
+    if (w == 15) return launch_doubling_warp<Op, 15>(xv, yv, n, w, st);
   }
   const uint64_t nout = n - w + 1;
   // tile: tout = 8*TPB outputs (register accumulators) from L = tout + w - 1 inputs held in
