@@ -176,6 +176,9 @@ typedef struct mz_out {
   uint64_t* pos;             /* device, capacity entries */
   uint64_t capacity;
   uint64_t* d_count;         /* device, 1 entry          */
+  uint64_t* items;           /* device, capacity entries, or NULL: packed seed-table items
+                                fp(hash) << 32 | (pos mod 2^32), fp = the top 32 bits of the
+                                2k-bit key (seedtable_build_items' input)            */
 } mz_out_t;
 
 /* scratch for mz_extract_ex on n bases (tile descriptors + packed copy for ASCII) */
@@ -204,6 +207,15 @@ size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits);
 int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
                     int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out,
                     void* ws, size_t ws_bytes, void* stream);
+/* The same table from the packed items mz_extract_ex wrote (out->items) beside hash/pos: the
+ * first radix pass reads the 8-byte items instead of the 16-byte (hash, pos) pairs.  Requires
+ * items[i] = fp(hash[i]) << 32 | (pos[i] mod 2^32) and positions ascending (as mz_extract_ex
+ * writes them).  hash and pos are still read: pos[0] and pos[m-1] decide the packed path,
+ * and the wide path (positions spanning >= 2^32) sorts from hash/pos.  Same workspace and
+ * output as seedtable_build. */
+int seedtable_build_items(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                          const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets,
+                          uint32_t* fp_out, uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream);
 
 /* Multi-GPU phases (owner(bucket) = bucket >> (bucket_bits - log2 nranks); nranks a
  * power of two; NCCL all_reduce / all_to_all run between these calls):

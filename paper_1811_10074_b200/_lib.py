@@ -42,7 +42,7 @@ class MzIn(ctypes.Structure):
 
 class MzOut(ctypes.Structure):
     _fields_ = [("hash", ctypes.c_void_p), ("pos", ctypes.c_void_p), ("capacity", ctypes.c_uint64),
-                ("d_count", ctypes.c_void_p)]
+                ("d_count", ctypes.c_void_p), ("items", ctypes.c_void_p)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -72,6 +72,8 @@ _mz_extract_path = _sig("mz_extract_path", _i32, ctypes.POINTER(MzIn), _i32, _i3
 _mz_extract = _sig("mz_extract", _i32, _vp, _u64, _i32, _i32, ctypes.POINTER(MzOut))
 _st_ws = _sig("seedtable_workspace_bytes", _sz, _u64, _i32)
 _st_build = _sig("seedtable_build", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+_st_build_items = _sig("seedtable_build_items", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
+                       _vp)
 _st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
 _st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
 _st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
@@ -83,7 +85,7 @@ _st_lk = _sig("seedtable_lookup", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _v
 _st_fin = _sig("seedtable_finalize", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 
 EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_encode", "mz_workspace_bytes",
-           "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_count",
+           "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_build_items", "seedtable_count",
            "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
            "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup",
            "seedtable_partition_p2p_workspace_bytes", "seedtable_partition_p2p"]
@@ -158,8 +160,11 @@ def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, ki
                   win_lo: int = 0, win_hi: int = U64_MAX, keymode: int = MZ_KEY_HASH,
                   capacity: int | None = None, out_hash: torch.Tensor | None = None,
                   out_pos: torch.Tensor | None = None, d_count: torch.Tensor | None = None,
-                  ws: torch.Tensor | None = None, stream=None, path: int = 0):
-    """Asynchronous minimizer extraction; returns (hash, pos, d_count) device tensors (count on device)."""
+                  ws: torch.Tensor | None = None, stream=None, path: int = 0,
+                  out_items: torch.Tensor | None = None):
+    """Asynchronous minimizer extraction; returns (hash, pos, d_count) device tensors (count on device).
+    out_items (uint64, capacity entries, optional) also receives the packed seed-table items
+    (seedtable_build_items)."""
     if n is None:
         n = seq.numel() if kind == MZ_IN_ASCII else seq.numel() * 32
     span = k + w - 1
@@ -177,7 +182,7 @@ def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, ki
         ws = _ws(mz_workspace_bytes(n, k, w, kind), dev)
     nreads = 0 if read_off is None else read_off.numel() - 1
     mi = MzIn(kind, _ptr(seq), _ptr(invalid), n, _ptr(read_off), nreads, pos_base, win_lo, win_hi)
-    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count))
+    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count), _ptr(out_items))
     _check(_mz_extract_path(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
                             _stream(stream), path), "mz_extract_ex")
     return out_hash, out_pos, d_count
@@ -216,6 +221,27 @@ def seedtable_build(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *
         ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
     _check(_st_build(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out), _ptr(pos_out),
                      _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build")
+    return offsets, pos_out, fp_out
+
+
+def seedtable_build_items(items: torch.Tensor, hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *,
+                          m: int | None = None, d_m: torch.Tensor | None = None, with_fp: bool = True,
+                          offsets: torch.Tensor | None = None, pos_out: torch.Tensor | None = None,
+                          fp_out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """seedtable_build from mz_extract_ex's packed items (out_items) beside hash/pos."""
+    if m is None:
+        m = hash_.numel()
+    dev = hash_.device
+    if offsets is None:
+        offsets = torch.empty((1 << bits) + 1, dtype=torch.uint64, device=dev)
+    if pos_out is None:
+        pos_out = torch.empty(max(1, m), dtype=torch.uint64, device=dev)
+    if fp_out is None and with_fp:
+        fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    if ws is None:
+        ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _check(_st_build_items(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out),
+                           _ptr(pos_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build_items")
     return offsets, pos_out, fp_out
 
 

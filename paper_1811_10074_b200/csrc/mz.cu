@@ -77,6 +77,7 @@ struct MzArgs {
   int k, w, raw, canon;      // key mode: raw code (R4) / canonical strand (R32)
   uint64_t* out_hash;
   uint64_t* out_pos;
+  uint64_t* out_items;       // optional packed seed-table items (fp << 32 | pos mod 2^32)
   uint64_t capacity;
   uint64_t* d_count;
   uint64_t* status;          // look-back tile status [ntiles]
@@ -89,6 +90,13 @@ struct MzArgs {
 // read-start search to the reads of one 8 kbp block (a few loads instead of ~20 dependent ones)
 constexpr int kRidxShift = 13;
 
+// packed seed-table item of a record (seedtable_build_items): the fingerprint (the top 32 bits
+// of the 2k-bit key, R21) over the position mod 2^32
+__device__ __forceinline__ uint64_t item_of(uint64_t h, int k, uint64_t pos) {
+  const int b = 2 * k;
+  const uint32_t f = b >= 32 ? (uint32_t)(h >> (b - 32)) : (uint32_t)(h << (32 - b));
+  return ((uint64_t)f << 32) | (uint32_t)pos;
+}
 __device__ __forceinline__ uint64_t ldw(const MzArgs& a, int64_t i) {
   return (i >= 0 && (uint64_t)i < a.nwords) ? __ldg(a.words + i) : 0ull;
 }
@@ -544,8 +552,10 @@ __device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, in
     const int slot_all = list[i];
     const int sub = slot_all / NS, slot = slot_all - sub * NS;
     const int64_t q = super_lo + (int64_t)sub * a.tw - 1 + slot;
-    a.out_hash[oo] = key_at<H64>(a, q);
+    const uint64_t h = key_at<H64>(a, q);
+    a.out_hash[oo] = h;
     a.out_pos[oo] = a.pos_base + (uint64_t)q;
+    if (a.out_items) a.out_items[oo] = item_of(h, a.k, a.pos_base + (uint64_t)q);
   }
 }
 
@@ -711,8 +721,10 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
     for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * G::TPB;
       if (i < lim) {
-        a.out_hash[base + i] = key_from_words<H64, KK, CN ? 1 : 0>(a, q[u], A[u], B[u]);
+        const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, q[u], A[u], B[u]);
+        a.out_hash[base + i] = h;
         a.out_pos[base + i] = a.pos_base + (uint64_t)q[u];
+        if (a.out_items) a.out_items[base + i] = item_of(h, KK ? KK : a.k, a.pos_base + (uint64_t)q[u]);
       }
     }
   }
@@ -1121,6 +1133,7 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   a.canon = keymode == MZ_KEY_CANON || keymode == MZ_KEY_CANON_RAW;
   a.out_hash = out->hash;
   a.out_pos = out->pos;
+  a.out_items = out->items;
   a.capacity = out->capacity;
   a.d_count = out->d_count;
   return launch_mz(a, path, st);

@@ -222,9 +222,9 @@ __device__ __forceinline__ uint64_t make_item(const NIn<IN, T>& r, uint32_t j, i
     uint32_t f;
     if constexpr (IN == kInHashPos) f = fingerprint(r.a[j], k);
     else f = r.a[j];
-    const uint64_t pr = r.p[j] - p0;
-    bad |= (pr >> 32) != 0;
-    return ((uint64_t)f << 32) | (uint32_t)pr;
+    const uint64_t pj = r.p[j];
+    bad |= ((pj - p0) >> 32) != 0;
+    return ((uint64_t)f << 32) | (uint32_t)pj;  // the low 32 bits of the position (see put)
   }
 }
 
@@ -463,10 +463,12 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       } else if (dfp) {
         const uint32_t d = (uint32_t)(v >> dsh) & dmask;
         dfp[d][g] = (uint32_t)(v >> 32);  // a plain store: over NVLink when the buffer is a peer's
-        dpos[d][g] = p0 + (uint32_t)v;
+        dpos[d][g] = p0 + (uint32_t)((uint32_t)v - (uint32_t)p0);
       } else {
         static_cast<uint32_t*>(a_out)[g] = (uint32_t)(v >> 32);
-        p_out[g] = p0 + (uint32_t)v;
+        // the item holds pos mod 2^32; pos - p0 < 2^32 (the narrow precondition), so
+        // pos = p0 + ((pos - p0) mod 2^32)
+        p_out[g] = p0 + (uint32_t)((uint32_t)v - (uint32_t)p0);
       }
     };
     if (nvalid == (uint32_t)T) {
@@ -764,7 +766,8 @@ int launch_nsweep_cfg(int cfg, const void* a_in, const uint64_t* p_in, void* a_o
 // (packed u64 items, ctl[0] == 1) and the wide one (u32 + u64 entries, ctl[0] == 0); see
 // ctl_kernel.  After the call s.totals holds the digit totals of the LAST pass.
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
-                int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st) {
+                int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st,
+                const uint64_t* items = nullptr) {
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
   const uint64_t nch = (m + s.chunk - 1) / s.chunk;
@@ -787,6 +790,16 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     uint64_t* pk; uint32_t* fo; uint64_t* po;
     pass_out(0, pk, fo, po);
     const int nb = std::min(8, hi_bit - lo_bit);
+    if (items) {
+      // pre-packed items (mz_extract_ex's out->items, positions ascending): pass 0 is an
+      // ordinary 8-byte item pass; the hash/pos arrays serve only the wide path
+      rc = count_pass<2>(items, d_m, m, k, lo_bit, nb, nch, s, 1, st);
+      if (rc) return rc;
+      const int tma_it = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
+      rc = npass == 1 ? launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
+                      : launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_it, st);
+      if (rc) return rc;
+    } else {
     rc = from_hash ? count_pass<0>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st)
                    : count_pass<1>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st);
     if (rc) return rc;
@@ -798,6 +811,7 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
                       : launch_nsweep_cfg<kInFpPos, kOutPk>(ipt_first, keys, pos, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_in, st);
     }
     if (rc) return rc;
+    }
   }
   // ---- wide path: every pass (gated off when the narrow path holds); the same ranking and
   // staging as the narrow passes with (u32 fp, u64 position) entries (nsweep_kernel WD)
@@ -887,9 +901,9 @@ MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
   return z.used;
 }
 
-MZS_API int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,
-                            int bucket_bits, uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out, void* ws,
-                            size_t ws_bytes, void* stream) {
+static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                                const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out,
+                                uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream) {
   if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
   if (!offsets || (m && (!hash || !pos || !pos_out))) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
@@ -915,9 +929,24 @@ MZS_API int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t 
   if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
-  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st);
+  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items);
   if (rc) return rc;
   return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st);
+}
+
+MZS_API int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,
+                            int bucket_bits, uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out, void* ws,
+                            size_t ws_bytes, void* stream) {
+  return seedtable_build_impl(nullptr, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, pos_out, ws, ws_bytes,
+                              stream);
+}
+
+MZS_API int seedtable_build_items(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                                  const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out,
+                                  uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream) {
+  if (m && !items) return SLSUM_EINVAL;
+  return seedtable_build_impl(items, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, pos_out, ws, ws_bytes,
+                              stream);
 }
 
 MZS_API int seedtable_count(const uint64_t* hash, uint64_t m, const uint64_t* d_m, int k, int bucket_bits,

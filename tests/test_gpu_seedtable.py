@@ -218,3 +218,38 @@ def test_partition_p2p_rejects_wide_spans():
     b = torch.empty(100, dtype=torch.uint64, device="cuda")
     rc = P.seedtable_partition_p2p(kt, pt, 19, 24, [b.data_ptr()] * 2, [b.data_ptr()] * 2, [0, 0])
     assert rc == P.SLSUM_EUNSUPPORTED
+
+
+def _fp_np(h, k):
+    b = 2 * k
+    h = h.astype(np.uint64)
+    return (h >> np.uint64(b - 32)) if b >= 32 else (h << np.uint64(32 - b)) & np.uint64(0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("k,pos_base,path", [(19, 0, 0), (15, 0, 0), (19, (1 << 32) - 300_000, 0),
+                                             (15, (1 << 33) + 5, 1), (22, 7, 0)])
+def test_items_path_vs_oracle(k, pos_base, path):
+    """mz_extract_ex's packed items (fp << 32 | pos mod 2^32) and seedtable_build_items: the
+    items match their definition, and the table built from them equals the oracle's and
+    seedtable_build's -- also when the positions cross a multiple of 2^32."""
+    w, bits = 10, 24
+    seq = G.C3(n=700_000).ascii(0, 600_000)
+    st = torch.from_numpy(seq).cuda()
+    cap = 200_000
+    items = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    h, p, c = P.mz_extract_ex(st, k, w, pos_base=pos_base, capacity=cap, out_items=items, path=path)
+    torch.cuda.synchronize()
+    m = int(c.view(torch.int64).item())
+    hk, pp = h[:m].cpu().numpy(), p[:m].cpu().numpy()
+    it = items[:m].cpu().numpy()
+    want_it = (_fp_np(hk, k) << np.uint64(32)) | (pp & np.uint64(0xFFFFFFFF))
+    assert np.array_equal(it, want_it)
+    wk, wp = O.mz(seq, k, w, pos_base=pos_base)
+    assert np.array_equal(hk, wk) and np.array_equal(pp, wp)
+    wo, wf, wpos = O.seedtable(wk, wp, k, bits)
+    for d_m in (None, c):
+        off, po, fp = P.seedtable_build_items(items, h, p, k, bits, m=(m if d_m is None else cap), d_m=d_m)
+        torch.cuda.synchronize()
+        assert np.array_equal(off.cpu().numpy(), wo)
+        assert np.array_equal(po[:m].cpu().numpy(), wpos)
+        assert np.array_equal(fp[:m].cpu().numpy(), wf)
