@@ -576,6 +576,13 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 11) return launch_generic_warp<Op, 11, B4 ? 44 : 22>(xv, yv, n, w, st);
     if (w == 13) return launch_generic_warp<Op, 13, B4 ? 52 : 26>(xv, yv, n, w, st);
     if (w == 15) return launch_generic_warp<Op, 15, B4 ? 60 : 30>(xv, yv, n, w, st);
+    if (w == 20) return launch_generic_warp<Op, 20, 20>(xv, yv, n, w, st);
+    if (w == 24) return launch_generic_warp<Op, 24, 24>(xv, yv, n, w, st);
+    if (w == 28) return launch_generic_warp<Op, 28, 28>(xv, yv, n, w, st);
+    if (w == 18) return launch_generic_warp<Op, 18, B4 ? 36 : 18>(xv, yv, n, w, st);
+    if (w == 22) return launch_generic_warp<Op, 22, B4 ? 44 : 22>(xv, yv, n, w, st);
+    if (w == 26) return launch_generic_warp<Op, 26, B4 ? 52 : 26>(xv, yv, n, w, st);
+    if (w == 30) return launch_generic_warp<Op, 30, B4 ? 60 : 30>(xv, yv, n, w, st);
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);

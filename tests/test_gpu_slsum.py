@@ -16,7 +16,7 @@ OPS = [(P.SLSUM_MIN_U32, O.MIN_U32), (P.SLSUM_MAX_U32, O.MAX_U32), (P.SLSUM_ADD_
        (P.SLSUM_ADD_F32, O.ADD_F32), (P.SLSUM_AFFINE_U32X2, O.AFFINE_U32X2), (P.SLSUM_MIN_U64, O.MIN_U64),
        (P.SLSUM_CONCAT_U32X2, O.CONCAT_U32X2)]
 PAIR_OPS = (P.SLSUM_AFFINE_U32X2, P.SLSUM_CONCAT_U32X2)    # (n, 2) uint32, not commutative
-WS = [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 31, 32, 33, 64, 100, 255, 256, 1000, 1024]
+WS = [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 20, 22, 24, 26, 28, 30, 31, 32, 33, 64, 100, 255, 256, 1000, 1024]
 
 
 def _input(op, n, rng):
