@@ -18,14 +18,14 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_1811_10074_b200")
 
 
-def _bench_path(seq, n, k, w, cap, read_off=None):
-    """bench.py's step: mz_encode + mz_extract_ex(PACKED2, invalid bitmap, d_count)."""
+def _bench_path(seq, n, k, w, cap, read_off=None, items=None):
+    """bench.py's step: mz_encode + mz_extract_ex(PACKED2, invalid bitmap, d_count[, items])."""
     nw = (n + 31) // 32
     words = torch.empty(nw + 1, dtype=torch.uint64, device="cuda")
     inval = torch.empty(nw + 1, dtype=torch.uint32, device="cuda")
     P.mz_encode(seq, words, inval)
     h, p, c = P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, read_off=read_off,
-                              capacity=cap)
+                              capacity=cap, out_items=items)
     return words, inval, h, p, c
 
 
@@ -42,10 +42,12 @@ def test_c3_bench_path_and_table_full_size_sampled():
     seq = D.c3_ascii(c3)
     nwin = n - (k + w - 1) + 1
     cap = int(0.25 * nwin) + 1024            # bench.py's capacity rule
-    _, _, h, p, c = _bench_path(seq, n, k, w, cap)
+    items = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    _, _, h, p, c = _bench_path(seq, n, k, w, cap, items=items)
     del seq
-    # seed table as bench.py builds it: capacity-sized inputs, device count
-    offsets, pos_out, fp_out = P.seedtable_build(h, p, k, bits, m=cap, d_m=c)
+    # seed table as bench.py builds it: from the packed items, capacity-sized inputs, device count
+    offsets, pos_out, fp_out = P.seedtable_build_items(items, h, p, k, bits, m=cap, d_m=c)
+    del items
     torch.cuda.synchronize()
     m = int(c.item())
     assert m <= cap and 0.176 < m / nwin < 0.186
