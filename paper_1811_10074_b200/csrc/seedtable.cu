@@ -155,8 +155,9 @@ __device__ unsigned long long g_prof[8];
 // ---------------------------------------------------------------- narrow passes (packed items)
 // When every position of the call lies in [pos0, pos0 + 2^32), pos0 = pos[0] (one
 // mz_extract_ex call on < 2^32 bases always qualifies), an entry travels between passes as
-// ONE u64 item = (fp << 32) | (pos - pos0): 8 B per entry per pass instead of 12, one load
-// and one store.  ctl_kernel makes the decision from pos[0] and pos[m-1]; the first narrow
+// ONE u64 item = (fp << 32) | (pos mod 2^32): 8 B per entry per pass instead of 12, one load
+// and one store; the last pass restores pos = pos0 + ((lo - pos0) mod 2^32), exact because
+// pos - pos0 < 2^32 (so items written elsewhere, e.g. by mz_extract_ex, need no common base).  ctl_kernel makes the decision from pos[0] and pos[m-1]; the first narrow
 // downsweep re-checks every entry and, on any violation (unsorted input), switches ctl[0]
 // to the wide path, whose kernels are enqueued behind it and then redo the sort.
 //
