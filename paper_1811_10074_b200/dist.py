@@ -55,6 +55,20 @@ def plan_reads(read_off, nranks: int) -> list[tuple[int, int]]:
     return [(cuts[g], max(cuts[g], cuts[g + 1])) for g in range(nranks)]
 
 
+def plan_slsum(n: int, w: int, nranks: int, align: int = 4) -> list[tuple[int, int, int, int]]:
+    """C2 sliding sums across ranks: rank g owns outputs [o_a, o_b) of the
+    n - w + 1 and reads inputs [o_a, o_b + w - 1) -- a w-1 element halo, no collective.
+    Cuts are rounded down to `align` elements (16-byte vectors for 4-byte types).  Returns
+    [(o_a, o_b, in_lo, in_hi)] per rank; concatenating the ranks' outputs gives y."""
+    nout = max(0, n - w + 1)
+    cuts = [0] + [(nout * g // nranks) // align * align for g in range(1, nranks)] + [nout]
+    out = []
+    for g in range(nranks):
+        a, b = cuts[g], max(cuts[g], cuts[g + 1])
+        out.append((a, b, a, b + w - 1 if b > a else a))
+    return out
+
+
 # ---------------------------------------------------------------- local phases
 class Phases:
     """Local seed-table phases on one rank (see include/mzslsum.h)."""

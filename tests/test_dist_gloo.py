@@ -187,3 +187,20 @@ def test_plan_reads_balanced():
     assert parts[0][0] == 0 and parts[-1][1] == 10_000
     sizes = [int(c4.read_off[b] - c4.read_off[a]) for a, b in parts]
     assert max(sizes) < 1.2 * (c4.n / 8)
+
+
+def test_plan_slsum_shards_concatenate():
+    """C2 sharding: every rank's slice, summed by the oracle on its own input
+    range (halo w-1), concatenates to the single-process result."""
+    from paper_1811_10074_b200 import dist as D
+    rng = np.random.default_rng(8)
+    for n, w, G in [(10_000, 4, 8), (10_000, 1000, 4), (5000, 17, 3), (64, 64, 2), (100, 3, 8)]:
+        x = rng.integers(0, 2 ** 32, size=n, dtype=np.uint64).astype(np.uint32)
+        want = O.slsum(O.MIN_U32, w, x)
+        parts = []
+        for a, b, lo, hi in D.plan_slsum(n, w, G):
+            assert a % 4 == 0 or a == 0
+            ys = O.slsum(O.MIN_U32, w, x[lo:hi]) if hi > lo else np.zeros(0, np.uint32)
+            assert len(ys) == b - a
+            parts.append(ys)
+        assert np.array_equal(np.concatenate(parts), want)
