@@ -186,6 +186,12 @@ size_t mz_workspace_bytes(uint64_t n, int k, int w, int kind);
 /* asynchronous extraction on `stream`. */
 int mz_extract_ex(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out,
                   void* ws, size_t ws_bytes, void* stream);
+/* mz_extract_ex with the kernel family forced (a test hook: both families compute the same
+ * output, bit for bit).  path 0 = automatic (what mz_extract_ex does: the compile-time-w fast
+ * kernel for w <= 16 and 2k <= 50, else the generic one); path 1 = the generic kernel
+ * (block-wide segmented S/P scans, any w <= 1024, any k).  Any other value is treated as 1. */
+int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out,
+                    void* ws, size_t ws_bytes, void* stream, int path);
 /* BASELINE shape: ASCII input, hashed keys, one segment, pos_base 0, default stream.
  * Synchronous; returns SLSUM_ECAPACITY if the count exceeds out->capacity
  * (*out->d_count then holds the required count). */
@@ -212,7 +218,9 @@ int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const
  * items[i] = fp(hash[i]) << 32 | (pos[i] mod 2^32) and positions ascending (as mz_extract_ex
  * writes them).  hash and pos are still read: pos[0] and pos[m-1] decide the packed path,
  * and the wide path (positions spanning >= 2^32) sorts from hash/pos.  Same workspace and
- * output as seedtable_build. */
+ * output as seedtable_build.  PRECONDITION: pos ascending.  Unlike seedtable_build, the
+ * per-entry range check is not done here (the items already carry pos mod 2^32), so an
+ * unsorted pos gives a wrong table, not a fallback. */
 int seedtable_build_items(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
                           const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets,
                           uint32_t* fp_out, uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream);
@@ -242,7 +250,11 @@ int seedtable_partition(const uint64_t* hash, const uint64_t* pos, uint64_t m, c
  *   memory over NVLink), starting at peer_base[o], the number of entries for owner o held by
  *   the senders of lower rank.  peer_fp/peer_pos/peer_base are HOST arrays of nranks values.
  *   Requires nranks >= 2 and pos ascending with pos[m-1] - pos[0] < 2^32 (one shard of < 4.29
- *   Gbases); returns SLSUM_EUNSUPPORTED otherwise (use partition + NCCL all_to_all).  Reads the
+ *   Gbases); returns SLSUM_EUNSUPPORTED otherwise (use partition + NCCL all_to_all).  The span
+ *   is checked from pos[0] and pos[m-1] before any write; an unsorted pos is detected by the
+ *   write pass itself, which then also returns SLSUM_EUNSUPPORTED, but only after it has
+ *   written wrong entries into the peers' buffers: the caller must then discard them and
+ *   fall back on every rank.  Reads the
  *   device count and two positions (a short synchronization), then runs asynchronously and
  *   synchronizes the stream before returning.  The caller barriers across ranks before the
  *   owners read their buffers. */

@@ -173,12 +173,25 @@ def hash_array(x: np.ndarray, b: int) -> np.ndarray:
 
 
 def mz(seq, k: int, w: int, read_off=None, keymode: int = KEY_HASH, pos_base: int = 0,
-       win_lo: int = 0, win_hi: int = 2 ** 64 - 1):
-    """Minimizers: returns (key uint64[M], pos uint64[M]) by ascending pos."""
+       win_lo: int = 0, win_hi: int = 2 ** 64 - 1, cap: int | None = None):
+    """Minimizers: returns (key uint64[M], pos uint64[M]) by ascending pos.
+
+    `cap` (marshalling only): when given, the output arrays are allocated with that many
+    entries and orc_mz runs once; if the count exceeds it, it runs again with the exact
+    count.  Without it, a counting call precedes the filling call."""
     s = as_bytes(seq)
     ro = None if read_off is None else np.ascontiguousarray(read_off, dtype=np.uint64)
     nreads = 0 if ro is None else len(ro) - 1
     L = lib()
+    if cap is not None:
+        key = np.empty(max(1, cap), np.uint64)
+        pos = np.empty(max(1, cap), np.uint64)
+        cnt = L.orc_mz(_p(s), len(s), k, w, _p(ro), nreads, keymode, pos_base, win_lo, win_hi,
+                       _p(key), _p(pos), cap)
+        if cnt < 0:
+            raise ValueError(f"orc_mz: error {cnt}")
+        if cnt <= cap:
+            return key[:cnt], pos[:cnt]
     cnt = L.orc_mz(_p(s), len(s), k, w, _p(ro), nreads, keymode, pos_base, win_lo, win_hi, None, None, 0)
     if cnt < 0:
         raise ValueError(f"orc_mz: error {cnt}")

@@ -115,6 +115,24 @@ def _ptr(t: torch.Tensor | None):
     return t.data_ptr()
 
 
+def _need(t: torch.Tensor | None, name: str, dtype, numel: int, allow_none: bool = False) -> None:
+    """Argument check before a raw device pointer crosses the ABI: the kernels trust sizes."""
+    if t is None:
+        if allow_none:
+            return
+        raise ValueError(f"{name} is required")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if t.numel() < numel:
+        raise ValueError(f"{name}: {t.numel()} elements, at least {numel} needed")
+
+
+# element layout of each slsum op: (dtype, values per element)
+OP_LAYOUT = {SLSUM_MIN_U32: (torch.uint32, 1), SLSUM_MAX_U32: (torch.uint32, 1), SLSUM_ADD_U32: (torch.uint32, 1),
+             SLSUM_ADD_F32: (torch.float32, 1), SLSUM_AFFINE_U32X2: (torch.uint32, 2),
+             SLSUM_MIN_U64: (torch.uint64, 1), SLSUM_CONCAT_U32X2: (torch.uint32, 2)}
+
+
 def _stream(stream: torch.cuda.Stream | None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
@@ -129,10 +147,17 @@ def slsum_run(op: int, w: int, x: torch.Tensor, y: torch.Tensor | None = None, p
               stream=None) -> torch.Tensor:
     """y_i = x_i (+) ... (+) x_{i+w-1} on the device.  AFFINE_U32X2 and CONCAT_U32X2 take x of
     shape (n, 2)."""
+    if op not in OP_LAYOUT:
+        raise ValueError(f"unknown op {op}")
+    dt, per = OP_LAYOUT[op]
+    if x.dtype != dt or tuple(x.shape[1:]) != ((per,) if per > 1 else ()):
+        raise ValueError(f"op {op} takes x of dtype {dt} and shape (n{', %d' % per if per > 1 else ''}); "
+                         f"got {x.dtype} {tuple(x.shape)}")
     n = x.shape[0]
     nout = max(0, n - w + 1)
     if y is None:
         y = torch.empty((nout,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    _need(y, "y", dt, nout * per)
     _check(_slsum_run_ex(op, w, _ptr(x), _ptr(y), n, path, _stream(stream)), "slsum_run_ex")
     return y
 
@@ -146,6 +171,9 @@ def mz_encode(seq: torch.Tensor, words: torch.Tensor | None = None, invalid: tor
         words = torch.empty(nw, dtype=torch.uint64, device=seq.device)
     if invalid is None:
         invalid = torch.empty(nw, dtype=torch.uint32, device=seq.device)
+    _need(seq, "seq", torch.uint8, n)
+    _need(words, "words", torch.uint64, nw)
+    _need(invalid, "invalid", torch.uint32, nw)
     _check(_mz_encode(_ptr(seq), n, _ptr(words), _ptr(invalid), _stream(stream)), "mz_encode")
     return words, invalid
 
@@ -181,10 +209,25 @@ def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, ki
     if ws is None:
         ws = _ws(mz_workspace_bytes(n, k, w, kind), dev)
     nreads = 0 if read_off is None else read_off.numel() - 1
+    if kind == MZ_IN_ASCII:
+        _need(seq, "seq", torch.uint8, n)
+    else:
+        _need(seq, "seq (packed words)", torch.uint64, (n + 31) // 32)
+        _need(invalid, "invalid", torch.uint32, (n + 31) // 32, allow_none=True)
+    for name, t in (("out_hash", out_hash), ("out_pos", out_pos), ("out_items", out_items)):
+        _need(t, name, torch.uint64, capacity, allow_none=name == "out_items")
+    _need(d_count, "d_count", torch.uint64, 1)
+    _need(read_off, "read_off", torch.uint64, 2, allow_none=True)
+    if ws.numel() < mz_workspace_bytes(n, k, w, kind):
+        raise ValueError("ws smaller than mz_workspace_bytes")
     mi = MzIn(kind, _ptr(seq), _ptr(invalid), n, _ptr(read_off), nreads, pos_base, win_lo, win_hi)
     mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count), _ptr(out_items))
-    _check(_mz_extract_path(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
-                            _stream(stream), path), "mz_extract_ex")
+    if path == 0:      # the declared entry point (automatic kernel choice)
+        _check(_mz_extract_ex(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
+                              _stream(stream)), "mz_extract_ex")
+    else:              # test hook: force the generic kernel (include/mzslsum.h mz_extract_path)
+        _check(_mz_extract_path(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
+                                _stream(stream), path), "mz_extract_path")
     return out_hash, out_pos, d_count
 
 
@@ -203,6 +246,18 @@ def seedtable_workspace_bytes(m: int, bits: int) -> int:
     return int(_st_ws(m, bits))
 
 
+def _table_checks(hash_, pos, m, d_m, bits, offsets, pos_out, fp_out, ws):
+    _need(hash_, "hash", torch.uint64, m)
+    _need(pos, "pos", torch.uint64, m)
+    _need(d_m, "d_m", torch.uint64, 1, allow_none=True)
+    if 1 <= bits <= 30:                      # other values are the library's EINVAL to report
+        _need(offsets, "offsets", torch.uint64, (1 << bits) + 1)
+    _need(pos_out, "pos_out", torch.uint64, m)
+    _need(fp_out, "fp_out", torch.uint32, m, allow_none=True)
+    if 1 <= bits <= 30 and ws.numel() < seedtable_workspace_bytes(max(1, m), bits):
+        raise ValueError("ws smaller than seedtable_workspace_bytes")
+
+
 def seedtable_build(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *, m: int | None = None,
                     d_m: torch.Tensor | None = None, with_fp: bool = True, offsets: torch.Tensor | None = None,
                     pos_out: torch.Tensor | None = None, fp_out: torch.Tensor | None = None,
@@ -219,6 +274,7 @@ def seedtable_build(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *
         fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
     if ws is None:
         ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _table_checks(hash_, pos, m, d_m, bits, offsets, pos_out, fp_out, ws)
     _check(_st_build(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out), _ptr(pos_out),
                      _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build")
     return offsets, pos_out, fp_out
@@ -240,6 +296,8 @@ def seedtable_build_items(items: torch.Tensor, hash_: torch.Tensor, pos: torch.T
         fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
     if ws is None:
         ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _table_checks(hash_, pos, m, d_m, bits, offsets, pos_out, fp_out, ws)
+    _need(items, "items", torch.uint64, m)
     _check(_st_build_items(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out),
                            _ptr(pos_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build_items")
     return offsets, pos_out, fp_out
@@ -265,12 +323,20 @@ def seedtable_lookup(qkey: torch.Tensor, k: int, bits: int, offsets: torch.Tenso
         d_total = torch.zeros(1, dtype=torch.uint64, device=dev)
     if ws is None:
         ws = _ws(seedtable_lookup_workspace_bytes(max(1, nq)), dev)
+    _need(qkey, "qkey", torch.uint64, nq)
+    _need(d_nq, "d_nq", torch.uint64, 1, allow_none=True)
+    _need(hit_off, "hit_off", torch.uint64, nq + 1)
+    _need(fp, "fp", torch.uint32, 0)
+    _need(pos_tab, "pos_tab", torch.uint64, 0)
+    if 1 <= bits <= 30:
+        _need(offsets, "offsets", torch.uint64, (1 << bits) + 1)
     if hit_cap is None:
         _check(_st_lk(_ptr(qkey), nq, _ptr(d_nq), k, bits, _ptr(offsets), _ptr(fp), _ptr(pos_tab), _ptr(hit_off),
                       None, 0, _ptr(d_total), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_lookup")
         hit_cap = int(d_total.view(torch.int64).item())
     if hit_pos is None:
         hit_pos = torch.empty(max(1, hit_cap), dtype=torch.uint64, device=dev)
+    _need(hit_pos, "hit_pos", torch.uint64, hit_cap)
     _check(_st_lk(_ptr(qkey), nq, _ptr(d_nq), k, bits, _ptr(offsets), _ptr(fp), _ptr(pos_tab), _ptr(hit_off),
                   _ptr(hit_pos), hit_cap, _ptr(d_total), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_lookup")
     return hit_off, hit_pos, d_total

@@ -1076,9 +1076,14 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
                                          tma_in, s.chunk, 1, reinterpret_cast<uint32_t* const*>(dptr),
                                          reinterpret_cast<uint64_t* const*>(dptr + nranks));
   MZS_LAUNCHED();
-  // the host vectors above were read by the async copies; make them complete before returning
+  // the host vectors above were read by the async copies; make them complete before returning.
+  // The downsweep re-checks every entry against the narrow range and clears ctl[0] on a
+  // violation (unsorted input): the peers' buffers then hold wrong entries, and the caller
+  // must fall back to partition + NCCL (uniformly across ranks).
+  uint64_t narrow = 0;
+  MZS_CUDA(cudaMemcpyAsync(&narrow, s.ctl, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   MZS_CUDA(cudaStreamSynchronize(st));
-  return SLSUM_OK;
+  return narrow ? SLSUM_OK : SLSUM_EUNSUPPORTED;
 }
 
 MZS_API size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bits, int nranks) {

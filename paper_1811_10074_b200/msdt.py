@@ -8,7 +8,8 @@ The tables of this library are bucketed CSRs (include/mzslsum.h, R21):
   * direct mode is the Fig. 1 table: RAW keys with bucket_bits = 2k (k <= 12), so the
     pointer table has 4^k + 1 offsets and an entry's seed is its bucket;
   * hashed mode stores each entry's 32-bit fingerprint as its seed (the table keeps the top 32
-    bits of the 2k-bit hash, not the hash itself), with no pointer table (SPEC's sorted-hash mode).
+    bits of the 2k-bit hash, not the hash itself), with no pointer table (SPEC's sorted-hash mode):
+    entries are written sorted by (seed, position), so the seed column is non-decreasing.
 Readers reject an unknown magic or version.  Host-side I/O only (numpy), not the hot path.
 """
 from __future__ import annotations
@@ -37,7 +38,12 @@ def save(path: str, offsets, fp, pos, k: int, w: int, mode: int) -> None:
             raise ValueError("direct mode needs k <= 12 and 4^k + 1 offsets (bucket_bits = 2k, raw keys)")
         seeds = (fp[:m].astype(np.uint64) >> np.uint64(32 - 2 * k))
     elif mode == MODE_HASHED:
-        seeds = fp[:m].astype(np.uint64)
+        # SPEC's hashed mode lists entries by (seed, position) so a reader can binary-search the
+        # seed column.  The table is in (bucket, position) order and a bucket holds several
+        # fingerprints, so sort stably by the fingerprint: positions stay ascending per seed.
+        o = np.argsort(fp[:m], kind="stable")
+        seeds = fp[:m][o].astype(np.uint64)
+        pos = pos[:m][o]
     else:
         raise ValueError(f"unknown mode {mode}")
     with open(path, "wb") as f:

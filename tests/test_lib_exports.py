@@ -55,3 +55,31 @@ def test_argument_errors_are_rejected_before_any_launch():
     assert lib.slsum_run_ex(0, 0, None, None, 10, 0, None) == -1      # w = 0
     assert lib.slsum_run_ex(99, 3, None, None, 10, 0, None) == -1     # bad op
     assert lib.slsum_run_ex(0, 3, None, None, 2, 0, None) == 0        # n < w: zero outputs
+
+
+def test_binding_rejects_mis_sized_buffers_before_the_abi():
+    """The Python binding checks dtypes and sizes before a raw device pointer crosses the ABI
+    (the kernels trust them).  The checks run before any device use, so CPU tensors serve."""
+    import pytest
+    import torch
+    P = __import__("paper_1811_10074_b200")
+    L = P._lib
+    x32 = torch.zeros(100, dtype=torch.uint32)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # MIN_U64 on a uint32 tensor
+        L.slsum_run(L.SLSUM_MIN_U64, 4, x32)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # a pair op on a 1-D tensor
+        L.slsum_run(L.SLSUM_AFFINE_U32X2, 4, x32)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # y too short
+        L.slsum_run(L.SLSUM_MIN_U32, 4, x32, y=torch.zeros(10, dtype=torch.uint32))
+    seq = torch.zeros(1000, dtype=torch.uint8)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # capacity beyond out_hash
+        L.mz_extract_ex(seq, 15, 10, capacity=500, out_hash=torch.zeros(10, dtype=torch.uint64))
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # items shorter than capacity
+        L.mz_extract_ex(seq, 15, 10, capacity=500, out_items=torch.zeros(10, dtype=torch.uint64))
+    h = torch.zeros(100, dtype=torch.uint64)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # pos shorter than m
+        L.seedtable_build(h, torch.zeros(50, dtype=torch.uint64), 19, 24)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # items shorter than m
+        L.seedtable_build_items(torch.zeros(5, dtype=torch.uint64), h, h, 19, 24)
+    with pytest.raises(ValueError, match="dtype|elements|shape"):                     # offsets too short for 2^bits + 1
+        L.seedtable_build(h, h, 19, 10, offsets=torch.zeros(1024, dtype=torch.uint64))

@@ -47,7 +47,20 @@ def test_hashed_round_trip_and_rejects(tmp_path):
     p = tmp_path / "h.msdt"
     M.save(str(p), off, fp, pt, 19, 10, M.MODE_HASHED)
     t = M.load(str(p))
-    assert t["offsets"] is None and np.array_equal(t["seeds"], fp.astype(np.uint64)) and np.array_equal(t["pos"], pt)
+    o = np.argsort(fp, kind="stable")
+    assert t["offsets"] is None and np.array_equal(t["seeds"], fp[o].astype(np.uint64)) and np.array_equal(t["pos"], pt[o])
+    # SPEC's sorted-hash layout: seeds non-decreasing, positions ascending within a seed, and the
+    # entries are exactly the (fingerprint, position) pairs of the records
+    sd, ps = t["seeds"], t["pos"]
+    assert bool(np.all(sd[1:] >= sd[:-1]))
+    same = sd[1:] == sd[:-1]
+    assert bool(np.all(ps[1:][same] > ps[:-1][same]))
+    fpk = np.array([O.fingerprint(int(x), 19) for x in key], dtype=np.uint64)
+    assert sorted(zip(sd.tolist(), ps.tolist())) == sorted(zip(fpk.tolist(), pos.tolist()))
+    # binary search of the seed column finds every record
+    for j in range(0, 3000, 97):
+        lo, hi = np.searchsorted(sd, fpk[j], "left"), np.searchsorted(sd, fpk[j], "right")
+        assert pos[j] in ps[lo:hi]
     raw = bytearray(p.read_bytes())
     bad = tmp_path / "bad.msdt"
     bad.write_bytes(b"XSDT" + raw[4:])
