@@ -45,6 +45,7 @@ SEEDTABLE_BYTES_PER_REC = 8 + 12 + 12   # histogram reads 8 B, the scatter reads
 # algorithmic 32-bit integer operations per base of the fused minimizer kernel
 # (k=19, w=10): roll 3 + H_38 28 + key 2 + three 64-bit minima 12 + change/emit 3
 MZ_INT_OPS_PER_BASE = {19: 48, 15: 30}
+SURVEY_OPS_PER_BASE = {19: 65, 15: 35}
 # N>1 seed-table exchange: "p2p" = partition fused with the all-to-all over symmetric memory
 # (dist.exchange_seedtable_p2p, the product); "nccl" = partition + NCCL all_to_all_single
 EXCHANGE = os.environ.get("MZS_EXCHANGE", "p2p")
@@ -198,12 +199,24 @@ def reference_main(args, rank, world):
 
 
 # ------------------------------------------------------------------ secondary configs
-def _timed(fn, steps, warmup, stream):
-    """Device time per call (CUDA events on the launching stream, synchronize on both sides)."""
+def _nccl_log_env():
+    """NCCL's communicator init lines (rank, nranks, transport) in the run's stderr, so the
+    number of ranks a communicator really spans can be checked from the log."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+
+
+def _timed(fn, steps, warmup, stream, world=1):
+    """Device time per call (CUDA events on the launching stream, synchronize on both sides);
+    at N>1 a barrier before and after, and the maximum over ranks."""
     import torch
+    import torch.distributed as dist
     for _ in range(max(3, warmup)):
         fn()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
@@ -211,49 +224,61 @@ def _timed(fn, steps, warmup, stream):
         fn()
     b.record(stream)
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / steps
+    ms = a.elapsed_time(b) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
 
 
-def bench_c2(args):
-    """C2: slsum_run_ex on 2^28 elements (inputs 1 GiB >> L2, no flush needed)."""
+def bench_c2(args, rank=0, world=1):
+    """C2: slsum_run_ex on 2^28 elements (inputs 1 GiB >> L2, no flush needed).  At N>1 every
+    rank owns a contiguous range of the outputs and reads its inputs with a w-1 halo
+    (dist.plan_slsum; no collective on the data path); each run's time is the max over ranks."""
     import torch
     import paper_1811_10074_b200 as P
+    from paper_1811_10074_b200 import dist as D
     from synthgen import device as SD
     hbm_peak, peak_kind, _ = load_peaks()
     n = 1 << 28
     stream = torch.cuda.current_stream()
-    xu = SD.c2_u32(n)
-    xf = SD.c2_f32(n)
-    yu = torch.empty(n, dtype=torch.uint32, device="cuda")
-    yf = torch.empty(n, dtype=torch.float32, device="cuda")
-    ops = [("MIN_U32", P.SLSUM_MIN_U32, xu, yu), ("ADD_U32", P.SLSUM_ADD_U32, xu, yu),
-           ("ADD_F32", P.SLSUM_ADD_F32, xf, yf)]
+    names = [("MIN_U32", P.SLSUM_MIN_U32), ("ADD_U32", P.SLSUM_ADD_U32), ("ADD_F32", P.SLSUM_ADD_F32)]
     runs, tot_ms = [], 0.0
-    with Clocks(0) as clk:
-        for name, op, x, y in ops:
-            for w in (4, 16, 64, 256, 1024):
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for w in (4, 16, 64, 256, 1024):
+            oa, ob, lo, hi = D.plan_slsum(n, w, world)[rank]
+            xu = SD.c2_u32(hi - lo, lo=lo)
+            xf = SD.c2_f32(hi - lo, lo=lo)
+            yu = torch.empty(max(1, ob - oa), dtype=torch.uint32, device="cuda")
+            yf = torch.empty(max(1, ob - oa), dtype=torch.float32, device="cuda")
+            for name, op in names:
+                x, y = (xf, yf) if op == P.SLSUM_ADD_F32 else (xu, yu)
                 paths = [("generic", P.SLSUM_PATH_GENERIC), ("commutative", P.SLSUM_PATH_COMMUTATIVE),
                          ("scalar_alg1", P.SLSUM_PATH_SCALAR)]
                 if op == P.SLSUM_ADD_U32:   # the invertible op also has the recurrent path (P:L229, NEXT f2)
                     paths.append(("recurrent", P.SLSUM_PATH_RECURRENT))
                 for pname, path in paths:
-                    ms = _timed(lambda: P.slsum_run(op, w, x, y[: n - w + 1], path=path), args.steps, args.warmup,
-                                stream)
+                    ms = _timed(lambda: P.slsum_run(op, w, x, y[: ob - oa], path=path), args.steps, args.warmup,
+                                stream, world)
                     tot_ms += ms
-                    gbs = 8.0 * n / (ms * 1e-3) / 1e9
+                    gbs = 8.0 * n / world / (ms * 1e-3) / 1e9          # per GPU
                     runs.append({"op": name, "w": w, "path": pname, "ms": ms, "gelem_s": n / (ms * 1e-3) / 1e9,
                                  "hbm_gbs": gbs, "hbm_frac": gbs / hbm_peak})
+            del xu, xf, yu, yf
     clk_sum = clk.summary()
+    if rank != 0:
+        return 0
     best = max(runs, key=lambda r: r["hbm_frac"])
     gen = [r for r in runs if r["path"] == "generic"]
     # the headline aggregates the O(1)/O(log w) paths; Alg. 1 is O(w) per output by design
     fast = [r for r in runs if r["path"] != "scalar_alg1"]
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         # the oracle's strict O(wN) left fold on the same 15 (op, w) runs, first 2^23 elements each
         import oracle as O
         ns = 1 << 23
-        xs_u, xs_f = xu[:ns].cpu().numpy(), xf[:ns].cpu().numpy()
+        xs_u, xs_f = SD.c2_u32(ns).cpu().numpy(), SD.c2_f32(ns).cpu().numpy()
         t0 = time.perf_counter()
         for oop, xs in ((O.MIN_U32, xs_u), (O.ADD_U32, xs_u), (O.ADD_F32, xs_f)):
             for w in (4, 16, 64, 256, 1024):
@@ -264,12 +289,13 @@ def bench_c2(args):
     line = {
         "metric": "generic sliding window sums (Eq. 2), Gelem/s",
         "value": len(fast) * n / (sum(r["ms"] for r in fast) * 1e-3) / 1e9,
-        "unit": "Gelem/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup),
+        "unit": "Gelem/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": tot_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/f32",
         "data": "synthetic",
         "config": {"workload": "C2: 2^28 elements x {MIN_U32, ADD_U32, ADD_F32} x w {4..1024} x {generic, commutative,"
                                " scalar (Alg. 1)} (+ recurrent for ADD_U32)",
-                   "step": f"all {len(runs)} runs", "l2": "inputs 1 GiB >> L2; no flush needed"},
+                   "step": f"all {len(runs)} runs", "l2": "inputs 1 GiB >> L2; no flush needed",
+                   "parallelism": f"output ranges over {world} GPUs, w-1 input halo, no collective"},
         "roofline": {"bound": "hbm", "kernel": f"slsum {best['path']} {best['op']} w={best['w']} (best)",
                      "achieved": best["hbm_gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": best["hbm_frac"],
                      "traffic": None, "peak_kind": peak_kind},
@@ -280,18 +306,24 @@ def bench_c2(args):
     return 0
 
 
-def bench_c4(args):
-    """C4: 1M lognormal reads, k=15 w=10; encode + segmented minimizer extraction."""
+def bench_c4(args, rank=0, world=1):
+    """C4: 1M lognormal reads, k=15 w=10; encode + segmented minimizer extraction.  At N>1 every
+    rank takes a contiguous range of reads balanced by bases (dist.plan_reads; windows never
+    cross a read, so no halo and no collective); the time is the max over ranks."""
     import torch
     import paper_1811_10074_b200 as P
+    from paper_1811_10074_b200 import dist as D
     from synthgen import device as SD
     from synthgen import host as H
     hbm_peak, peak_kind, sm_max = load_peaks()
     k, w = 15, 10
     c4 = H.C4()
-    n = c4.n
-    seq = SD.c4_ascii(c4)
-    ro = torch.from_numpy(c4.read_off.astype(np.uint64).view(np.int64)).cuda().view(torch.uint64)
+    n_total = c4.n
+    r0, r1 = D.plan_reads(c4.read_off, world)[rank]
+    base = int(c4.read_off[r0])
+    n = int(c4.read_off[r1]) - base
+    seq = SD.c4_ascii(c4) if world == 1 else SD.c4_ascii_reads(c4, r0, r1)
+    ro = torch.from_numpy((c4.read_off[r0:r1 + 1] - base).astype(np.uint64).view(np.int64)).cuda().view(torch.uint64)
     nw = (n + 31) // 32
     words = torch.empty(nw + 1, dtype=torch.uint64, device="cuda")
     inval = torch.empty(nw + 1, dtype=torch.uint32, device="cuda")
@@ -312,13 +344,13 @@ def bench_c4(args):
         if record:
             e[1].record(stream)
         P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, read_off=ro, capacity=cap,
-                        out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws, keymode=keymode)
+                        out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws, keymode=keymode, pos_base=base)
         if record:
             e[2].record(stream)
             ev.append(e)
 
-    with Clocks(0) as clk:
-        ms = _timed(lambda: step(True), args.steps, args.warmup, stream)
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        ms = _timed(lambda: step(True), args.steps, args.warmup, stream, world)
     m = int(d_count.view(torch.int64).item())
     if m > cap:
         raise RuntimeError(f"capacity {cap} < {m} records")
@@ -330,8 +362,10 @@ def bench_c4(args):
     int_peak = SM_COUNT * INT32_LANES_PER_SM_CLK * sm_mhz * 1e6 / 1e12
     ops = MZ_INT_OPS_PER_BASE[15] * n
     ach = ops / (mz_ms * 1e-3) / 1e12
+    if rank != 0:
+        return 0
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         import oracle as O
         r1 = 2000
         hi = int(c4.read_off[r1])
@@ -342,17 +376,20 @@ def bench_c4(args):
         cpu = {"value": hi / dt / 1e9, "unit": "Gbases/s", "cores": O.num_threads(), "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"first {r1} reads ({hi} bases) of C4 ({dt:.1f} s)"}
     line = {
-        "metric": "minimizer extraction over a long-read batch, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
-        "unit": "Gbases/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "metric": "minimizer extraction over a long-read batch, Gbases/s", "value": n_total / (ms * 1e-3) / 1e9,
+        "unit": "Gbases/s", "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": "C4: 1M reads, lognormal(mean 10 kbp, sd 8 kbp), 10% substitutions"
                                + (" (canonical minimizers)" if args.canonical else ""), "k": k, "w": w,
-                   "bases": n, "reads": c4.nreads, "records": m, "density": m / n,
+                   "bases": n_total, "reads": c4.nreads, "records_rank0": m, "density": m / n,
+                   "parallelism": f"reads balanced by bases over {world} GPUs, no halo, no collective",
                    "l2": f"inputs ({n / 1e9:.1f} GB) >> L2; no flush needed"},
         "roofline": {"bound": "alu", "kernel": "mz_fast_kernel<10,0,15> (a2-a7 fused, read-segmented)",
                      "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": None,
                      "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
-                     "ops_per_base": MZ_INT_OPS_PER_BASE[15], "ms": mz_ms},
+                     "ops_per_base": MZ_INT_OPS_PER_BASE[15], "ms": mz_ms,
+                     "frac_survey_ops": SURVEY_OPS_PER_BASE[15] * n / (mz_ms * 1e-3) / 1e12 / int_peak,
+                     "survey_ops_per_base": SURVEY_OPS_PER_BASE[15]},
         "hbm_step": {"encode_ms": enc_ms, "extract_ms": mz_ms,
                      "encode_frac": n * 1.375 / (enc_ms * 1e-3) / 1e9 / hbm_peak,
                      "extract_frac": (n * 0.375 + m * 16) / (mz_ms * 1e-3) / 1e9 / hbm_peak, "peak": hbm_peak,
@@ -410,10 +447,20 @@ def bench_lookup(args):
         ms = _timed(step, args.steps, args.warmup, stream)
     clk_sum = clk.summary()
     mean_slice = mt / (1 << bits)
-    # algorithmic bytes per query: key 8, two offsets 16, the bucket's fingerprints 4/entry,
-    # its CSR offset written + read 16, and per hit its position read + written 16 -- count
-    # and emit both read key, offsets and fingerprints (2 passes)
-    alg = nq * (2 * (8 + 16 + 4 * mean_slice) + 16) + hits * 16
+    # algorithmic bytes per query (R30): key 8, two offsets 16, its CSR offset written + read 16,
+    # the fingerprints of ITS bucket 4 per entry (the hits are the entries of that slice whose
+    # fingerprint matches, so one scan of the slice is the method's own work), and per hit its
+    # position read + written 16.  Minimizer hashes are skewed low, so the buckets queries fall
+    # in are longer than the mean bucket: the slice lengths are summed over the actual queries.
+    kk = 2 * k
+    qf = (q.view(torch.int64) >> (kk - 32)) if kk >= 32 else ((q.view(torch.int64) << (32 - kk)) & 0xFFFFFFFF)
+    qb = (qf & 0xFFFFFFFF) >> (32 - bits)
+    offl = off.view(torch.int64)
+    qlen = int((offl[qb + 1] - offl[qb]).sum().item())
+    del qf, qb
+    alg = nq * (8 + 16 + 16) + 4 * qlen + hits * 16
+    # the earlier accounting (2 passes over a bucket of the MEAN length), kept for comparison
+    alg_mean = nq * (2 * (8 + 16 + 4 * mean_slice) + 16) + hits * 16
     cpu = None
     if not args.no_cpu_baseline:
         import oracle as O
@@ -438,7 +485,8 @@ def bench_lookup(args):
         "roofline": {"bound": "hbm", "kernel": "lookup_kernel count + emit, scan (one step)",
                      "achieved": alg / (ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                      "frac": alg / (ms * 1e-3) / 1e9 / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                     "algorithmic_bytes": alg},
+                     "algorithmic_bytes": alg, "query_bucket_mean_len": qlen / max(1, nq),
+                     "frac_mean_bucket_model": alg_mean / (ms * 1e-3) / 1e9 / hbm_peak},
         "cpu_baseline": cpu, "clocks": clk_sum, "gpu_launches": 5 * args.steps,
     }
     print(json.dumps(line), flush=True)
@@ -457,12 +505,22 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if args.config in ("c2", "c4", "lookup"):
+    if args.config == "lookup":
         if world > 1 and rank != 0:
-            return 0          # secondary configs are single-GPU measurements
-        return {"c2": bench_c2, "c4": bench_c4, "lookup": bench_lookup}[args.config](args)
+            return 0          # the lookup line is a single-GPU measurement
+        return bench_lookup(args)
+    if args.config in ("c2", "c4"):
+        if world > 1:
+            _nccl_log_env()
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            return {"c2": bench_c2, "c4": bench_c4}[args.config](args, rank, world)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
     dev = torch.device("cuda", local)
     if world > 1:
+        _nccl_log_env()
         dist.init_process_group("nccl", device_id=dev)
     import paper_1811_10074_b200 as P
     from paper_1811_10074_b200 import dist as D
@@ -499,9 +557,10 @@ def main():
             self.inval = torch.empty(nw + 1, dtype=torch.uint32, device=dev)
             self.out_h = torch.empty(cap, dtype=torch.uint64, device=dev)
             self.out_p = torch.empty(cap, dtype=torch.uint64, device=dev)
-            # packed seed-table items written by the minimizer kernel beside (hash, pos):
-            # the table's first radix pass reads 8 B per record instead of 16
-            self.out_i = torch.empty(cap, dtype=torch.uint64, device=dev) if world == 1 else None
+            # packed seed-table items written by the minimizer kernel beside (hash, pos): the
+            # table's first radix pass (N=1) or the fused owner partition (N>1) reads 8 B per
+            # record instead of 16
+            self.out_i = torch.empty(cap, dtype=torch.uint64, device=dev)
             self.d_count = torch.zeros(1, dtype=torch.uint64, device=dev)
             self.mz_ws = torch.empty(P.mz_workspace_bytes(n, k, w, P.MZ_IN_PACKED2), dtype=torch.uint8, device=dev)
             if world == 1:
@@ -509,12 +568,13 @@ def main():
                 self.offsets = torch.empty((1 << bits) + 1, dtype=torch.uint64, device=dev)
                 self.pos_out = torch.empty(cap, dtype=torch.uint64, device=dev)
                 self.fp_out = torch.empty(cap, dtype=torch.uint32, device=dev)
+                self.pos32_out = None   # (e2e) the 32-bit position table, allocated on first use
 
     B0 = Bufs()
     d_count = B0.d_count
     ev = {name: [] for name in ("encode", "extract", "table")}
 
-    def step(seq_dev, record=False, bf=B0):
+    def step(seq_dev, record=False, bf=B0, pos32=False):
         st = torch.cuda.current_stream()
         e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if record else None
         if record:
@@ -528,14 +588,22 @@ def main():
                         keymode=P.MZ_KEY_CANON if args.canonical else P.MZ_KEY_HASH)
         if record:
             e[2].record(st)
-        if world == 1:
+        if world == 1 and pos32:
+            # seedtable_build_items32: positions mod 2^32, exact here (C3 < 2^32 bases)
+            if bf.pos32_out is None:
+                bf.pos32_out = torch.empty(cap, dtype=torch.uint32, device=dev)
+            P.seedtable_build_items32(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count,
+                                      offsets=bf.offsets, pos_out=bf.pos32_out, fp_out=bf.fp_out, ws=bf.st_ws)
+            res = (bf.offsets, bf.pos32_out)
+        elif world == 1:
             P.seedtable_build_items(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count,
                                     offsets=bf.offsets, pos_out=bf.pos_out, fp_out=bf.fp_out, ws=bf.st_ws)
             res = (bf.offsets, bf.pos_out)
         else:
-            m = int(bf.d_count.view(torch.int64).item())
+            # the record count stays on the device (capacity-sized arrays + d_count) up to the
+            # exchange's own host read of the gathered owner counts
             xchg = D.exchange_seedtable_p2p if EXCHANGE == "p2p" else D.exchange_seedtable
-            res = xchg(bf.out_h[:m], bf.out_p[:m], m, k, bits, D.CudaPhases())
+            res = xchg(bf.out_h, bf.out_p, cap, k, bits, D.CudaPhases(d_m=bf.d_count, items=bf.out_i))
         if record:
             e[3].record(st)
             ev["encode"].append((e[0], e[1]))
@@ -644,55 +712,68 @@ def main():
         seqd = [torch.empty_like(seq) for _ in range(nset)]
         del seq
         s_h2d, s_cmp, s_d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-        ev_h2d = [torch.cuda.Event() for _ in range(nset)]
-        ev_cmp = [torch.cuda.Event() for _ in range(nset)]
-        ev_d2h = [torch.cuda.Event() for _ in range(nset)]
-        started = [False] * nset
 
-        def enqueue(b):
-            with torch.cuda.stream(s_h2d):
-                if started[b]:
-                    s_h2d.wait_event(ev_cmp[b])      # set b's input was consumed by its last compute
-                seqd[b].copy_(host_in, non_blocking=True)
-                ev_h2d[b].record(s_h2d)
-            with torch.cuda.stream(s_cmp):
-                s_cmp.wait_event(ev_h2d[b])
-                if started[b]:
-                    s_cmp.wait_event(ev_d2h[b])      # set b's table was read back
-                step(seqd[b], bf=sets[b])
-                host_cnt[b:b + 1].copy_(sets[b].d_count.view(torch.int64), non_blocking=True)
-                ev_cmp[b].record(s_cmp)
-            started[b] = True
+        def e2e_run(pos32: bool):
+            ev_h2d = [torch.cuda.Event() for _ in range(nset)]
+            ev_cmp = [torch.cuda.Event() for _ in range(nset)]
+            ev_d2h = [torch.cuda.Event() for _ in range(nset)]
+            started = [False] * nset
+            esz = 4 if pos32 else 8
+            # pinned host position tables (u32 ones viewed out of the u64 buffers)
+            hpos = [hp.view(torch.uint32)[:cap] if pos32 else hp for hp in host_pos]
 
-        def readback(b):
-            ev_cmp[b].synchronize()                  # the record count decides how much to read back
-            m = int(host_cnt[b].item())
-            with torch.cuda.stream(s_d2h):
-                s_d2h.wait_event(ev_cmp[b])
-                host_off[b].copy_(sets[b].offsets, non_blocking=True)
-                host_pos[b][:m].copy_(sets[b].pos_out[:m], non_blocking=True)
-                ev_d2h[b].record(s_d2h)
-            return 8 * ((1 << bits) + 1) + 8 * m
+            def enqueue(b):
+                with torch.cuda.stream(s_h2d):
+                    if started[b]:
+                        s_h2d.wait_event(ev_cmp[b])      # set b's input was consumed by its last compute
+                    seqd[b].copy_(host_in, non_blocking=True)
+                    ev_h2d[b].record(s_h2d)
+                with torch.cuda.stream(s_cmp):
+                    s_cmp.wait_event(ev_h2d[b])
+                    if started[b]:
+                        s_cmp.wait_event(ev_d2h[b])      # set b's table was read back
+                    step(seqd[b], bf=sets[b], pos32=pos32)
+                    host_cnt[b:b + 1].copy_(sets[b].d_count.view(torch.int64), non_blocking=True)
+                    ev_cmp[b].record(s_cmp)
+                started[b] = True
 
-        ke = max(3, min(args.steps, 6))
-        enqueue(0)                                   # warm-up step (untimed)
-        readback(0)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        bev = torch.cuda.Event(enable_timing=True)
-        a.record(s_h2d)
-        d2h = 0
-        for i in range(ke):
-            enqueue(i % nset)
-            if i > 0:
-                d2h = readback((i - 1) % nset)
-        d2h = readback((ke - 1) % nset)
-        bev.record(s_d2h)
-        torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(bev) / ke
-        e2e = {"value": n_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gbases/s", "h2d_bytes_per_step": n,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
-               "pipeline": f"{nset} buffer sets, streams H2D | compute | D2H; step i's D2H overlaps step i+1"}
+            def readback(b):
+                ev_cmp[b].synchronize()                  # the record count decides how much to read back
+                m = int(host_cnt[b].item())
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_cmp[b])
+                    host_off[b].copy_(sets[b].offsets, non_blocking=True)
+                    src = sets[b].pos32_out if pos32 else sets[b].pos_out
+                    hpos[b][:m].copy_(src[:m], non_blocking=True)
+                    ev_d2h[b].record(s_d2h)
+                return 8 * ((1 << bits) + 1) + esz * m
+
+            ke = max(3, min(args.steps, 6))
+            enqueue(0)                                   # warm-up step (untimed)
+            readback(0)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            bev = torch.cuda.Event(enable_timing=True)
+            a.record(s_h2d)
+            d2h = 0
+            for i in range(ke):
+                enqueue(i % nset)
+                if i > 0:
+                    d2h = readback((i - 1) % nset)
+            d2h = readback((ke - 1) % nset)
+            bev.record(s_d2h)
+            torch.cuda.synchronize()
+            e2e_ms = a.elapsed_time(bev) / ke
+            return {"value": n_total / (e2e_ms * 1e-3) / 1e9, "unit": "Gbases/s", "h2d_bytes_per_step": n,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
+                    "table_positions": "u32 (seedtable_build_items32; exact: C3 has < 2^32 bases)" if pos32
+                    else "u64 (seedtable_build_items)",
+                    "pipeline": f"{nset} buffer sets, streams H2D | compute | D2H; step i's D2H overlaps step i+1"}
+
+        use32 = c3 is not None and n_total < (1 << 32)
+        e2e = e2e_run(pos32=use32)
+        if use32:
+            e2e["pos64"] = e2e_run(pos32=False)    # the same pipeline with the u64 position table
         del host_in, host_off, host_pos, seqd, extra
     elif not args.no_e2e and world > 1:
         # N GPUs: every rank copies its shard's ASCII in (H2D), runs the step (extraction, then
@@ -756,7 +837,11 @@ def main():
                             f"{per_phase_bytes['extract']:.3e} B",
             "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
             "peak_measured": load_int_peak(),
-            "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"]}
+            "ops_per_base": MZ_INT_OPS_PER_BASE.get(k, 48), "ms": phase_ms["extract"],
+            # the same fraction with SURVEY 8(d)'s estimate of the algorithmic work (65 ops/base at
+            # k=19, 35 at k=15) instead of DESIGN.md's count
+            "frac_survey_ops": SURVEY_OPS_PER_BASE.get(k, 65) * n / (phase_ms["extract"] * 1e-3) / 1e12 / int_peak,
+            "survey_ops_per_base": SURVEY_OPS_PER_BASE.get(k, 65)}
     tab_ach = per_phase_bytes["table"] / (phase_ms["table"] * 1e-3) / 1e9
     roof_table = {"bound": "hbm", "kernel": "seed table (3 packed-item LSD radix passes + pointer table), "
                             "from the minimizer kernel's packed items",
@@ -774,10 +859,28 @@ def main():
                 "phase_frac": {kk: per_phase_bytes[kk] / (phase_ms[kk] * 1e-3) / 1e9 / hbm_peak for kk in phase_ms}}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and c3 is not None:
         v, dt, cores, mm = cpu_oracle_run(args.cpu_sample_bases)
         cpu = {"value": v, "unit": "Gbases/s", "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"first {args.cpu_sample_bases} bases of C3, k={k} w={w}: oracle mz + seedtable ({dt:.1f} s)"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # C1 in full: the oracle on all host cores and on one thread (SURVEY 8(d) "a 1-thread run on C1")
+        import oracle as O
+        s1 = H.c1_ascii(n_total)
+        res = {}
+        for nt in (O.num_threads(), 1):
+            prev = O.num_threads()
+            O.set_num_threads(nt)
+            t0 = time.perf_counter()
+            kk_, pp_ = O.mz(s1, k, w)
+            O.seedtable(kk_, pp_, k, bits)
+            res[nt] = time.perf_counter() - t0
+            O.set_num_threads(prev)
+        ncores = max(res)
+        cpu = {"value": n_total / res[ncores] / 1e9, "unit": "Gbases/s", "cores": ncores, "cpu_model": cpu_model(),
+               "kind": "oracle", "sample": f"C1 in full ({n_total} bases): oracle mz + seedtable ({res[ncores]:.2f} s)",
+               "single_thread": {"value": n_total / res[1] / 1e9, "unit": "Gbases/s", "cores": 1,
+                                 "seconds": res[1]}}
 
     if rank == 0:
         line = {

@@ -225,6 +225,14 @@ int seedtable_build_items(const uint64_t* items, const uint64_t* hash, const uin
                           const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets,
                           uint32_t* fp_out, uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream);
 
+/* seedtable_build_items with a 32-bit position table: pos32_out[m] (uint32) receives every
+ * position mod 2^32 -- the positions themselves when they are below 2^32 (one genome of
+ * < 4.29 Gbases per table, e.g. C3), half the bytes of pos_out.  Offsets and fp_out as in
+ * seedtable_build.  Same workspace (seedtable_workspace_bytes). */
+int seedtable_build_items32(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                            const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets,
+                            uint32_t* fp_out, uint32_t* pos32_out, void* ws, size_t ws_bytes, void* stream);
+
 /* Multi-GPU phases (owner(bucket) = bucket >> (bucket_bits - log2 nranks); nranks a
  * power of two; NCCL all_reduce / all_to_all run between these calls):
  *  seedtable_count      counts[2^bits] (uint32) = per-bucket record counts (overwritten).
@@ -263,6 +271,15 @@ int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, uint64_t 
                             int k, int bucket_bits, int nranks, const uint64_t* peer_fp,
                             const uint64_t* peer_pos, const uint64_t* peer_base, void* ws,
                             size_t ws_bytes, void* stream);
+/* seedtable_partition_p2p from the packed items mz_extract_ex wrote (out->items, see
+ *   seedtable_build_items): reads 8 B per entry instead of the 16-byte (hash, pos) pair; pos is
+ *   read only at pos[0] and pos[m-1] (the narrow precondition and the base of the positions).
+ *   PRECONDITION: pos ascending (not re-checked per entry: an unsorted pos gives wrong entries,
+ *   not SLSUM_EUNSUPPORTED).  Same workspace (seedtable_partition_p2p_workspace_bytes). */
+int seedtable_partition_p2p_items(const uint64_t* items, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
+                                  int k, int bucket_bits, int nranks, const uint64_t* peer_fp,
+                                  const uint64_t* peer_pos, const uint64_t* peer_base, void* ws,
+                                  size_t ws_bytes, void* stream);
 size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bits, int nranks);
 int seedtable_finalize(const uint32_t* recv_fp, const uint64_t* recv_pos, uint64_t m_recv,
                        const uint32_t* global_counts, int bucket_bits, int rank, int nranks,

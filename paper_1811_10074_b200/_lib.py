@@ -74,21 +74,26 @@ _st_ws = _sig("seedtable_workspace_bytes", _sz, _u64, _i32)
 _st_build = _sig("seedtable_build", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _st_build_items = _sig("seedtable_build_items", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
                        _vp)
+_st_build_items32 = _sig("seedtable_build_items32", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp,
+                         _sz, _vp)
 _st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
 _st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
 _st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _st_p2p_ws = _sig("seedtable_partition_p2p_workspace_bytes", _sz, _u64, _i32)
 _st_p2p = _sig("seedtable_partition_p2p", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
+_st_p2p_it = _sig("seedtable_partition_p2p_items", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                  _sz, _vp)
 _st_fin_ws = _sig("seedtable_finalize_workspace_bytes", _sz, _u64, _i32, _i32)
 _st_lk_ws = _sig("seedtable_lookup_workspace_bytes", _sz, _u64)
 _st_lk = _sig("seedtable_lookup", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _sz, _vp)
 _st_fin = _sig("seedtable_finalize", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 
 EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_encode", "mz_workspace_bytes",
-           "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_build_items", "seedtable_count",
+           "mz_extract_ex", "mz_extract", "seedtable_workspace_bytes", "seedtable_build", "seedtable_build_items", "seedtable_build_items32", "seedtable_count",
            "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
            "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup",
-           "seedtable_partition_p2p_workspace_bytes", "seedtable_partition_p2p"]
+           "seedtable_partition_p2p_workspace_bytes", "seedtable_partition_p2p", "seedtable_partition_p2p_items",
+           "mz_extract_path"]
 
 
 def strerror(rc: int) -> str:
@@ -252,7 +257,7 @@ def _table_checks(hash_, pos, m, d_m, bits, offsets, pos_out, fp_out, ws):
     _need(d_m, "d_m", torch.uint64, 1, allow_none=True)
     if 1 <= bits <= 30:                      # other values are the library's EINVAL to report
         _need(offsets, "offsets", torch.uint64, (1 << bits) + 1)
-    _need(pos_out, "pos_out", torch.uint64, m)
+    _need(pos_out, "pos_out", torch.uint64, m, allow_none=pos_out is None)
     _need(fp_out, "fp_out", torch.uint32, m, allow_none=True)
     if 1 <= bits <= 30 and ws.numel() < seedtable_workspace_bytes(max(1, m), bits):
         raise ValueError("ws smaller than seedtable_workspace_bytes")
@@ -300,6 +305,30 @@ def seedtable_build_items(items: torch.Tensor, hash_: torch.Tensor, pos: torch.T
     _need(items, "items", torch.uint64, m)
     _check(_st_build_items(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out),
                            _ptr(pos_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build_items")
+    return offsets, pos_out, fp_out
+
+
+def seedtable_build_items32(items: torch.Tensor, hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *,
+                            m: int | None = None, d_m: torch.Tensor | None = None, with_fp: bool = True,
+                            offsets: torch.Tensor | None = None, pos_out: torch.Tensor | None = None,
+                            fp_out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """seedtable_build_items with a uint32 position table (positions mod 2^32; exact below 2^32)."""
+    if m is None:
+        m = hash_.numel()
+    dev = hash_.device
+    if offsets is None:
+        offsets = torch.empty((1 << bits) + 1, dtype=torch.uint64, device=dev)
+    if pos_out is None:
+        pos_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    if fp_out is None and with_fp:
+        fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    if ws is None:
+        ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _table_checks(hash_, pos, m, d_m, bits, offsets, None, fp_out, ws)
+    _need(items, "items", torch.uint64, m)
+    _need(pos_out, "pos_out", torch.uint32, m)
+    _check(_st_build_items32(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out),
+                             _ptr(pos_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build_items32")
     return offsets, pos_out, fp_out
 
 
@@ -370,18 +399,27 @@ def seedtable_partition(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: in
 
 def seedtable_partition_p2p(hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, peer_fp: list[int],
                             peer_pos: list[int], peer_base: list[int], *, m: int | None = None, d_m=None, ws=None,
-                            stream=None) -> int:
+                            stream=None, items: torch.Tensor | None = None) -> int:
     """Partition fused with the all-to-all: entries go straight into the owners' receive
     buffers (device pointers, e.g. peer-mapped symmetric memory).  Returns the status code:
-    SLSUM_OK, or SLSUM_EUNSUPPORTED when the narrow precondition fails (use the NCCL path)."""
+    SLSUM_OK, or SLSUM_EUNSUPPORTED when the narrow precondition fails (use the NCCL path).
+    With `items` (mz_extract_ex's out_items) the pass reads the packed items instead of hash."""
     if m is None:
         m = hash_.numel()
     nranks = len(peer_fp)
+    _need(hash_, "hash", torch.uint64, m)
+    _need(pos, "pos", torch.uint64, m)
+    _need(items, "items", torch.uint64, m, allow_none=True)
+    _need(d_m, "d_m", torch.uint64, 1, allow_none=True)
     if ws is None:
         ws = _ws(_st_p2p_ws(max(1, m), nranks), hash_.device)
     arr = ctypes.c_uint64 * nranks
-    rc = _st_p2p(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, nranks, arr(*peer_fp), arr(*peer_pos),
-                 arr(*peer_base), _ptr(ws), ws.numel(), _stream(stream))
+    if items is not None:
+        rc = _st_p2p_it(_ptr(items), _ptr(pos), m, _ptr(d_m), k, bits, nranks, arr(*peer_fp), arr(*peer_pos),
+                        arr(*peer_base), _ptr(ws), ws.numel(), _stream(stream))
+    else:
+        rc = _st_p2p(_ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, nranks, arr(*peer_fp), arr(*peer_pos),
+                     arr(*peer_base), _ptr(ws), ws.numel(), _stream(stream))
     if rc not in (SLSUM_OK, SLSUM_EUNSUPPORTED):
         _check(rc, "seedtable_partition_p2p")
     return rc

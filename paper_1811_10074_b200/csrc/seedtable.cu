@@ -21,6 +21,9 @@
 namespace mzs {
 namespace {
 
+#ifndef MZS_RANK_SYNCWARP
+#define MZS_RANK_SYNCWARP 1
+#endif
 constexpr int kTPB = 256;
 constexpr int kNW = kTPB / 32;
 
@@ -170,7 +173,7 @@ __device__ unsigned long long g_prof[8];
 // 32 B sectors at run edges are merged in L2 (tools/microbench_radix.cu: DRAM writes stay
 // at the algorithmic bytes for runs >= 4 items).
 enum { kInHashPos = 0, kInFpPos = 1, kInPk = 2 };
-enum { kOutPk = 0, kOutFpPos = 1 };
+enum { kOutPk = 0, kOutFpPos = 1, kOutFpPos32 = 2 };  // kOutFpPos32: positions mod 2^32 (u32)
 // items ranked per round of __syncwarp (their shared-memory round trips overlap): 4 for big
 // tiles, 2 where the smaller footprint lets a third CTA fit on the SM
 template <int TPB, int IPT> constexpr int peer_tables() { return TPB >= 512 ? 1 : (IPT >= 16 ? 4 : 2); }
@@ -370,7 +373,9 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       }
       // per-warp digit counters, in item order: the lowest peer adds the peer count (every
       // other lane adds 0 to its own dummy word, so there is no branch); the old value is
-      // broadcast to the peers.  Same-warp shared atomics are performed in issue order.
+      // broadcast to the peers.  The leaders of one digit in two item rounds can be different
+      // lanes; MZS_RANK_SYNCWARP puts a __syncwarp between the rounds so that their atomics
+      // are ordered by the memory model, not only by the warp's in-order issue.
       uint32_t old[IPT];
 #pragma unroll
       for (int it = 0; it < IPT; ++it) {
@@ -378,6 +383,9 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
         const bool lead = valid && (peers[it] & lt) == 0u;
         uint32_t* tgt = lead ? &S.wcnt[wid][(uint32_t)(item[it] >> dsh) & dmask] : &S.dummy[wid][lane];
         old[it] = atomicAdd(tgt, lead ? (uint32_t)__popc(peers[it]) : 0u);
+#if MZS_RANK_SYNCWARP
+        if (it + 1 < IPT) __syncwarp();
+#endif
       }
 #pragma unroll
       for (int it = 0; it < IPT; ++it) {
@@ -461,6 +469,9 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
       if constexpr (OUT == kOutPk) {
         static_cast<uint64_t*>(a_out)[g] = v;
+      } else if constexpr (OUT == kOutFpPos32) {
+        static_cast<uint32_t*>(a_out)[g] = (uint32_t)(v >> 32);
+        reinterpret_cast<uint32_t*>(p_out)[g] = (uint32_t)v;  // the item carries pos mod 2^32
       } else if (dfp) {
         const uint32_t d = (uint32_t)(v >> dsh) & dmask;
         dfp[d][g] = (uint32_t)(v >> 32);  // a plain store: over NVLink when the buffer is a peer's
@@ -637,6 +648,17 @@ __global__ void counts_scan_kernel(const uint32_t* counts, uint64_t b0, uint64_t
   if (threadIdx.x == kTPB - 1) offsets[nb] = tot;
 }
 
+// (wide path, 32-bit position table) positions mod 2^32 from the wide path's u64 table; runs
+// only when ctl[0] selects the wide path
+__global__ void __launch_bounds__(kTPB) pos_to_u32_kernel(const uint64_t* __restrict__ p64, const uint64_t* d_m,
+                                                          uint64_t m_cap, uint32_t* __restrict__ p32,
+                                                          const uint64_t* ctl) {
+  if (gate_off(ctl, 0)) return;
+  const uint64_t m = block_count(d_m, m_cap);
+  for (uint64_t i = (uint64_t)blockIdx.x * kTPB + threadIdx.x; i < m; i += (uint64_t)gridDim.x * kTPB)
+    p32[i] = (uint32_t)p64[i];
+}
+
 // identity partition (one rank): fingerprints + positions in input order, count = m
 __global__ void fp_copy_kernel(const uint64_t* __restrict__ hash, const uint64_t* __restrict__ pos, const uint64_t* d_m,
                                uint64_t m_cap, int k, uint32_t* __restrict__ fp, uint64_t* __restrict__ pos_out,
@@ -667,6 +689,7 @@ struct SortWs {
   uint32_t* fpB;
   uint64_t* posB;             // also the narrow path's packed items (B)
   uint32_t* fpF;              // final fingerprints when the caller gave none
+  uint64_t* posW;             // (32-bit position table) the wide path's u64 positions
 };
 
 // Chunk size: kChunk entries, but small inputs take smaller chunks (a multiple of 4096) so that
@@ -696,6 +719,7 @@ void size_sort_ws(C& c, uint64_t m, int npass, bool need_fp) {
     c.template take<uint64_t>(m + 1);
   }
   if (need_fp) c.template take<uint32_t>(m + 1);
+  if (npass != 3) c.template take<uint64_t>(m + 1);  // posW (with 3 passes the A buffer is free)
 }
 
 bool carve_sort_ws(Carve& c, uint64_t m, int npass, bool need_fp, SortWs& s) {
@@ -709,6 +733,7 @@ bool carve_sort_ws(Carve& c, uint64_t m, int npass, bool need_fp, SortWs& s) {
   if (npass >= 2) { s.fpA = c.take<uint32_t>(m + 1); s.posA = c.take<uint64_t>(m + 1); }
   if (npass >= 3) { s.fpB = c.take<uint32_t>(m + 1); s.posB = c.take<uint64_t>(m + 1); }
   if (need_fp) s.fpF = c.take<uint32_t>(m + 1);
+  s.posW = npass != 3 ? c.take<uint64_t>(m + 1) : s.posA;
   return c.ok;
 }
 
@@ -768,7 +793,8 @@ int launch_nsweep_cfg(int cfg, const void* a_in, const uint64_t* p_in, void* a_o
 // ctl_kernel.  After the call s.totals holds the digit totals of the LAST pass.
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st,
-                const uint64_t* items = nullptr) {
+                const uint64_t* items = nullptr, uint32_t* pos32_dst = nullptr) {
+  // pos32_dst (packed items only): the final positions as u32 (pos mod 2^32) instead of pos_dst
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
   const uint64_t nch = (m + s.chunk - 1) / s.chunk;
@@ -781,8 +807,9 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
   MZS_LAUNCHED();
   if (force == 0) MZS_CUDA(cudaMemsetAsync(s.ctl, 0, sizeof(uint64_t), st));
   const int tma_in = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0;
+  if (pos32_dst && !items) return SLSUM_EINVAL;
   auto pass_out = [&](int p, uint64_t*& pk, uint32_t*& fo, uint64_t*& po) {
-    if (p == npass - 1) { fo = fp_dst; po = pos_dst; pk = nullptr; }
+    if (p == npass - 1) { fo = fp_dst; po = pos32_dst ? reinterpret_cast<uint64_t*>(pos32_dst) : pos_dst; pk = nullptr; }
     else if (p % 2 == 0) { fo = s.fpA; po = s.posA; pk = s.posA; }
     else { fo = s.fpB; po = s.posB; pk = s.posB; }
   };
@@ -797,8 +824,9 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       rc = count_pass<2>(items, d_m, m, k, lo_bit, nb, nch, s, 1, st);
       if (rc) return rc;
       const int tma_it = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
-      rc = npass == 1 ? launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
-                      : launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_it, st);
+      rc = npass != 1 ? launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
+           : pos32_dst ? launch_nsweep<kInPk, kOutFpPos32, 256, 16>(items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
+                       : launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st);
       if (rc) return rc;
     } else {
     rc = from_hash ? count_pass<0>(keys, d_m, m, k, lo_bit, nb, nch, s, 1, st)
@@ -823,6 +851,7 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     for (int p = 0; p < npass; ++p) {
       uint64_t* pk; uint32_t* fo; uint64_t* po;
       pass_out(p, pk, fo, po);
+      if (pos32_dst && p == npass - 1) po = s.posW;  // u64 here, narrowed below
       const int sh = lo_bit + 8 * p;
       const int nb = std::min(8, hi_bit - sh);
       rc = kin_hash ? count_pass<0>(kin, d_m, m, k, sh, nb, nch, s, 0, st) : count_pass<1>(kin, d_m, m, k, sh, nb, nch, s, 0, st);
@@ -834,6 +863,10 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       kin = fo;
       pin = po;
       kin_hash = false;
+    }
+    if (pos32_dst) {
+      pos_to_u32_kernel<<<grid_stride_blocks(m), kTPB, 0, st>>>(s.posW, d_m, m, pos32_dst, s.ctl);
+      MZS_LAUNCHED();
     }
   }
   // ---- narrow passes 1.. (packed items in, packed or final out)
@@ -847,8 +880,9 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
       const int nb = std::min(8, hi_bit - sh);
       rc = count_pass<2>(kin, d_m, m, k, sh, nb, nch, s, 1, st);
       if (rc) return rc;
-      rc = p == npass - 1 ? launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st)
-                          : launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, kin, nullptr, pk, nullptr, d_m, m, k, sh, nb, nch, s, 1, st);
+      rc = p != npass - 1 ? launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, kin, nullptr, pk, nullptr, d_m, m, k, sh, nb, nch, s, 1, st)
+           : pos32_dst ? launch_nsweep<kInPk, kOutFpPos32, 256, 16>(kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st)
+                       : launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, kin, nullptr, fo, po, d_m, m, k, sh, nb, nch, s, 1, st);
       if (rc) return rc;
       kin = pk;
     }
@@ -904,9 +938,10 @@ MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
 
 static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
                                 const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out,
-                                uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream) {
+                                uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream,
+                                uint32_t* pos32_out = nullptr) {
   if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
-  if (!offsets || (m && (!hash || !pos || !pos_out))) return SLSUM_EINVAL;
+  if (!offsets || (m && (!hash || !pos || (!pos_out && !pos32_out)))) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
   const uint64_t nb = 1ull << bucket_bits;
   if (m == 0) {
@@ -930,7 +965,7 @@ static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, con
   if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
-  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items);
+  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items, pos32_out);
   if (rc) return rc;
   return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st);
 }
@@ -948,6 +983,14 @@ MZS_API int seedtable_build_items(const uint64_t* items, const uint64_t* hash, c
   if (m && !items) return SLSUM_EINVAL;
   return seedtable_build_impl(items, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, pos_out, ws, ws_bytes,
                               stream);
+}
+
+MZS_API int seedtable_build_items32(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                                    const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out,
+                                    uint32_t* pos32_out, void* ws, size_t ws_bytes, void* stream) {
+  if (m && (!items || !pos32_out)) return SLSUM_EINVAL;
+  return seedtable_build_impl(items, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, nullptr, ws, ws_bytes,
+                              stream, pos32_out);
 }
 
 MZS_API int seedtable_count(const uint64_t* hash, uint64_t m, const uint64_t* d_m, int k, int bucket_bits,
@@ -1017,15 +1060,16 @@ MZS_API size_t seedtable_partition_p2p_workspace_bytes(uint64_t m, int nranks) {
 // every entry straight into its owner's receive buffer (peer memory over NVLink), at the offset
 // peer_base[o] this sender owns there.  Narrow path only (positions of the call within 2^32 of
 // pos[0]); returns SLSUM_EUNSUPPORTED otherwise, and the caller uses partition + NCCL.
-MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,
-                                    int bucket_bits, int nranks, const uint64_t* peer_fp, const uint64_t* peer_pos,
-                                    const uint64_t* peer_base, void* ws, size_t ws_bytes, void* stream) {
+static int partition_p2p_impl(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                              const uint64_t* d_m, int k, int bucket_bits, int nranks, const uint64_t* peer_fp,
+                              const uint64_t* peer_pos, const uint64_t* peer_base, void* ws, size_t ws_bytes,
+                              void* stream) {
   if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
   if (!is_pow2(nranks) || nranks < 2 || nranks > 256 || log2i(nranks) > bucket_bits || !peer_fp || !peer_pos ||
       !peer_base)
     return SLSUM_EINVAL;
   if (m == 0) return SLSUM_OK;
-  if (!hash || !pos) return SLSUM_EINVAL;
+  if ((!items && !hash) || !pos) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
   TempWs tmp;
   const size_t need = seedtable_partition_p2p_workspace_bytes(m, nranks);
@@ -1056,7 +1100,8 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   MZS_LAUNCHED();
   const int nb = g;
   const int sh = 32 - nb;
-  int rc = count_pass<0>(hash, d_m, m, k, sh, nb, nch, s, 1, st);
+  int rc = items ? count_pass<2>(items, d_m, m, k, sh, nb, nch, s, 1, st)
+                 : count_pass<0>(hash, d_m, m, k, sh, nb, nch, s, 1, st);
   if (rc) return rc;
   // destinations: digit o -> owner o's buffers, from this sender's base there (replacing the
   // digit scan's bases; digits >= nranks carry no entries)
@@ -1068,13 +1113,25 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   }
   MZS_CUDA(cudaMemcpyAsync(dptr, hp.data(), sizeof(uint64_t) * 2 * nranks, cudaMemcpyHostToDevice, st));
   MZS_CUDA(cudaMemcpyAsync(s.dbase, hb.data(), sizeof(unsigned long long) * 256, cudaMemcpyHostToDevice, st));
-  const int tma_in = ((reinterpret_cast<uintptr_t>(hash) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0;
-  auto kern = nsweep_kernel<kInHashPos, kOutFpPos, 256, 8>;
-  const size_t smem = nsweep_smem<kInHashPos, 256, 8>();
-  MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)nch, 256, smem, st>>>(hash, pos, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
-                                         tma_in, s.chunk, 1, reinterpret_cast<uint32_t* const*>(dptr),
-                                         reinterpret_cast<uint64_t* const*>(dptr + nranks));
+  if (items) {
+    // packed items (fp << 32 | pos mod 2^32): 8 B per entry in; the positions are restored from
+    // pos[0] (ctl[1]) as in the last pass of seedtable_build_items
+    const int tma_in = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
+    auto kern = nsweep_kernel<kInPk, kOutFpPos, 256, 8>;
+    const size_t smem = nsweep_smem<kInPk, 256, 8>();
+    MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)nch, 256, smem, st>>>(items, nullptr, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch,
+                                           s.ctl, tma_in, s.chunk, 1, reinterpret_cast<uint32_t* const*>(dptr),
+                                           reinterpret_cast<uint64_t* const*>(dptr + nranks));
+  } else {
+    const int tma_in = ((reinterpret_cast<uintptr_t>(hash) | reinterpret_cast<uintptr_t>(pos)) & 15) == 0;
+    auto kern = nsweep_kernel<kInHashPos, kOutFpPos, 256, 8>;
+    const size_t smem = nsweep_smem<kInHashPos, 256, 8>();
+    MZS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)nch, 256, smem, st>>>(hash, pos, nullptr, nullptr, d_m, m, k, sh, nb, s.offs, s.dbase, nch, s.ctl,
+                                           tma_in, s.chunk, 1, reinterpret_cast<uint32_t* const*>(dptr),
+                                           reinterpret_cast<uint64_t* const*>(dptr + nranks));
+  }
   MZS_LAUNCHED();
   // the host vectors above were read by the async copies; make them complete before returning.
   // The downsweep re-checks every entry against the narrow range and clears ctl[0] on a
@@ -1084,6 +1141,22 @@ MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, u
   MZS_CUDA(cudaMemcpyAsync(&narrow, s.ctl, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   MZS_CUDA(cudaStreamSynchronize(st));
   return narrow ? SLSUM_OK : SLSUM_EUNSUPPORTED;
+}
+
+MZS_API int seedtable_partition_p2p(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,
+                                    int bucket_bits, int nranks, const uint64_t* peer_fp, const uint64_t* peer_pos,
+                                    const uint64_t* peer_base, void* ws, size_t ws_bytes, void* stream) {
+  return partition_p2p_impl(nullptr, hash, pos, m, d_m, k, bucket_bits, nranks, peer_fp, peer_pos, peer_base, ws,
+                            ws_bytes, stream);
+}
+
+MZS_API int seedtable_partition_p2p_items(const uint64_t* items, const uint64_t* pos, uint64_t m, const uint64_t* d_m,
+                                          int k, int bucket_bits, int nranks, const uint64_t* peer_fp,
+                                          const uint64_t* peer_pos, const uint64_t* peer_base, void* ws,
+                                          size_t ws_bytes, void* stream) {
+  if (m && !items) return SLSUM_EINVAL;
+  return partition_p2p_impl(items, nullptr, pos, m, d_m, k, bucket_bits, nranks, peer_fp, peer_pos, peer_base, ws,
+                            ws_bytes, stream);
 }
 
 MZS_API size_t seedtable_finalize_workspace_bytes(uint64_t m_recv, int bucket_bits, int nranks) {

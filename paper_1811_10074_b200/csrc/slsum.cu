@@ -553,6 +553,156 @@ int launch_generic_cta(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStr
   return SLSUM_OK;
 }
 
+// GENERIC path, a TEAM of NWT warps per block of w = 32*EL*NWT inputs (EL = 8 consecutive per
+// lane), streaming: every team walks its own contiguous range of blocks and keeps the suffix
+// folds S of the previous block in registers, so there is no halo except one block per team
+// range, and the only synchronisation is a named barrier among the team's warps per block.
+// Per block b+1 (warp k holds its part k):
+//   in-lane prefix and suffix strips, warp shuffle scans -> the part's local P and S and its
+//   left / right folds T_k, R_k (shared memory, two slots by parity) -> team barrier ->
+//   carries C_k = T_0 (+) .. (+) T_{k-1}, D_k = R_{k+1} (+) .. (+) R_{NWT-1};
+//   P = C_k (+) P_local, S = S_local (+) D_k;
+//   outputs of block b: y_i = S_b[i] (+) P_{b+1}[i+w-1], the P one position to the left: the
+//   same register, the previous lane's last, or (lane 0 of warp k > 0) C_k itself.
+// Operand order is preserved (any associative op).  NWT = 1 needs no shared memory at all.
+constexpr int kTeamEL = 8;
+
+template <class Op, int NWT>
+__global__ void __launch_bounds__(256) slsum_generic_team_kernel(const typename Op::T* __restrict__ x,
+                                                                typename Op::T* __restrict__ y, uint64_t n,
+                                                                uint64_t nout, uint64_t blocks_per_team) {
+  using T = typename Op::T;
+  constexpr int EL = kTeamEL;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  constexpr uint32_t PW = 32 * EL;                          // elements of one warp's part
+  constexpr uint32_t W = PW * NWT;
+  constexpr int NTEAM = 8 / NWT;                            // teams per 256-thread CTA
+  static_assert(EL % OV == 0 && 8 % NWT == 0, "team shape");
+  __shared__ T sT[2][NTEAM][NWT], sR[2][NTEAM][NWT];
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t team = wid / NWT, k = wid % NWT;
+  const uint64_t gteam = (uint64_t)blockIdx.x * NTEAM + team;
+  const uint64_t nb = (n + W - 1) / W;
+  const uint64_t nbo = (nout + W - 1) / W;
+  const uint64_t b0 = gteam * blocks_per_team;
+  if (b0 >= nbo) return;                                    // whole teams leave together
+  const uint64_t b1 = min(nbo, b0 + blocks_per_team);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  auto team_sync = [&]() {
+    if (NWT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * NWT) : "memory");
+  };
+  auto load = [&](uint64_t b, T (&v)[EL]) {
+    const uint64_t g = b * W + (uint64_t)k * PW + (uint64_t)lane * EL;
+    if (aligned && b + 1 < nb) {
+#pragma unroll
+      for (int q = 0; q < EL; q += OV) *reinterpret_cast<uint4*>(v + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
+    } else {
+#pragma unroll
+      for (int j = 0; j < EL; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+    }
+  };
+  int par = 0;
+  // block b's prefix folds into v (in place) and suffix folds into S (from v), both team-wide;
+  // returns C_k (the fold of the parts left of k; unused for k == 0)
+  auto folds = [&](T (&v)[EL], T (&S)[EL]) -> T {
+    S[EL - 1] = v[EL - 1];
+#pragma unroll
+    for (int j = EL - 2; j >= 0; --j) S[j] = Op::op(v[j], S[j + 1]);
+#pragma unroll
+    for (int j = 1; j < EL; ++j) v[j] = Op::op(v[j - 1], v[j]);
+    T lt = v[EL - 1], rt = S[0];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T a = shfl_up(lt, o);
+      const T c = shfl_down(rt, o);
+      if (lane >= (uint32_t)o) lt = Op::op(a, lt);
+      if (lane + o < 32) rt = Op::op(rt, c);
+    }
+    const T le = shfl_up(lt, 1), re = shfl_down(rt, 1);
+    if (lane > 0) {
+#pragma unroll
+      for (int j = 0; j < EL; ++j) v[j] = Op::op(le, v[j]);
+    }
+    if (lane < 31) {
+#pragma unroll
+      for (int j = 0; j < EL; ++j) S[j] = Op::op(S[j], re);
+    }
+    T C = Op::id();
+    if (NWT > 1) {
+      const T tot_l = shfl_idx(lt, 31);     // fold of the whole part
+      const T tot_r = shfl_idx(rt, 0);
+      if (lane == 0) {
+        sT[par][team][k] = tot_l;
+        sR[par][team][k] = tot_r;
+      }
+      team_sync();
+      if (k > 0) {
+        C = sT[par][team][0];
+        for (uint32_t q = 1; q < k; ++q) C = Op::op(C, sT[par][team][q]);
+#pragma unroll
+        for (int j = 0; j < EL; ++j) v[j] = Op::op(C, v[j]);
+      }
+      if (k + 1 < (uint32_t)NWT) {
+        T D = sR[par][team][NWT - 1];
+        for (int q = NWT - 2; q > (int)k; --q) D = Op::op(sR[par][team][q], D);
+#pragma unroll
+        for (int j = 0; j < EL; ++j) S[j] = Op::op(S[j], D);
+      }
+      par ^= 1;
+    }
+    return C;
+  };
+  T Sp[EL];
+  {
+    T v[EL];
+    load(b0, v);
+    folds(v, Sp);
+  }
+  for (uint64_t b = b0; b < b1; ++b) {
+    T v[EL], Sn[EL];
+    load(b + 1, v);
+    const T C = folds(v, Sn);                               // v: P of block b+1
+    const T pl = shfl_up(v[EL - 1], 1);                     // the previous lane's last prefix
+    T o[EL];
+    if (lane > 0) o[0] = Op::op(Sp[0], pl);
+    else o[0] = k == 0 ? Sp[0] : Op::op(Sp[0], C);
+#pragma unroll
+    for (int j = 1; j < EL; ++j) o[j] = Op::op(Sp[j], v[j - 1]);
+    const uint64_t g = b * W + (uint64_t)k * PW + (uint64_t)lane * EL;
+    if (aligned && g + EL <= nout) {
+#pragma unroll
+      for (int q = 0; q < EL; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
+    } else {
+#pragma unroll
+      for (int j = 0; j < EL; ++j)
+        if (g + j < nout) y[g + j] = o[j];
+    }
+#pragma unroll
+    for (int j = 0; j < EL; ++j) Sp[j] = Sn[j];
+  }
+}
+
+template <class Op, int NWT>
+int launch_generic_team(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr uint32_t W = 32 * kTeamEL * NWT;
+  const uint64_t nout = n - w + 1;
+  const uint64_t nbo = (nout + W - 1) / W;
+  static int occ = 0;
+  if (occ == 0) {
+    MZS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slsum_generic_team_kernel<Op, NWT>, 256, 0));
+    occ = std::max(occ, 1);
+  }
+  const uint64_t teams = (uint64_t)num_sms() * occ * (8 / NWT);
+  const uint64_t per = std::max<uint64_t>(4, (nbo + teams - 1) / teams);
+  const uint64_t nt = (nbo + per - 1) / per;
+  const uint64_t grid = (nt + (8 / NWT) - 1) / (8 / NWT);
+  slsum_generic_team_kernel<Op, NWT><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv),
+                                                                     n, nout, per);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
@@ -586,6 +736,12 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
     if (w == 2 * E) return launch_generic_warpm<Op, 2>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_generic_warpm<Op, 4>(xv, yv, n, w, st);
     if (w == 8 * E) return launch_generic_warpm<Op, 8>(xv, yv, n, w, st);
+    if (!env_flag("MZS_SLSUM_NO_TEAM")) {            // a team of warps per block, streaming
+      if (w == 256) return launch_generic_team<Op, 1>(xv, yv, n, w, st);
+      if (w == 512) return launch_generic_team<Op, 2>(xv, yv, n, w, st);
+      if (w == 1024) return launch_generic_team<Op, 4>(xv, yv, n, w, st);
+      if (w == 2048) return launch_generic_team<Op, 8>(xv, yv, n, w, st);
+    }
     if (w == 16 * E) return launch_generic_cta<Op, 256, 16>(xv, yv, n, w, st);  // 256 > 512 lanes (75 vs 68 %)
     if (w == 32 * E) return launch_generic_cta<Op, 512, 32>(xv, yv, n, w, st);
     if (w == 64 * E) return launch_generic_cta<Op, 512, 64>(xv, yv, n, w, st);  // 512 > 1024 lanes (61 vs 54 %)
@@ -735,6 +891,120 @@ int launch_doubling_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaS
   return SLSUM_OK;
 }
 
+// COMMUTATIVE path for large w (>= 8E): the first RR rounds (shifts 1 .. 2E, < 4E) run in
+// registers on warp spans of 32E consecutive inputs -- a shift below E moves values inside a
+// lane plus the next lane's first d values by shuffles, a shift of E or 2E moves whole
+// registers from lane + 1 or + 2 -- and only the rounds with shifts >= 4E go through the
+// shared-memory ping-pong.  Warp spans overlap by 4E inputs so that every stored t_RR value
+// saw its whole 2^RR-input window; a CTA tile of L = NW*28E + 4E inputs gives L - w outputs
+// (rounded down to whole 16-byte vectors).  Power-of-two w for any commutative op; other w
+// only for idempotent ops (overlap finish t_m[i] (+) t_m[i + w - 2^m]).
+template <class Op, int TPB>
+__global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename Op::T* __restrict__ x,
+                                                               typename Op::T* __restrict__ y, uint64_t n,
+                                                               uint32_t w, uint64_t nout, uint32_t tout) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  constexpr int NWp = TPB / 32;
+  constexpr int RR = (E == 16) ? 6 : 5;       // 2^RR = 4E
+  constexpr uint32_t VS = 28 * E;             // valid positions per warp span after RR rounds
+  constexpr uint32_t Lv = NWp * VS;           // valid t_RR positions of the tile
+  constexpr uint32_t L = Lv + 4 * E;          // inputs of the tile
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* B = A + L + 2 * OV;
+  const uint64_t g0 = (uint64_t)blockIdx.x * tout;
+  const uint32_t t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const bool vin = ((reinterpret_cast<uintptr_t>(x + g0) & 15) == 0) && g0 + L <= n;
+  if (vin) {
+    for (uint32_t e = t * OV; e < L; e += TPB * OV)
+      *reinterpret_cast<uint4*>(A + e) = __ldg(reinterpret_cast<const uint4*>(x + g0 + e));
+  } else {
+    for (uint32_t e = t; e < L; e += TPB) A[e] = (g0 + e < n) ? x[g0 + e] : Op::id();
+  }
+  __syncthreads();
+  {
+    const uint32_t base = wid * VS + lane * E;
+    T v[E];
+#pragma unroll
+    for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(v + q) = *reinterpret_cast<const uint4*>(A + base + q);
+#pragma unroll
+    for (int r = 0; r < RR; ++r) {
+      const int d = 1 << r;
+      T u[E];
+      if (d < E) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) u[j] = (j + d < E) ? v[j + d] : shfl_down(v[(j + d) % E], 1);
+      } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) u[j] = shfl_down(v[j], d / E);
+      }
+#pragma unroll
+      for (int j = 0; j < E; ++j) v[j] = Op::op(v[j], u[j]);
+    }
+    if (lane * E < VS) {
+#pragma unroll
+      for (int q = 0; q < E; q += OV) *reinterpret_cast<uint4*>(B + base + q) = *reinterpret_cast<const uint4*>(v + q);
+    }
+  }
+  __syncthreads();
+  T* cur = B;
+  T* nxt = A;
+  const int m = 31 - __clz(w);
+  for (int r = RR; r < m; ++r) {
+    const uint32_t d = 1u << r;               // a multiple of OV
+    for (uint32_t e = t * OV; e + d < Lv; e += TPB * OV) {
+      T a[OV], c[OV], o[OV];
+      *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(cur + e);
+      *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(cur + e + d);
+#pragma unroll
+      for (uint32_t q = 0; q < OV; ++q) o[q] = Op::op(a[q], c[q]);
+      *reinterpret_cast<uint4*>(nxt + e) = *reinterpret_cast<const uint4*>(o);
+    }
+    __syncthreads();
+    T* tmp = cur; cur = nxt; nxt = tmp;
+  }
+  const uint32_t dd = w - (1u << m);          // 0 unless an idempotent op with w not a power of two
+  const uint32_t e_end = (uint32_t)min((uint64_t)tout, nout - g0);
+  const bool vout = ((reinterpret_cast<uintptr_t>(y + g0) & 15) == 0) && e_end == tout;
+  if (vout) {
+    for (uint32_t e = t * OV; e < tout; e += TPB * OV) {
+      T a[OV], c[OV], o[OV];
+      *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(cur + e);
+      if (dd) {
+        ld_shifted<T, OV>(cur, e, dd, c);
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q) o[q] = Op::op(a[q], c[q]);
+      } else {
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q) o[q] = a[q];
+      }
+      *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(o);
+    }
+  } else {
+    for (uint32_t e = t; e < e_end; e += TPB) y[g0 + e] = dd ? Op::op(cur[e], cur[e + dd]) : cur[e];
+  }
+}
+
+template <class Op, int TPB>
+int launch_doubling_rs(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
+  using T = typename Op::T;
+  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr uint32_t OV = 16 / sizeof(T);
+  constexpr uint32_t L = (TPB / 32) * 28 * E + 4 * E;
+  if (w + OV >= L) return SLSUM_EUNSUPPORTED;
+  const uint32_t tout = (L - w) & ~(OV - 1);
+  const uint64_t nout = n - w + 1;
+  const uint64_t grid = (nout + tout - 1) / tout;
+  const size_t smem = 2 * sizeof(T) * ((size_t)L + 2 * OV);
+  auto k = slsum_doubling_rs_kernel<Op, TPB>;
+  MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, w, nout, tout);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
+
 template <class Op>
 int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
@@ -759,6 +1029,12 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
     if (w == 13) return launch_doubling_warp<Op, 13>(xv, yv, n, w, st);
     if (w == 14) return launch_doubling_warp<Op, 14>(xv, yv, n, w, st);
     if (w == 15) return launch_doubling_warp<Op, 15>(xv, yv, n, w, st);
+  }
+  // w >= 8E: the first rounds in registers (power-of-two w, or any w for idempotent ops)
+  if (!env_flag("MZS_SLSUM_NO_RS") && w >= 8u * E && ((w & (w - 1)) == 0 || Op::kIdempotent) &&
+      n >= (uint64_t)w + 16 * 1024) {
+    if (w < 512) return launch_doubling_rs<Op, 512>(xv, yv, n, w, st);
+    if (w < 8192) return launch_doubling_rs<Op, 1024>(xv, yv, n, w, st);
   }
   const uint64_t nout = n - w + 1;
   // tile: tout = 8*TPB outputs (register accumulators) from L = tout + w - 1 inputs held in

@@ -87,14 +87,17 @@ class Phases:
 
 
 class CudaPhases(Phases):
-    """The product: every phase is a libmzslsum call on the current stream."""
+    """The product: every phase is a libmzslsum call on the current stream.  `d_m` (optional,
+    a device uint64 count with m as its upper bound) keeps the record count on the device."""
 
-    def __init__(self):
+    def __init__(self, d_m=None, items=None):
         from . import _lib as L
         self.L = L
+        self.d_m = d_m
+        self.items = items    # mz_extract_ex's packed items: the fused partition reads 8 B per entry
 
     def count(self, hash_, m, k, bits):
-        return self.L.seedtable_count(hash_, k, bits, m=m).view(torch.int32)
+        return self.L.seedtable_count(hash_, k, bits, m=m, d_m=self.d_m).view(torch.int32)
 
     def partition(self, hash_, pos, m, k, bits, nranks):
         fp, p, c = self.L.seedtable_partition(hash_, pos, k, bits, nranks, m=m)
@@ -108,7 +111,7 @@ class CudaPhases(Phases):
 
     def partition_p2p(self, hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base):
         return self.L.seedtable_partition_p2p(hash_.view(torch.uint64), pos.view(torch.uint64), k, bits,
-                                              peer_fp, peer_pos, peer_base, m=m)
+                                              peer_fp, peer_pos, peer_base, m=m, d_m=self.d_m, items=self.items)
 
 
 # ---------------------------------------------------------------- the exchange
@@ -122,6 +125,9 @@ def exchange_seedtable(hash_, pos, m: int, k: int, bits: int, phases: Phases, gr
     G = dist.get_world_size(group)
     if G & (G - 1):
         raise ValueError("world size must be a power of two (bucket ownership by top bits)")
+    d_m = getattr(phases, "d_m", None)
+    if d_m is not None:                              # all_to_all needs host split sizes anyway
+        m = min(m, int(d_m.view(torch.int64).item()))
     counts = phases.count(hash_, m, k, bits)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)        # uint32 sums as int32 bits
     send_fp, send_pos, send_counts = phases.partition(hash_, pos, m, k, bits, G)
@@ -160,25 +166,45 @@ def p2p_plan(owner_counts, span_ok):
 class SymmPeerMem:
     """The product's peer memory: one torch symmetric-memory buffer per (group, device), cap u64
     positions then cap u32 fingerprints, mapped into every peer over NVLink.  Grow-only with
-    1/8 headroom; every rank takes the same decision (cap is agreed).  get() returns
-    (c, local recv_pos int64[c], local recv_fp int32[c], fp pointers[G], pos pointers[G])."""
+    1/8 headroom; every rank takes the same decision (cap is agreed).
+
+    Two steps, so that a rank that cannot allocate never leaves the others waiting inside the
+    collective mapping: prepare() allocates locally (no collective) and returns whether it
+    could; the caller agrees on the result (all_reduce MIN) and only then calls get(), whose
+    rendezvous is collective.  get() returns (c, local recv_pos int64[c], local recv_fp
+    int32[c], fp pointers[G], pos pointers[G])."""
 
     def __init__(self):
         self._ent = {}
+        self._new = {}
 
-    def get(self, cap: int, dev, group):
-        import torch.distributed._symmetric_memory as symm_mem
+    def prepare(self, cap: int, dev, group) -> bool:
         key = (id(group), dev.index)
         ent = self._ent.get(key)
-        if ent is None or ent[0] < cap:
+        if ent is not None and ent[0] >= cap:
+            return True
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
             c = cap + cap // 8 + 1024
-            buf = symm_mem.empty(c + (c + 1) // 2, dtype=torch.uint64, device=dev)
+            self._new[key] = (c, symm_mem.empty(c + (c + 1) // 2, dtype=torch.uint64, device=dev))
+            return True
+        except Exception:                          # no symmetric memory on this box / out of memory
+            self._new.pop(key, None)
+            return False
+
+    def get(self, cap: int, dev, group):
+        key = (id(group), dev.index)
+        ent = self._ent.get(key)
+        if key not in self._new and (ent is None or ent[0] < cap) and not self.prepare(cap, dev, group):
+            raise RuntimeError("symmetric memory allocation failed")   # (callers agree on prepare() first)
+        if key in self._new:
+            import torch.distributed._symmetric_memory as symm_mem
+            c, buf = self._new.pop(key)
             hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
             G = dist.get_world_size(group)
             ptrs = [hdl.get_buffer(o, (1,), torch.uint8, 0).data_ptr() for o in range(G)]
-            ent = (c, buf, hdl, ptrs)
-            self._ent[key] = ent
-        c, buf, _, ptrs = ent
+            self._ent[key] = (c, buf, hdl, ptrs)
+        c, buf, _, ptrs = self._ent[key]
         return (c, buf[:c].view(torch.int64), buf[c:].view(torch.uint32)[:c].view(torch.int32),
                 [p + 8 * c for p in ptrs], list(ptrs))
 
@@ -200,36 +226,42 @@ def exchange_seedtable_p2p(hash_, pos, m: int, k: int, bits: int, phases: Phases
         raise ValueError("fused exchange needs a power-of-two world size >= 2")
     peer_mem = peer_mem or _PEER_MEM
     dev = hash_.device
+    d_m = getattr(phases, "d_m", None)             # device record count (CudaPhases), if any
     counts = phases.count(hash_, m, k, bits)
     nbl = (1 << bits) // G
     own = (counts.to(torch.int64) & 0xFFFFFFFF).view(G, nbl).sum(1)
-    span_ok = 1
+    # the narrow-item precondition (positions span < 2^32), decided on the device
     if m > 0:
-        ends = torch.stack([pos[0], pos[m - 1]]).view(torch.int64).cpu().tolist()
-        span_ok = int(((ends[1] - ends[0]) & ((1 << 64) - 1)) < (1 << 32))
-    row = torch.cat([own, torch.tensor([span_ok], dtype=torch.int64, device=dev)])
+        last = (d_m.view(torch.int64).clamp(1, m) - 1) if d_m is not None else torch.tensor([m - 1], device=dev)
+        ends = torch.cat([pos[:1].view(torch.int64), pos.view(torch.int64).index_select(0, last)])
+        span = (ends[1] - ends[0]).view(1)
+        span_ok = ((span >= 0) & (span < (1 << 32))).to(torch.int64)
+    else:
+        span_ok = torch.ones(1, dtype=torch.int64, device=dev)
+    row = torch.cat([own, span_ok])
     rows = [torch.empty_like(row) for _ in range(G)]
     dist.all_gather(rows, row, group=group)
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-    mat = [r.cpu().tolist() for r in rows]
+    mat = torch.stack(rows).cpu().tolist()         # the one host read: every sender's owner counts
     use, base, recv, cap = p2p_plan([r[:G] for r in mat], [r[G] for r in mat])
     if not use:
         return exchange_seedtable(hash_, pos, m, k, bits, phases, group)
-    try:
-        got = peer_mem.get(cap, dev, group)
-        ok = 1
-    except Exception:                              # no peer mapping on this box (no NVLink / IPC)
-        got, ok = None, 0
-    flag = torch.tensor([ok], dtype=torch.int64, device=dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
-    if not int(flag.item()):
+
+    def agree(ok: bool) -> bool:
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        return bool(int(flag.item()))
+
+    # local allocation first, agreed on by every rank, then the collective mapping
+    if not agree(peer_mem.prepare(cap, dev, group)):
         return exchange_seedtable(hash_, pos, m, k, bits, phases, group)
-    c, recv_pos, recv_fp, fp_ptrs, pos_ptrs = got
+    c, recv_pos, recv_fp, fp_ptrs, pos_ptrs = peer_mem.get(cap, dev, group)
     dist.barrier(group=group)                      # every owner is done with its previous contents
     rc = phases.partition_p2p(hash_, pos, m, k, bits, fp_ptrs, pos_ptrs, base[rank])
-    if rc != 0:
-        raise RuntimeError(f"seedtable_partition_p2p failed: {rc}")
-    dist.barrier(group=group)                      # every sender's writes have landed (it synced)
+    # a sender whose input broke the narrow precondition (unsorted positions) has written wrong
+    # entries into the owners' buffers: every rank then discards them and takes the NCCL path
+    if not agree(rc == 0):
+        return exchange_seedtable(hash_, pos, m, k, bits, phases, group)
     off, pl, fl = phases.finalize(recv_fp, recv_pos, recv[rank], counts, bits, rank, G)
     b0 = int((counts.to(torch.int64) & 0xFFFFFFFF)[: rank * nbl].sum().item())
     return off, pl, fl, b0

@@ -72,6 +72,20 @@ def c4_ascii(c4: "H.C4", device="cuda", out=None) -> torch.Tensor:
     return out
 
 
+def c4_ascii_reads(c4: "H.C4", r0: int, r1: int, device="cuda") -> torch.Tensor:
+    """Bases of reads [r0, r1) of the C4 batch (global positions [read_off[r0], read_off[r1]))."""
+    a, b = int(c4.read_off[r0]), int(c4.read_off[r1])
+    out = torch.empty(max(1, b - a), dtype=torch.uint8, device=device)
+    if r1 > r0:
+        ro = torch.from_numpy(c4.read_off[r0:r1 + 1]).to(device)
+        st = torch.from_numpy(c4.starts[r0:r1]).to(device)
+        # the kernel writes base t of read r at out[read_off[r] + t]: shift the base pointer by -a
+        _ok(lib().sg_reads_ascii(out.data_ptr() - a, ro.data_ptr(), st.data_ptr(), r1 - r0, c4.seed_t, c4.seed_sub,
+                                 H.C4_SUBST_T, _s()))
+        torch.cuda.current_stream().synchronize()
+    return out[: b - a]
+
+
 def c2_u32(n: int, seed: int = H.SEED_C2_U32, lo: int = 0, device="cuda") -> torch.Tensor:
     out = torch.empty(n, dtype=torch.uint32, device=device)
     _ok(lib().sg_u32(out.data_ptr(), lo, n, seed, _s()))

@@ -78,17 +78,26 @@ class FilePeerMem:
     """Test-only stand-in for the symmetric buffers: one shared file pair per rank; the
     'pointers' handed to partition_p2p are the peers' file paths."""
 
-    def __init__(self, root, rank, world):
+    def __init__(self, root, rank, world, fail_prepare=False):
         self.root, self.rank, self.world = root, rank, world
+        self.fail_prepare = fail_prepare
 
     def _paths(self, o):
         return os.path.join(self.root, f"fp{o}"), os.path.join(self.root, f"pos{o}")
 
-    def get(self, cap, dev, group):
+    def prepare(self, cap, dev, group):
+        """Local allocation (no collective), as SymmPeerMem.prepare."""
+        if self.fail_prepare:
+            return False
         c = cap + 7
         fpp, psp = self._paths(self.rank)
         np.memmap(fpp, dtype=np.int32, mode="w+", shape=(c,)).flush()
         np.memmap(psp, dtype=np.int64, mode="w+", shape=(c,)).flush()
+        return True
+
+    def get(self, cap, dev, group):
+        c = cap + 7
+        fpp, psp = self._paths(self.rank)
         dist.barrier(group=group)
         self.local = (np.memmap(fpp, dtype=np.int32, mode="r"), np.memmap(psp, dtype=np.int64, mode="r"))
         return (c, _LazyFile(psp, np.int64), _LazyFile(fpp, np.int32),
@@ -105,7 +114,25 @@ class _LazyFile:
         return torch.from_numpy(np.array(np.memmap(self.path, dtype=self.dt, mode="r"))[sl])
 
 
-def _worker(rank, world, port, q, p2p_root=None):
+class BadInputPhases(OraclePhases):
+    """Test-only: the fused write reports a broken precondition on rank 1 (as the kernel does
+    for unsorted positions), after writing garbage into the owners' buffers."""
+
+    def __init__(self, rank):
+        self.rank = rank
+
+    def partition_p2p(self, hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base):
+        rc = super().partition_p2p(hash_, pos, m, k, bits, peer_fp, peer_pos, peer_base)
+        if self.rank != 1:
+            return rc
+        for o in range(len(peer_fp)):
+            f = np.memmap(peer_fp[o], dtype=np.int32, mode="r+")
+            f[:] = -1
+            f.flush()
+        return -2
+
+
+def _worker(rank, world, port, q, p2p_root=None, mode="ok"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -116,26 +143,33 @@ def _worker(rank, world, port, q, p2p_root=None):
         sub = seq[sh.base_lo: sh.base_hi]
         key, pos = O.mz(sub, K, W, pos_base=sh.base_lo, win_lo=sh.win_lo, win_hi=sh.win_hi)
         m = len(key)
+        phases = BadInputPhases(rank) if mode == "bad_input" else OraclePhases()
         args = (torch.from_numpy(key.view(np.int64).copy()), torch.from_numpy(pos.view(np.int64).copy()),
-                m, K, BITS, OraclePhases())
+                m, K, BITS, phases)
         if p2p_root is None:
             off, pl, fl, base = D.exchange_seedtable(*args)
         else:
-            off, pl, fl, base = D.exchange_seedtable_p2p(*args, peer_mem=FilePeerMem(p2p_root, rank, world))
+            pm = FilePeerMem(p2p_root, rank, world, fail_prepare=(mode == "no_peer_mem" and rank == world - 1))
+            off, pl, fl, base = D.exchange_seedtable_p2p(*args, peer_mem=pm)
         q.put((rank, key, pos, off.numpy(), pl.numpy(), fl.numpy(), base))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,p2p", [(2, False), (4, False), (2, True), (4, True)])
-def test_sharded_extraction_and_exchange(world, p2p, tmp_path):
+@pytest.mark.parametrize("world,p2p,mode", [(2, False, "ok"), (4, False, "ok"), (8, False, "ok"), (2, True, "ok"),
+                                           (4, True, "ok"), (8, True, "ok"), (4, True, "no_peer_mem"),
+                                           (2, True, "bad_input")])
+def test_sharded_extraction_and_exchange(world, p2p, mode, tmp_path):
     """p2p=True runs exchange_seedtable_p2p (the fused partition-to-peers path) with
-    file-backed peer buffers in place of NVLink-mapped symmetric memory."""
+    file-backed peer buffers in place of NVLink-mapped symmetric memory.  no_peer_mem: one
+    rank cannot allocate its buffer, so every rank takes the NCCL exchange (no rank is left in
+    the collective mapping).  bad_input: one sender's fused write reports a broken precondition
+    after writing garbage; every rank discards the buffers and takes the NCCL exchange."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     root = str(tmp_path) if p2p else None
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, root)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, root, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])

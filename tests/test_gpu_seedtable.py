@@ -169,15 +169,17 @@ def test_multi_rank_phases_emulated(nranks):
     assert np.array_equal(np.concatenate(all_fp), wf)
 
 
-@pytest.mark.parametrize("nranks", [2, 4, 8])
-def test_partition_p2p_emulated(nranks):
-    """The partition fused with the all-to-all (seedtable_partition_p2p), with the ranks
-    emulated in one process on one GPU: every sender writes straight into all owners' receive
-    buffers (here plain device buffers; peer-mapped symmetric memory on a real box) at its base
-    offsets; each owner then finalizes.  The concatenated slices must equal the oracle table."""
+@pytest.mark.parametrize("nranks,items,pos_base", [(2, False, 0), (4, False, 0), (8, False, 0), (2, True, 0),
+                                                   (8, True, (1 << 32) - 1_000_000)])
+def test_partition_p2p_emulated(nranks, items, pos_base):
+    """The partition fused with the all-to-all (seedtable_partition_p2p, and _items from the
+    packed items), with the ranks emulated in one process on one GPU: every sender writes
+    straight into all owners' receive buffers (here plain device buffers; peer-mapped symmetric
+    memory on a real box) at its base offsets; each owner then finalizes.  The concatenated
+    slices must equal the oracle table (also across a multiple of 2^32 in the positions)."""
     k, bits = 19, 24
     c3 = G.C3(n=3_000_000)
-    key, pos = O.mz(c3.ascii(), k, 10)
+    key, pos = O.mz(c3.ascii(), k, 10, pos_base=pos_base)
     m = len(key)
     cuts = [m * g // nranks for g in range(nranks + 1)]
     nbl = (1 << bits) // nranks
@@ -194,8 +196,12 @@ def test_partition_p2p_emulated(nranks):
              torch.empty(max(1, int(recv[o])), dtype=torch.uint64, device="cuda")) for o in range(nranks)]
     for g, (kt, pt) in enumerate(shards):
         base = [int(cnt[:g, o].sum()) for o in range(nranks)]
+        it = None
+        if items:   # items as mz_extract_ex writes them: fp << 32 | pos mod 2^32 (from the oracle's records)
+            kn, pn = key[cuts[g]:cuts[g + 1]], pos[cuts[g]:cuts[g + 1]]
+            it = _dev((_fp_np(kn, k) << np.uint64(32)) | (pn & np.uint64(0xFFFFFFFF)))
         rc = P.seedtable_partition_p2p(kt, pt, k, bits, [b[0].data_ptr() for b in bufs],
-                                       [b[1].data_ptr() for b in bufs], base)
+                                       [b[1].data_ptr() for b in bufs], base, items=it)
         assert rc == P.SLSUM_OK
     torch.cuda.synchronize()
     gc32 = gcounts.to(torch.int32).view(torch.uint32)
@@ -253,3 +259,30 @@ def test_items_path_vs_oracle(k, pos_base, path):
         assert np.array_equal(off.cpu().numpy(), wo)
         assert np.array_equal(po[:m].cpu().numpy(), wpos)
         assert np.array_equal(fp[:m].cpu().numpy(), wf)
+        # the 32-bit position table: the same entries, positions mod 2^32
+        off32, po32, fp32 = P.seedtable_build_items32(items, h, p, k, bits, m=(m if d_m is None else cap), d_m=d_m)
+        torch.cuda.synchronize()
+        assert np.array_equal(off32.cpu().numpy(), wo)
+        assert np.array_equal(po32[:m].cpu().numpy(), (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+        assert np.array_equal(fp32[:m].cpu().numpy(), wf)
+
+
+@pytest.mark.parametrize("npass_bits", [12, 16, 24, 30])
+def test_items32_wide_spans_and_bit_widths(npass_bits):
+    """seedtable_build_items32 when the positions span >= 2^32 (the wide path, narrowed to u32
+    afterwards) and for 1, 2, 3 and 4 radix passes (the u64 scratch of the wide path's last pass
+    is a separate buffer unless there are exactly 3 passes)."""
+    k = 19
+    rng = np.random.default_rng(npass_bits)
+    m = 50_000
+    key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
+    for step in (7, 200_003):                       # narrow span, then a span >= 2^32 (wide path)
+        pos = (np.arange(m, dtype=np.uint64) * np.uint64(step) + np.uint64(12345))
+        fpk = _fp_np(key, k)
+        items = _dev((fpk << np.uint64(32)) | (pos & np.uint64(0xFFFFFFFF)))
+        wo, wf, wpos = O.seedtable(key, pos, k, npass_bits)
+        off, po, fp = P.seedtable_build_items32(items, _dev(key), _dev(pos), k, npass_bits)
+        torch.cuda.synchronize()
+        assert np.array_equal(off.cpu().numpy(), wo), step
+        assert np.array_equal(po.cpu().numpy(), (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32)), step
+        assert np.array_equal(fp.cpu().numpy(), wf), step

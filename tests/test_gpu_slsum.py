@@ -218,3 +218,42 @@ def test_c2_full_size_sampled(w):
             else:
                 assert abs(float(ys[j]) - float(o)) <= 1e-5 * abs(float(o)) + 1e-6 * w
         del y
+
+
+@pytest.mark.parametrize("op", [P.SLSUM_MIN_U32, P.SLSUM_ADD_F32, P.SLSUM_AFFINE_U32X2, P.SLSUM_MIN_U64])
+@pytest.mark.parametrize("m_lanes", [16, 32, 64, 128])
+def test_generic_large_blocks(op, m_lanes):
+    """GENERIC for w = M*E (M = 16..128 lanes of E elements per block): the team kernel (a team
+    of warps per block of 256*NWT, streaming over a range of blocks, carrying the suffix folds)
+    and the one-shot CTA kernel (8-byte w = 128): inputs that are an exact multiple of the
+    block and tile sizes, ragged ones, many blocks per team, and a misaligned view."""
+    e = 8 if op in (P.SLSUM_AFFINE_U32X2, P.SLSUM_MIN_U64) else 16
+    w = m_lanes * e
+    L = 256 * e
+    rng = np.random.default_rng(op * 100 + m_lanes)
+    for n in (3 * L, 7 * L + 5, 1_500 * L, 1_500 * L + L - 1):
+        x = _input(op, n, rng)
+        _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_GENERIC))
+    x = _input(op, 40 * L + 3, rng)
+    xt = torch.from_numpy(np.concatenate([x[:1], x])).cuda()[1:]      # 4/8-byte aligned, not 16
+    y = P.slsum_run(op, w, xt, path=P.SLSUM_PATH_GENERIC)
+    torch.cuda.synchronize()
+    _check(op, w, x, y.cpu().numpy())
+
+
+@pytest.mark.parametrize("op,w", [(P.SLSUM_MIN_U32, 128), (P.SLSUM_MIN_U32, 1024), (P.SLSUM_ADD_U32, 256),
+                                  (P.SLSUM_ADD_U32, 4096), (P.SLSUM_ADD_F32, 512), (P.SLSUM_MAX_U32, 300),
+                                  (P.SLSUM_MAX_U32, 2049), (P.SLSUM_MIN_U64, 64), (P.SLSUM_MIN_U64, 777)])
+def test_commutative_register_start(op, w):
+    """The COMMUTATIVE kernel for w >= 8E (first rounds in registers on overlapping warp spans,
+    the rest in shared memory): power-of-two w for any commutative op, other w for idempotent
+    ones; several tiles, a ragged end, and a misaligned view."""
+    rng = np.random.default_rng(op * 31 + w)
+    for n in (w + 16 * 1024, 200_003, 1 << 20):
+        x = _input(op, n, rng)
+        _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_COMMUTATIVE))
+    x = _input(op, 100_001, rng)
+    xt = torch.from_numpy(np.concatenate([x[:1], x])).cuda()[1:]
+    y = P.slsum_run(op, w, xt, path=P.SLSUM_PATH_COMMUTATIVE)
+    torch.cuda.synchronize()
+    _check(op, w, x, y.cpu().numpy())
