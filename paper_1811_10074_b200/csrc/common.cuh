@@ -74,6 +74,22 @@ struct TempWs {
   ~TempWs() { if (p) cudaFreeAsync(p, s); }
 };
 
+// ---------------------------------------------------------------- device self-checks
+// MZS_DCHECK: bounds / invariant checks inside the kernels, compiled in only by a debug build
+// (-DMZS_DEBUG_CHECKS=1, tools/variant_lib.sh); a violated check traps, which fails the launch.
+// compute-sanitizer is not available on this pool, so a test run against the checked build
+// stands in for memcheck on the indices the kernels compute themselves.
+#if defined(MZS_DEBUG_CHECKS) && MZS_DEBUG_CHECKS
+#define MZS_DCHECK(cond) \
+  do {                   \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define MZS_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }

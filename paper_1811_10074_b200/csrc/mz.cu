@@ -609,7 +609,10 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
       // bit); the carried-in argmin of window jb-1, owned by the strip on the left, is cleared
       // once after the strip (R3)
       if (MASKED) em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
-      else em |= 1ull << (s - (uint32_t)(jb + 1));
+      else {
+        MZS_DCHECK(s - (uint32_t)(jb + 1) < 64u);
+        em |= 1ull << (s - (uint32_t)(jb + 1));
+      }
     } else {
       const bool v = valid_of(j);
       const bool e = v && (!vprev || s != sprev) && ((unsigned)(j - elo) < (unsigned)(ehi - elo));
@@ -708,6 +711,7 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
     for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * G::TPB;
       const uint32_t slot_all = i < lim ? list[i] : 0u;
+      MZS_DCHECK(slot_all < (uint32_t)(G::SUBS * G::NS));
       const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
       const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
       q[u] = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
@@ -722,6 +726,7 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
       const uint32_t i = i0 + u * G::TPB;
       if (i < lim) {
         const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, q[u], A[u], B[u]);
+        MZS_DCHECK(base + i < a.capacity && q[u] >= 0 && (uint64_t)q[u] < a.n);
         a.out_hash[base + i] = h;
         a.out_pos[base + i] = a.pos_base + (uint64_t)q[u];
         if (a.out_items) a.out_items[base + i] = item_of(h, KK ? KK : a.k, a.pos_base + (uint64_t)q[u]);

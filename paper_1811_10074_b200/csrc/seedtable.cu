@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
     for (int it = 0; it < IPT; ++it) {
       if (rank[it] != 0xffffffffu) {
         const uint32_t sl = wrow[(uint32_t)(item[it] >> dsh) & dmask] + rank[it];
+        MZS_DCHECK(sl < nvalid);
         if constexpr (WD) {
           stage_f[sl] = (uint32_t)(item[it] >> 32);
           stage[sl] = ipos[WD ? it : 0];
@@ -467,6 +468,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       }
       const uint64_t v = stage[j];
       const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & dmask] + j;
+      MZS_DCHECK(dfp != nullptr || g < m);
       if constexpr (OUT == kOutPk) {
         static_cast<uint64_t*>(a_out)[g] = v;
       } else if constexpr (OUT == kOutFpPos32) {

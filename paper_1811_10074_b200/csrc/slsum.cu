@@ -669,6 +669,7 @@ __global__ void __launch_bounds__(256) slsum_generic_team_kernel(const typename 
 #pragma unroll
     for (int j = 1; j < EL; ++j) o[j] = Op::op(Sp[j], v[j - 1]);
     const uint64_t g = b * W + (uint64_t)k * PW + (uint64_t)lane * EL;
+    MZS_DCHECK(b < nb);
     if (aligned && g + EL <= nout) {
 #pragma unroll
       for (int q = 0; q < EL; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
