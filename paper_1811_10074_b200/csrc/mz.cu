@@ -24,6 +24,12 @@ namespace mzs {
 namespace {
 
 constexpr int kSlotBits = 14;  // slot index inside a tile (< 16384)
+#ifndef MZS_MZ_MARK32
+#define MZS_MZ_MARK32 1
+#endif
+#ifndef MZS_MZ_OUT_U
+#define MZS_MZ_OUT_U 4   // records per thread per step of the fast path's output loop
+#endif
 constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1;
 
 struct DKey;  // defined with the other key types below
@@ -576,6 +582,7 @@ struct FastGeom {
   static_assert(R + W <= 64, "per-thread emission mask");
   static_assert(NS < (1 << kSlotBits), "slot bits");
   static_assert(SUBS * NS * 2 <= NS * 8 && SUBS * NS < 65536, "phase-3 slot list fits in the keys smem");
+  static_assert((SUBS - 1) * TW + NS <= 65536, "phase-3 list entries (k-mer offsets) fit 16 bits");
   static_assert(TPB >= W + 1, "halo slots");
 };
 
@@ -597,6 +604,10 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
   uint32_t s_carry;  // argmin slot of window jb-1 (FULL strips)
   bool vprev;
   uint64_t em = 0;  // bit i <-> slot jb + 1 + i
+  // FULL unmasked strips mark into a 32-bit mask per block of W windows (their argmins lie in
+  // the block's slots + W - 1 more: < 2W <= 32 bits), folded into em once per block
+  constexpr bool kM32 = FULL && !MASKED && MZS_MZ_MARK32;
+  uint32_t m32 = 0, mbase = 0;
   auto valid_of = [&](int j) -> bool {
     if (FULL) return true;
     const bool in = (unsigned)(j - vlo) < (unsigned)(vhi - vlo);
@@ -609,7 +620,10 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
       // bit); the carried-in argmin of window jb-1, owned by the strip on the left, is cleared
       // once after the strip (R3)
       if (MASKED) em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
-      else {
+      else if (kM32) {
+        MZS_DCHECK(s - mbase < 32u);
+        m32 |= 1u << (s - mbase);
+      } else {
         MZS_DCHECK(s - (uint32_t)(jb + 1) < 64u);
         em |= 1ull << (s - (uint32_t)(jb + 1));
       }
@@ -638,6 +652,10 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
 #pragma unroll 1
   for (int b = 1; b <= G::M; ++b) {
     const int jblk = jb + (b - 1) * W;
+    if (kM32) {
+      m32 = 0;
+      mbase = (uint32_t)(jblk + 1);
+    }
     visit(jblk, S[0]);
     const int sb = jb + 1 + b * W;
 #pragma unroll
@@ -651,6 +669,7 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
     S[W - 1] = kb[W - 1];
 #pragma unroll
     for (int q = W - 2; q >= 0; --q) S[q] = kmin(kb[q], S[q + 1]);
+    if (kM32) em |= (uint64_t)m32 << (jblk - jb);
   }
   if (FULL && (!MASKED || (vm & 1u))) {  // (an invalid window jb-1 carries no record)
     const uint32_t rel = s_carry - (uint32_t)(jb + 1);  // wraps (large) when the carry is left of the strip
@@ -685,10 +704,14 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
     const int u = u0 + uu;
     if (u >= NSWT) break;
     uint32_t bits = emit[u];
+    // list entries are k-mer offsets from the super-tile start minus one: slot s of sub-tile
+    // `sub` is the k-mer super_lo + sub*TW - 1 + s (< SUBS*TW + NS <= 2^16; emitted s >= 1)
+    const int sub = u / G::NSW;
+    const uint32_t rel0 = (uint32_t)(sub * G::TW + (u - sub * G::NSW) * 32);
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
-      list[o++] = (uint16_t)(u * 32 + b);
+      list[o++] = (uint16_t)(rel0 + b - 1);
     }
   }
   if (warp_id() == 0) {
@@ -703,18 +726,16 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
   const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
   // four records per thread per step: their word loads are all in flight before the hashes
   const uint32_t lim = (uint32_t)min((uint64_t)total, a.capacity > base ? a.capacity - base : (uint64_t)0);
-  constexpr int U = 4;
+  constexpr int U = MZS_MZ_OUT_U;
   for (uint32_t i0 = threadIdx.x; i0 < lim; i0 += U * G::TPB) {
     int64_t q[U];
     uint64_t A[U], B[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * G::TPB;
-      const uint32_t slot_all = i < lim ? list[i] : 0u;
-      MZS_DCHECK(slot_all < (uint32_t)(G::SUBS * G::NS));
-      const uint32_t sub = slot_all / (uint32_t)G::NS;          // compile-time divisor
-      const uint32_t slot = slot_all - sub * (uint32_t)G::NS;
-      q[u] = super_lo + (int64_t)(sub * G::TW) - 1 + slot;
+      const uint32_t rel = i < lim ? list[i] : 0u;
+      MZS_DCHECK(rel < (uint32_t)(G::SUBS * G::TW + W));
+      q[u] = super_lo + rel;
       // an emitted k-mer lies in [0, n), so its first word exists; the next one is needed only
       // when the k-mer crosses into it, so clamping its index (instead of a bounds test) is safe
       const uint64_t wq = (uint64_t)max(q[u] >> 5, (int64_t)0);
