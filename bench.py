@@ -69,10 +69,14 @@ def parse():
 
 
 def load_traffic(name):
-    """DRAM bytes per launch of the step's kernels from the committed ncu --set full capture
-    (profiles/r01/traffic_c3.json, written by tools/ncu_summary.py traffic); None if absent."""
-    p = os.path.join(ROOT, "profiles", "r01", name)
-    if not os.path.exists(p):
+    """DRAM bytes per launch of the step's kernels from the latest committed ncu --set full
+    capture (profiles/r02 or r01 traffic_c3.json, written by tools/ncu_summary.py traffic);
+    None if absent."""
+    for rd in ("r02", "r01"):
+        p = os.path.join(ROOT, "profiles", rd, name)
+        if os.path.exists(p):
+            break
+    else:
         return None
     try:
         return json.load(open(p))
@@ -833,7 +837,7 @@ def main():
     tab_traffic = sum(v["dram_bytes"] for kk, v in tr.items() if kk.startswith(("nsweep", "upsweep"))) if tr else None
     roof = {"bound": "alu", "kernel": "mz_fast_kernel (a2-a7 fused, one launch per step)",
             "achieved": ach, "peak": int_peak, "unit": "Tops/s", "frac": ach / int_peak, "traffic": mz_traffic,
-            "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r01/traffic_c3.json); algorithmic "
+            "traffic_note": "DRAM bytes per launch, ncu --set full (profiles/r0x/traffic_c3.json); algorithmic "
                             f"{per_phase_bytes['extract']:.3e} B",
             "peak_kind": f"derived: {SM_COUNT} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x {sm_mhz:.0f} MHz",
             "peak_measured": load_int_peak(),

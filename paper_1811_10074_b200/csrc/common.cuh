@@ -74,6 +74,13 @@ struct TempWs {
   ~TempWs() { if (p) cudaFreeAsync(p, s); }
 };
 
+// ---------------------------------------------------------------- shared host entry points
+// (seedtable.cu) stable sort of (u32 fingerprint, u64 index) pairs by fingerprint bits
+// [lo_bit, 32), used by the sorted seed lookup
+size_t sort_fp_idx_workspace_bytes(uint64_t m, int lo_bit);
+int sort_fp_idx(const uint32_t* fp, const uint64_t* idx, uint64_t m, int lo_bit, uint32_t* fp_out, uint64_t* idx_out,
+                void* ws, size_t ws_bytes, cudaStream_t st);
+
 // ---------------------------------------------------------------- device self-checks
 // MZS_DCHECK: bounds / invariant checks inside the kernels, compiled in only by a debug build
 // (-DMZS_DEBUG_CHECKS=1, tools/variant_lib.sh); a violated check traps, which fails the launch.

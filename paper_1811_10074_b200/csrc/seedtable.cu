@@ -915,6 +915,22 @@ bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
 
 }  // namespace
+
+// Stable sort of m (fingerprint, index) pairs by fingerprint bits [lo_bit, 32), for other
+// translation units (the sorted seed lookup, lookup.cu): the seed table's own radix passes.
+size_t sort_fp_idx_workspace_bytes(uint64_t m, int lo_bit) {
+  Sizer z;
+  size_sort_ws(z, m, (32 - lo_bit + 7) / 8, false);
+  return z.used;
+}
+int sort_fp_idx(const uint32_t* fp, const uint64_t* idx, uint64_t m, int lo_bit, uint32_t* fp_out, uint64_t* idx_out,
+                void* ws, size_t ws_bytes, cudaStream_t st) {
+  Carve c(ws, ws_bytes);
+  SortWs s;
+  if (!carve_sort_ws(c, m, (32 - lo_bit + 7) / 8, false, s)) return SLSUM_ENOMEM;
+  return stable_sort(false, fp, idx, nullptr, m, 0, lo_bit, 32, fp_out, idx_out, s, st);
+}
+
 }  // namespace mzs
 
 using namespace mzs;

@@ -900,18 +900,20 @@ int launch_doubling_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaS
 // saw its whole 2^RR-input window; a CTA tile of L = NW*28E + 4E inputs gives L - w outputs
 // (rounded down to whole 16-byte vectors).  Power-of-two w for any commutative op; other w
 // only for idempotent ops (overlap finish t_m[i] (+) t_m[i + w - 2^m]).
-template <class Op, int TPB>
+template <class Op, int TPB, int XR = 0>
 __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename Op::T* __restrict__ x,
                                                                typename Op::T* __restrict__ y, uint64_t n,
                                                                uint32_t w, uint64_t nout, uint32_t tout) {
+  // XR extra register rounds: shifts up to 2E << XR, spans overlapping by 4E << XR
   using T = typename Op::T;
   constexpr int E = (sizeof(T) == 4) ? 16 : 8;
   constexpr uint32_t OV = 16 / sizeof(T);
   constexpr int NWp = TPB / 32;
-  constexpr int RR = (E == 16) ? 6 : 5;       // 2^RR = 4E
-  constexpr uint32_t VS = 28 * E;             // valid positions per warp span after RR rounds
-  constexpr uint32_t Lv = NWp * VS;           // valid t_RR positions of the tile
-  constexpr uint32_t L = Lv + 4 * E;          // inputs of the tile
+  constexpr int RR = ((E == 16) ? 6 : 5) + XR;    // 2^RR = 4E << XR
+  constexpr uint32_t HALO = 4u * E << XR;
+  constexpr uint32_t VS = 32 * E - HALO;          // valid positions per warp span after RR rounds
+  constexpr uint32_t Lv = NWp * VS;               // valid t_RR positions of the tile
+  constexpr uint32_t L = Lv + HALO;               // inputs of the tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* A = reinterpret_cast<T*>(smem_raw);
   T* B = A + L + 2 * OV;
@@ -988,18 +990,19 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename O
   }
 }
 
-template <class Op, int TPB>
+template <class Op, int TPB, int XR = 0>
 int launch_doubling_rs(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
   constexpr int E = (sizeof(T) == 4) ? 16 : 8;
   constexpr uint32_t OV = 16 / sizeof(T);
-  constexpr uint32_t L = (TPB / 32) * 28 * E + 4 * E;
+  constexpr uint32_t HALO = 4u * E << XR;
+  constexpr uint32_t L = (TPB / 32) * (32 * E - HALO) + HALO;
   if (w + OV >= L) return SLSUM_EUNSUPPORTED;
   const uint32_t tout = (L - w) & ~(OV - 1);
   const uint64_t nout = n - w + 1;
   const uint64_t grid = (nout + tout - 1) / tout;
   const size_t smem = 2 * sizeof(T) * ((size_t)L + 2 * OV);
-  auto k = slsum_doubling_rs_kernel<Op, TPB>;
+  auto k = slsum_doubling_rs_kernel<Op, TPB, XR>;
   MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, w, nout, tout);
   MZS_LAUNCHED();
@@ -1034,8 +1037,11 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
   // w >= 8E: the first rounds in registers (power-of-two w, or any w for idempotent ops)
   if (!env_flag("MZS_SLSUM_NO_RS") && w >= 8u * E && ((w & (w - 1)) == 0 || Op::kIdempotent) &&
       n >= (uint64_t)w + 16 * 1024) {
+    // one more register round (spans overlapping by 8E) below w = 4096: w=1024 264 -> 272,
+    // w=2048 224 -> 230 Gelem/s; at 4096 the wider overlap costs more than the round saves
     if (w < 512) return launch_doubling_rs<Op, 512>(xv, yv, n, w, st);
-    if (w < 8192) return launch_doubling_rs<Op, 1024>(xv, yv, n, w, st);
+    if (w < 4096) return launch_doubling_rs<Op, 1024, 1>(xv, yv, n, w, st);
+    if (w < 8192) return launch_doubling_rs<Op, 1024, 0>(xv, yv, n, w, st);
   }
   const uint64_t nout = n - w + 1;
   // tile: tout = 8*TPB outputs (register accumulators) from L = tout + w - 1 inputs held in

@@ -96,3 +96,28 @@ def test_reads_against_template_end_to_end():
     assert np.array_equal(ho.cpu().numpy(), ho_w)
     assert np.array_equal(hp[: len(hp_w)].cpu().numpy(), hp_w)
     assert int(tot.view(torch.int64).item()) > mr // 10    # reads do hit their template
+
+
+@pytest.mark.parametrize("k,bits", [(15, 24), (19, 24), (15, 28), (8, 16)])
+def test_sorted_lookup_large_batches(k, bits):
+    """Batches of >= 2^20 queries take the sorted lookup (queries radix-sorted by bucket, then
+    served in bucket order, results at their own index): the CSR equals the oracle's, with
+    repeated queries, hitless ones and multi-hit seeds."""
+    rng = np.random.default_rng(k * 7 + bits)
+    m, nq = 400_000, (1 << 20) + 12_345
+    span = min(1 << (2 * k), 150_000)
+    key = rng.integers(0, span, size=m, dtype=np.uint64)
+    if 2 * k > 32:
+        lb = 2 * k - 32
+        key = (key << np.uint64(lb)) | rng.integers(0, 1 << lb, size=m, dtype=np.uint64)
+    pos = np.sort(rng.choice(10 ** 9, size=m, replace=False)).astype(np.uint64)
+    q = np.concatenate([key[rng.integers(0, m, size=nq // 2)],
+                        rng.integers(0, 1 << (2 * k), size=nq - nq // 2, dtype=np.uint64)])
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    ho_w, hp_w = O.lookup(q, k, bits, wo, wf, wp)
+    for kw in ({}, {"hit_cap": len(hp_w) // 2}):
+        ho, hp, t = _gpu_lookup(key, pos, q, k, bits, **kw)
+        assert t == len(hp_w)
+        assert np.array_equal(ho[: nq + 1], ho_w)
+        c = kw.get("hit_cap", t)
+        assert np.array_equal(hp[:c], hp_w[:c])
