@@ -49,6 +49,9 @@ SURVEY_OPS_PER_BASE = {19: 65, 15: 35}
 # N>1 seed-table exchange: "p2p" = partition fused with the all-to-all over symmetric memory
 # (dist.exchange_seedtable_p2p, the product); "nccl" = partition + NCCL all_to_all_single
 EXCHANGE = os.environ.get("MZS_EXCHANGE", "p2p")
+# MZS_FUSED_HIST=0: the table counts its first pass itself instead of taking the minimizer
+# kernel's fused histogram (mz_out.hist; A/B switch)
+FUSED_HIST = os.environ.get("MZS_FUSED_HIST", "1") != "0"
 SM_COUNT, INT32_LANES_PER_SM_CLK = 148, 128   # 4 SMSPs x 32 lanes issue (B200_PROFILING / B300_MICROARCH)
 
 
@@ -573,6 +576,10 @@ def main():
                 self.pos_out = torch.empty(cap, dtype=torch.uint64, device=dev)
                 self.fp_out = torch.empty(cap, dtype=torch.uint32, device=dev)
                 self.pos32_out = None   # (e2e) the 32-bit position table, allocated on first use
+                # the table's first radix pass digit counts, accumulated by the minimizer kernel
+                # while it writes the records (mz_out.hist): the first pass skips its upsweep
+                self.hist = (torch.empty(P.seedtable_hist_words(cap, bits), dtype=torch.uint32, device=dev)
+                             if FUSED_HIST else None)
 
     B0 = Bufs()
     d_count = B0.d_count
@@ -589,6 +596,7 @@ def main():
         P.mz_extract_ex(bf.words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=bf.inval, pos_base=sh.base_lo,
                         win_lo=sh.win_lo, win_hi=sh.win_hi, capacity=cap, out_hash=bf.out_h, out_pos=bf.out_p,
                         d_count=bf.d_count, ws=bf.mz_ws, out_items=bf.out_i,
+                        out_hist=bf.hist if world == 1 else None, hist_bits=bits,
                         keymode=P.MZ_KEY_CANON if args.canonical else P.MZ_KEY_HASH)
         if record:
             e[2].record(st)
@@ -596,12 +604,13 @@ def main():
             # seedtable_build_items32: positions mod 2^32, exact here (C3 < 2^32 bases)
             if bf.pos32_out is None:
                 bf.pos32_out = torch.empty(cap, dtype=torch.uint32, device=dev)
-            P.seedtable_build_items32(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count,
-                                      offsets=bf.offsets, pos_out=bf.pos32_out, fp_out=bf.fp_out, ws=bf.st_ws)
+            P.seedtable_build_items_ex(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count, hist=bf.hist,
+                                       pos32=True, offsets=bf.offsets, pos_out=bf.pos32_out, fp_out=bf.fp_out,
+                                       ws=bf.st_ws)
             res = (bf.offsets, bf.pos32_out)
         elif world == 1:
-            P.seedtable_build_items(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count,
-                                    offsets=bf.offsets, pos_out=bf.pos_out, fp_out=bf.fp_out, ws=bf.st_ws)
+            P.seedtable_build_items_ex(bf.out_i, bf.out_h, bf.out_p, k, bits, m=cap, d_m=bf.d_count, hist=bf.hist,
+                                       offsets=bf.offsets, pos_out=bf.pos_out, fp_out=bf.fp_out, ws=bf.st_ws)
             res = (bf.offsets, bf.pos_out)
         else:
             # the record count stays on the device (capacity-sized arrays + d_count) up to the
@@ -617,7 +626,7 @@ def main():
 
     # encode + mz + seed table: path-select kernel, 3 narrow passes x (upsweep, chunk scan, digit
     # scan, downsweep), 3 wide passes (enqueued, gated off at entry), 4 pointer-table kernels
-    table_launches = 1 + 12 + 12 + 4
+    table_launches = 1 + 12 + 12 + 4 - (1 if FUSED_HIST else 0)
     # N>1: count, partition (NCCL: ctl + 4 narrow + 4 wide; p2p: ctl + 3 scan kernels + the fused
     # nsweep writing into the peers), finalize (ctl + 2 passes x 12 + 4)
     part = 5 if EXCHANGE == "p2p" else 1 + 4 + 4

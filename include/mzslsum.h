@@ -179,6 +179,17 @@ typedef struct mz_out {
   uint64_t* items;           /* device, capacity entries, or NULL: packed seed-table items
                                 fp(hash) << 32 | (pos mod 2^32), fp = the top 32 bits of the
                                 2k-bit key (seedtable_build_items' input)            */
+  uint32_t* hist;            /* device, or NULL: the digit counts of the seed table's FIRST
+                                radix pass over the written records (the first pass's
+                                "upsweep", fused into extraction; seedtable_build_items_ex's
+                                `hist`).  seedtable_hist_words(capacity, hist_bucket_bits)
+                                uint32 words; zeroed and filled by mz_extract_ex.  Layout:
+                                hist[d * nchunks + c] = number of records r < min(count,
+                                capacity) with r in chunk c (chunks of the seed table's radix
+                                chunk size for m = capacity) and digit d = bits
+                                [32 - bucket_bits, 40 - bucket_bits) of fp (the least
+                                significant 8 bits of the bucket, as many as it has).  */
+  int hist_bucket_bits;      /* bucket_bits of the table the hist is for (1..min(2k,30))  */
 } mz_out_t;
 
 /* scratch for mz_extract_ex on n bases (tile descriptors + packed copy for ASCII) */
@@ -232,6 +243,22 @@ int seedtable_build_items(const uint64_t* items, const uint64_t* hash, const uin
 int seedtable_build_items32(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
                             const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets,
                             uint32_t* fp_out, uint32_t* pos32_out, void* ws, size_t ws_bytes, void* stream);
+
+/* Size (uint32 words) of mz_out.hist for a table of `bucket_bits` built from `capacity` records
+ * (m = capacity in seedtable_build_items_ex). */
+size_t seedtable_hist_words(uint64_t capacity, int bucket_bits);
+/* seedtable_build_items / seedtable_build_items32 in one call, optionally starting from the first
+ * pass's digit counts that mz_extract_ex accumulated while writing the records (out->hist,
+ * out->hist_bucket_bits == bucket_bits, out->capacity == m): the first pass then skips its own
+ * count of the items (one read of 8 B per entry).  hist may be NULL (the counts are taken
+ * here).  Exactly one of pos_out (uint64) / pos32_out (uint32, positions mod 2^32, R34) is
+ * non-NULL.  Same preconditions, workspace and output as seedtable_build_items.  The hist is
+ * only used by the packed-item path; the wide path (positions spanning >= 2^32) counts
+ * itself. */
+int seedtable_build_items_ex(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                             const uint64_t* d_m, int k, int bucket_bits, const uint32_t* hist,
+                             uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out, uint32_t* pos32_out,
+                             void* ws, size_t ws_bytes, void* stream);
 
 /* Multi-GPU phases (owner(bucket) = bucket >> (bucket_bits - log2 nranks); nranks a
  * power of two; NCCL all_reduce / all_to_all run between these calls):

@@ -42,7 +42,8 @@ class MzIn(ctypes.Structure):
 
 class MzOut(ctypes.Structure):
     _fields_ = [("hash", ctypes.c_void_p), ("pos", ctypes.c_void_p), ("capacity", ctypes.c_uint64),
-                ("d_count", ctypes.c_void_p), ("items", ctypes.c_void_p)]
+                ("d_count", ctypes.c_void_p), ("items", ctypes.c_void_p), ("hist", ctypes.c_void_p),
+                ("hist_bucket_bits", ctypes.c_int)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -76,6 +77,9 @@ _st_build_items = _sig("seedtable_build_items", _i32, _vp, _vp, _vp, _u64, _vp, 
                        _vp)
 _st_build_items32 = _sig("seedtable_build_items32", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp,
                          _sz, _vp)
+_st_hist_words = _sig("seedtable_hist_words", _sz, _u64, _i32)
+_st_build_items_ex = _sig("seedtable_build_items_ex", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp,
+                          _vp, _vp, _sz, _vp)
 _st_count = _sig("seedtable_count", _i32, _vp, _u64, _vp, _i32, _i32, _vp, _vp)
 _st_part_ws = _sig("seedtable_partition_workspace_bytes", _sz, _u64, _i32)
 _st_part = _sig("seedtable_partition", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
@@ -194,10 +198,12 @@ def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, ki
                   capacity: int | None = None, out_hash: torch.Tensor | None = None,
                   out_pos: torch.Tensor | None = None, d_count: torch.Tensor | None = None,
                   ws: torch.Tensor | None = None, stream=None, path: int = 0,
-                  out_items: torch.Tensor | None = None):
+                  out_items: torch.Tensor | None = None, out_hist: torch.Tensor | None = None,
+                  hist_bits: int = 0):
     """Asynchronous minimizer extraction; returns (hash, pos, d_count) device tensors (count on device).
     out_items (uint64, capacity entries, optional) also receives the packed seed-table items
-    (seedtable_build_items)."""
+    (seedtable_build_items); out_hist (uint32, seedtable_hist_words(capacity, hist_bits)) the
+    first radix pass's digit counts of a table of `hist_bits` buckets (seedtable_build_items_ex)."""
     if n is None:
         n = seq.numel() if kind == MZ_IN_ASCII else seq.numel() * 32
     span = k + w - 1
@@ -223,10 +229,12 @@ def mz_extract_ex(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, ki
         _need(t, name, torch.uint64, capacity, allow_none=name == "out_items")
     _need(d_count, "d_count", torch.uint64, 1)
     _need(read_off, "read_off", torch.uint64, 2, allow_none=True)
+    if out_hist is not None:
+        _need(out_hist, "out_hist", torch.uint32, seedtable_hist_words(capacity, hist_bits))
     if ws.numel() < mz_workspace_bytes(n, k, w, kind):
         raise ValueError("ws smaller than mz_workspace_bytes")
     mi = MzIn(kind, _ptr(seq), _ptr(invalid), n, _ptr(read_off), nreads, pos_base, win_lo, win_hi)
-    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count), _ptr(out_items))
+    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count), _ptr(out_items), _ptr(out_hist), hist_bits)
     if path == 0:      # the declared entry point (automatic kernel choice)
         _check(_mz_extract_ex(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
                               _stream(stream)), "mz_extract_ex")
@@ -329,6 +337,39 @@ def seedtable_build_items32(items: torch.Tensor, hash_: torch.Tensor, pos: torch
     _need(pos_out, "pos_out", torch.uint32, m)
     _check(_st_build_items32(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(offsets), _ptr(fp_out),
                              _ptr(pos_out), _ptr(ws), ws.numel(), _stream(stream)), "seedtable_build_items32")
+    return offsets, pos_out, fp_out
+
+
+def seedtable_hist_words(capacity: int, bits: int) -> int:
+    return int(_st_hist_words(capacity, bits))
+
+
+def seedtable_build_items_ex(items: torch.Tensor, hash_: torch.Tensor, pos: torch.Tensor, k: int, bits: int, *,
+                             m: int | None = None, d_m: torch.Tensor | None = None, hist: torch.Tensor | None = None,
+                             pos32: bool = False, with_fp: bool = True, offsets: torch.Tensor | None = None,
+                             pos_out: torch.Tensor | None = None, fp_out: torch.Tensor | None = None,
+                             ws: torch.Tensor | None = None, stream=None):
+    """seedtable_build_items(32) starting from mz_extract_ex's first-pass digit counts (out_hist,
+    made with capacity == m and hist_bits == bits); hist=None counts here."""
+    if m is None:
+        m = hash_.numel()
+    dev = hash_.device
+    if offsets is None:
+        offsets = torch.empty((1 << bits) + 1, dtype=torch.uint64, device=dev)
+    if pos_out is None:
+        pos_out = torch.empty(max(1, m), dtype=torch.uint32 if pos32 else torch.uint64, device=dev)
+    if fp_out is None and with_fp:
+        fp_out = torch.empty(max(1, m), dtype=torch.uint32, device=dev)
+    if ws is None:
+        ws = _ws(seedtable_workspace_bytes(max(1, m), bits), dev)
+    _table_checks(hash_, pos, m, d_m, bits, offsets, None, fp_out, ws)
+    _need(items, "items", torch.uint64, m)
+    _need(pos_out, "pos_out", torch.uint32 if pos32 else torch.uint64, m)
+    _need(hist, "hist", torch.uint32, seedtable_hist_words(m, bits), allow_none=True)
+    p64, p32 = (None, pos_out) if pos32 else (pos_out, None)
+    _check(_st_build_items_ex(_ptr(items), _ptr(hash_), _ptr(pos), m, _ptr(d_m), k, bits, _ptr(hist), _ptr(offsets),
+                              _ptr(fp_out), _ptr(p64), _ptr(p32), _ptr(ws), ws.numel(), _stream(stream)),
+           "seedtable_build_items_ex")
     return offsets, pos_out, fp_out
 
 

@@ -74,6 +74,21 @@ struct TempWs {
   ~TempWs() { if (p) cudaFreeAsync(p, s); }
 };
 
+// ---------------------------------------------------------------- radix chunk layout
+// The seed-table radix passes cut their m entries into chunks (one downsweep CTA each): at
+// most 131072 entries, at least 4096, and about m/296 in between so that small tables still
+// spread over the SMs.  A pass's digit counts are laid out counts[digit * nchunks + chunk]
+// with nchunks = ceil(m / chunk).  mz_extract_ex's first-pass histogram (mz_out.hist) uses the
+// same layout with m = its capacity, so seedtable_build_items_ex can start from it.
+constexpr uint32_t kRadixChunkMax = 131072;
+constexpr uint32_t kRadixChunkMin = 4096;
+inline uint32_t radix_chunk_for(uint64_t m) {
+  const uint64_t want = (m + 295) / 296;
+  const uint64_t c = (want + kRadixChunkMin - 1) / kRadixChunkMin * kRadixChunkMin;
+  return (uint32_t)(c < kRadixChunkMin ? kRadixChunkMin : (c > kRadixChunkMax ? kRadixChunkMax : c));
+}
+inline uint64_t radix_nchunks(uint64_t m) { return (m + radix_chunk_for(m) - 1) / radix_chunk_for(m); }
+
 // ---------------------------------------------------------------- shared host entry points
 // (seedtable.cu) stable sort of (u32 fingerprint, u64 index) pairs by fingerprint bits
 // [lo_bit, 32), used by the sorted seed lookup

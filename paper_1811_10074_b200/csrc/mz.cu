@@ -91,6 +91,13 @@ struct MzArgs {
   uint64_t ntiles;
   uint32_t tw;               // windows per tile
   const uint64_t* ridx;      // coarse read index (kRidxShift), or nullptr
+  // first radix pass digit counts of the seed table (mz_out.hist) or nullptr: record r adds 1
+  // to hist[((fp >> hist_sh) & hist_mask) * hist_nch + r / hist_chunk]
+  uint32_t* hist;
+  uint64_t hist_nch;
+  uint32_t hist_chunk;
+  int hist_sh;
+  uint32_t hist_mask;
 };
 // ridx[b] = first read r in [0, nreads+1] with read_off[r] >= b * 2^kRidxShift: brackets every
 // read-start search to the reads of one 8 kbp block (a few loads instead of ~20 dependent ones)
@@ -561,7 +568,9 @@ __device__ __forceinline__ void phase3_output(const MzArgs& a, uint64_t tile, in
     const uint64_t h = key_at<H64>(a, q);
     a.out_hash[oo] = h;
     a.out_pos[oo] = a.pos_base + (uint64_t)q;
-    if (a.out_items) a.out_items[oo] = item_of(h, a.k, a.pos_base + (uint64_t)q);
+    const uint64_t it = item_of(h, a.k, a.pos_base + (uint64_t)q);
+    if (a.out_items) a.out_items[oo] = it;
+    if (a.hist) atomicAdd(&a.hist[(((uint32_t)(it >> 32) >> a.hist_sh) & a.hist_mask) * a.hist_nch + oo / a.hist_chunk], 1u);
   }
 }
 
@@ -688,12 +697,19 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
   }
 }
 
+#define G_TPB_OF(W) (FastGeom<W>::TPB)
 // Output of one finished super-tile (fast path): its emit bitmask -> ordered slot list in
 // `list` -> prefix via look-back -> records.  Called one super-tile LATE (see the kernel), so
 // the look-back finds its predecessors' aggregates already published.
 template <int W, bool H64, int KK, bool CN>
 __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, const uint32_t* emit, uint32_t excl,
-                                            uint32_t total, uint16_t* list, uint64_t* bcast) {
+                                            uint32_t total, uint16_t* list, uint64_t* bcast, uint32_t* shist) {
+  // shist[2][256]: this super-tile's first-radix-pass digit counts (a.hist) in the two radix
+  // chunks its records can touch (c0 = base / chunk and c0 + 1), flushed with one global atomic
+  // per non-zero counter; records past chunk c0 + 1 (only with chunks smaller than a
+  // super-tile's records, i.e. small capacities) add to the global counts directly
+  if (a.hist)
+    for (int i = threadIdx.x; i < 512; i += G_TPB_OF(W)) shist[i] = 0;
   using G = FastGeom<W>;
   constexpr int NSWT = G::SUBS * G::NSW;
   constexpr int WPT = (NSWT + G::TPB - 1) / G::TPB;
@@ -718,11 +734,18 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
     const uint64_t off = lookback_resolve(a.status, tile, total);
     if (lane_id() == 0) {
       *bcast = off;
+      // chunks are multiples of 4096 entries and off < 2^44: a 32-bit division
+      if (a.hist) bcast[1] = (uint32_t)(off >> 12) / (a.hist_chunk >> 12);
       if (tile == a.ntiles - 1) *a.d_count = off + total;
     }
   }
   __syncthreads();
   const uint64_t base = *bcast;
+  const uint64_t hc0 = a.hist ? bcast[1] : 0;
+  // record i of this super-tile lies in chunk c0 + 1 iff i >= i1 (i < total < 2^16)
+  const uint32_t i1 = (uint32_t)min((hc0 + 1) * a.hist_chunk - base, (uint64_t)0xffffffffu);
+  // records past chunk c0 + 1 exist only with chunks smaller than a super-tile's records
+  const bool hist_far = a.hist && (uint64_t)i1 + a.hist_chunk < total;
   const int64_t super_lo = (int64_t)tile * (G::SUBS * G::TW);
   // four records per thread per step: their word loads are all in flight before the hashes
   const uint32_t lim = (uint32_t)min((uint64_t)total, a.capacity > base ? a.capacity - base : (uint64_t)0);
@@ -750,11 +773,26 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
         MZS_DCHECK(base + i < a.capacity && q[u] >= 0 && (uint64_t)q[u] < a.n);
         a.out_hash[base + i] = h;
         a.out_pos[base + i] = a.pos_base + (uint64_t)q[u];
-        if (a.out_items) a.out_items[base + i] = item_of(h, KK ? KK : a.k, a.pos_base + (uint64_t)q[u]);
+        const uint64_t it = item_of(h, KK ? KK : a.k, a.pos_base + (uint64_t)q[u]);
+        if (a.out_items) a.out_items[base + i] = it;
+        if (a.hist) {
+          const uint32_t d = ((uint32_t)(it >> 32) >> a.hist_sh) & a.hist_mask;
+          if (!hist_far || i < i1 + a.hist_chunk) atomicAdd(&shist[(i >= i1 ? 256 : 0) + d], 1u);
+          else atomicAdd(&a.hist[d * a.hist_nch + (base + i) / a.hist_chunk], 1u);
+        }
       }
     }
   }
   __syncthreads();  // `list` and `emit` are reused next
+  if (a.hist) {
+    // each thread flushes the counters it zeroed (same indices: no barrier needed before the
+    // next super-tile's zeroing)
+    for (int i = threadIdx.x; i < 512; i += G::TPB) {
+      const uint32_t v = shist[i];
+      const uint64_t c = hc0 + (i >> 8);
+      if (v && c < a.hist_nch) atomicAdd(&a.hist[(uint64_t)(i & 255) * a.hist_nch + c], v);
+    }
+  }
 }
 
 // Persistent: every CTA claims super-tiles in order (atomic counter), computes phases 1-2 of
@@ -777,8 +815,9 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   constexpr int DW = (G::NS + 64 + 64) / 1024 + 3;
   __shared__ uint32_t dwm[2][DW];
   __shared__ uint64_t warp_sums[G::TPB / 32];
-  __shared__ uint64_t bcast;
+  __shared__ uint64_t bcast[2];
   __shared__ uint32_t s_tile;
+  __shared__ uint32_t shist[512];  // first radix pass digit counts of one super-tile (a.hist)
   // the read starts inside the current super-tile's bases (segmented input), found once per
   // super-tile by warp 0; s_nrs < 0: more than 31 (the sub-tiles search global memory)
   __shared__ int64_t s_rs[32];
@@ -892,7 +931,7 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
     if (t == 0) lookback_publish(a.status, tile, total);
     if (pend >= 0)
       fast_output<W, H64, KK, CN>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
-                              reinterpret_cast<uint16_t*>(keys), &bcast);
+                              reinterpret_cast<uint16_t*>(keys), bcast, shist);
     pend = (int64_t)tile;
     pend_excl = excl;
     pend_total = (uint32_t)total;
@@ -900,7 +939,7 @@ __global__ void __launch_bounds__(256, 3) mz_fast_kernel(MzArgs a) {
   }
   if (pend >= 0)
     fast_output<W, H64, KK, CN>(a, (uint64_t)pend, emit[cur ^ 1], pend_excl, pend_total,
-                            reinterpret_cast<uint16_t*>(keys), &bcast);
+                            reinterpret_cast<uint16_t*>(keys), bcast, shist);
 }
 
 // ------------------------------------------------------------------ generic path kernel
@@ -1111,6 +1150,8 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   const uint64_t span = (uint64_t)k + (uint64_t)w - 1;
   if (n < span || in->win_lo >= in->win_hi) {
     MZS_CUDA(cudaMemsetAsync(out->d_count, 0, sizeof(uint64_t), st));
+    if (out->hist && out->capacity)
+      MZS_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(uint32_t) * 256 * radix_nchunks(out->capacity), st));
     return SLSUM_OK;
   }
   if (!in->seq) return SLSUM_EINVAL;
@@ -1162,6 +1203,18 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   a.out_items = out->items;
   a.capacity = out->capacity;
   a.d_count = out->d_count;
+  if (out->hist) {
+    // the seed table's first radix pass: digit = the low 8 bits of the bucket (fp bits
+    // [32 - bits, 40 - bits)), chunks as seedtable_build_items_ex lays them out for m = capacity
+    const int bits = out->hist_bucket_bits;
+    if (bits < 1 || bits > 30 || bits > 2 * k || out->capacity == 0) return SLSUM_EINVAL;
+    a.hist = out->hist;
+    a.hist_chunk = radix_chunk_for(out->capacity);
+    a.hist_nch = radix_nchunks(out->capacity);
+    a.hist_sh = 32 - bits;
+    a.hist_mask = (1u << (bits < 8 ? bits : 8)) - 1u;
+    MZS_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(uint32_t) * 256 * a.hist_nch, st));
+  }
   return launch_mz(a, path, st);
 }
 

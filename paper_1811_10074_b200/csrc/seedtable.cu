@@ -24,6 +24,9 @@ namespace {
 #ifndef MZS_RANK_SYNCWARP
 #define MZS_RANK_SYNCWARP 1
 #endif
+#ifndef MZS_RANK_BALLOT
+#define MZS_RANK_BALLOT 0
+#endif
 constexpr int kTPB = 256;
 constexpr int kNW = kTPB / 32;
 
@@ -50,8 +53,8 @@ __device__ __forceinline__ uint64_t block_count(const uint64_t* d_m, uint64_t m_
 // (per-warp peer bit tables + per-warp counters, nsweep_kernel), stages them in digit order
 // in shared memory and writes each digit run contiguously.
 constexpr int kStages = 2;                  // TMA ring depth (sub-tiles in flight per CTA)
-constexpr int kChunk = 131072;              // entries per chunk (at most; see chunk_for)
-constexpr int kMinChunk = 4096;             // and at least: whole tiles of every kernel
+constexpr int kChunk = kRadixChunkMax;      // entries per chunk (at most; see chunk_for)
+constexpr int kMinChunk = kRadixChunkMin;   // and at least: whole tiles of every kernel
 
 // Path gate: the narrow (packed u64) and wide (u32 fp + u64 pos) passes are both enqueued;
 // each kernel runs only if ctl[0] selects its path (ctl == nullptr: always run).  ctl[0] is
@@ -214,7 +217,7 @@ struct NSmem {
   uint64_t gbase[256];       // staged entry j of digit d goes to gbase[d] + j
   uint32_t wcnt[NW][256];    // per-warp digit counters -> per-warp exclusive offsets
   uint32_t dummy[NW][32];    // atomic targets of non-leader lanes (branch-free ranking)
-  uint32_t pm[NW][peer_tables<TPB, T / TPB>()][256];  // per-warp peer bit tables
+  uint32_t pm[NW][MZS_RANK_BALLOT ? 1 : peer_tables<TPB, T / TPB>()][MZS_RANK_BALLOT ? 1 : 256];  // per-warp peer bit tables
   uint32_t ws2[NW > 8 ? NW : 8];  // per-warp digit-scan totals
 };
 
@@ -275,7 +278,8 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
   if (td < 256) S.run_off[td] = dbase[td] + offsets[(uint64_t)td * nchunks + c];
   for (uint32_t i = td; i < NW * 256; i += TPB) (&S.wcnt[0][0])[i] = 0;
   constexpr int kPeerTables = peer_tables<TPB, IPT>();
-  for (uint32_t i = td; i < NW * kPeerTables * 256; i += TPB) (&S.pm[0][0][0])[i] = 0;
+  if (!MZS_RANK_BALLOT)
+    for (uint32_t i = td; i < NW * kPeerTables * 256; i += TPB) (&S.pm[0][0][0])[i] = 0;
   if (td == 0) {
     for (int b = 0; b < kStages; ++b) mbar_init(&S.mbar[b], 1);
     fence_mbar_init();
@@ -337,8 +341,33 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
       // atomics of different lanes commute.  kPeerTables items share one round of syncwarps
       // (one table each), so their shared-memory round trips overlap.  ~20 SASS per item
       // instead of ~60 for an 8-ballot multi-split (tools/microbench_rank.cu).
-      uint32_t (*pm)[256] = S.pm[wid];
       unsigned peers[IPT];
+#if MZS_RANK_BALLOT
+#pragma unroll
+      for (int it = 0; it < IPT; ++it) {
+        const uint32_t j = wid * (IPT * 32) + it * 32 + lane;
+        if constexpr (WD) {
+          uint32_t f;
+          if constexpr (IN == kInHashPos) f = fingerprint(S.ring[b].a[j], k);
+          else f = S.ring[b].a[j];
+          item[it] = (uint64_t)f << 32;
+          ipos[it] = S.ring[b].p[j];
+        } else {
+          item[it] = make_item<IN, T>(S.ring[b], j, k, p0, bad);
+        }
+        const bool valid = kWhole || j < nvalid;
+        const uint32_t d = (uint32_t)(item[it] >> dsh) & dmask;
+        unsigned p = kWhole ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) {
+          const bool bit = (d >> bb) & 1u;
+          const unsigned mm = __ballot_sync(0xffffffffu, bit);
+          p &= bit ? mm : ~mm;
+        }
+        peers[it] = valid ? p : (1u << lane);
+      }
+#else
+      uint32_t (*pm)[256] = S.pm[wid];
 #pragma unroll
       for (int g = 0; g < IPT; g += kPeerTables) {
 #pragma unroll
@@ -371,6 +400,7 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
             atomicXor(&pm[u][(uint32_t)(item[it] >> dsh) & dmask], 1u << lane);
         }
       }
+#endif
       // per-warp digit counters, in item order: the lowest peer adds the peer count (every
       // other lane adds 0 to its own dummy word, so there is no branch); the old value is
       // broadcast to the peers.  The leaders of one digit in two item rounds can be different
@@ -698,11 +728,7 @@ struct SortWs {
 // about 296 CTAs (2 per SM) share the passes instead of a handful working through 128K
 // entries each (C1's 1.9e5 entries were 2 chunks).  A function of m only (no device query), so
 // the workspace size and the carve agree.
-uint32_t chunk_for(uint64_t m) {
-  const uint64_t want = (m + 295) / 296;
-  const uint64_t c = (want + kMinChunk - 1) / kMinChunk * kMinChunk;
-  return (uint32_t)std::min<uint64_t>(kChunk, std::max<uint64_t>(kMinChunk, c));
-}
+uint32_t chunk_for(uint64_t m) { return radix_chunk_for(m); }
 uint64_t chunks_for(uint64_t m) { return (m + chunk_for(m) - 1) / chunk_for(m) + 1; }
 
 template <class C>
@@ -751,13 +777,17 @@ int env_int(const char* name, int dflt) {
 }
 
 // One reduce-then-scan pass: upsweep (digit counts per chunk) + chunk scan + digit scan.
+// counts_in: the pass's digit counts computed elsewhere (mz_extract_ex's fused histogram,
+// mz_out.hist), in the upsweep's layout; the upsweep is then skipped.
 template <int IN>
 int count_pass(const void* kin, const uint64_t* d_m, uint64_t m, int k, int sh, int nb, uint64_t nch, SortWs& s,
-               int want, cudaStream_t st) {
-  const unsigned grid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms() * 8);
-  upsweep_kernel<IN><<<grid, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want, s.chunk);
-  MZS_LAUNCHED();
-  chunk_scan_kernel<<<256, kTPB, 0, st>>>(s.counts, nch, s.offs, s.totals, s.ctl, want);
+               int want, cudaStream_t st, const uint32_t* counts_in = nullptr) {
+  if (!counts_in) {
+    const unsigned grid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms() * 8);
+    upsweep_kernel<IN><<<grid, kTPB, 0, st>>>(kin, d_m, m, k, sh, nb, s.counts, nch, s.ctl, want, s.chunk);
+    MZS_LAUNCHED();
+  }
+  chunk_scan_kernel<<<256, kTPB, 0, st>>>(counts_in ? counts_in : s.counts, nch, s.offs, s.totals, s.ctl, want);
   MZS_LAUNCHED();
   digit_scan_kernel<<<1, 256, 0, st>>>(s.totals, s.dbase, s.ctl, want);
   MZS_LAUNCHED();
@@ -795,7 +825,8 @@ int launch_nsweep_cfg(int cfg, const void* a_in, const uint64_t* p_in, void* a_o
 // ctl_kernel.  After the call s.totals holds the digit totals of the LAST pass.
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st,
-                const uint64_t* items = nullptr, uint32_t* pos32_dst = nullptr) {
+                const uint64_t* items = nullptr, uint32_t* pos32_dst = nullptr, const uint32_t* hist0 = nullptr) {
+  // hist0 (with items): the first narrow pass's digit counts, from mz_extract_ex (mz_out.hist)
   // pos32_dst (packed items only): the final positions as u32 (pos mod 2^32) instead of pos_dst
   const int npass = (hi_bit - lo_bit + 7) / 8;
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
@@ -823,7 +854,7 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     if (items) {
       // pre-packed items (mz_extract_ex's out->items, positions ascending): pass 0 is an
       // ordinary 8-byte item pass; the hash/pos arrays serve only the wide path
-      rc = count_pass<2>(items, d_m, m, k, lo_bit, nb, nch, s, 1, st);
+      rc = count_pass<2>(items, d_m, m, k, lo_bit, nb, nch, s, 1, st, hist0);
       if (rc) return rc;
       const int tma_it = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
       rc = npass != 1 ? launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
@@ -957,7 +988,7 @@ MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
 static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
                                 const uint64_t* d_m, int k, int bucket_bits, uint64_t* offsets, uint32_t* fp_out,
                                 uint64_t* pos_out, void* ws, size_t ws_bytes, void* stream,
-                                uint32_t* pos32_out = nullptr) {
+                                uint32_t* pos32_out = nullptr, const uint32_t* hist0 = nullptr) {
   if (k < 1 || k > 31 || bucket_bits < 1 || bucket_bits > 30 || bucket_bits > 2 * k) return SLSUM_EINVAL;
   if (!offsets || (m && (!hash || !pos || (!pos_out && !pos32_out)))) return SLSUM_EINVAL;
   cudaStream_t st = as_stream(stream);
@@ -983,7 +1014,8 @@ static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, con
   if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
-  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items, pos32_out);
+  int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items, pos32_out,
+                       items ? hist0 : nullptr);
   if (rc) return rc;
   return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st);
 }
@@ -1009,6 +1041,21 @@ MZS_API int seedtable_build_items32(const uint64_t* items, const uint64_t* hash,
   if (m && (!items || !pos32_out)) return SLSUM_EINVAL;
   return seedtable_build_impl(items, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, nullptr, ws, ws_bytes,
                               stream, pos32_out);
+}
+
+MZS_API size_t seedtable_hist_words(uint64_t capacity, int bucket_bits) {
+  (void)bucket_bits;
+  return capacity ? (size_t)256 * radix_nchunks(capacity) : 0;
+}
+
+MZS_API int seedtable_build_items_ex(const uint64_t* items, const uint64_t* hash, const uint64_t* pos, uint64_t m,
+                                     const uint64_t* d_m, int k, int bucket_bits, const uint32_t* hist,
+                                     uint64_t* offsets, uint32_t* fp_out, uint64_t* pos_out, uint32_t* pos32_out,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  if ((pos_out != nullptr) == (pos32_out != nullptr)) return SLSUM_EINVAL;
+  if (m && !items) return SLSUM_EINVAL;
+  return seedtable_build_impl(items, hash, pos, m, d_m, k, bucket_bits, offsets, fp_out, pos_out, ws, ws_bytes,
+                              stream, pos32_out, hist);
 }
 
 MZS_API int seedtable_count(const uint64_t* hash, uint64_t m, const uint64_t* d_m, int k, int bucket_bits,

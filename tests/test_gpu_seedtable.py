@@ -286,3 +286,53 @@ def test_items32_wide_spans_and_bit_widths(npass_bits):
         assert np.array_equal(off.cpu().numpy(), wo), step
         assert np.array_equal(po.cpu().numpy(), (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32)), step
         assert np.array_equal(fp.cpu().numpy(), wf), step
+
+
+def _hist_oracle(wk, k, bits, cap):
+    """The first radix pass's digit counts, from the ORACLE records: chunks of the radix chunk
+    size for m = cap (at most 131072 entries, at least 4096, ~cap/296 rounded up to 4096
+    between), digit = the low min(8, bits) bits of the bucket fp >> (32 - bits)."""
+    want = (cap + 295) // 296
+    chunk = min(131072, max(4096, (want + 4095) // 4096 * 4096))
+    nch = (cap + chunk - 1) // chunk
+    d = (_fp_np(wk, k) >> np.uint64(32 - bits)) & np.uint64((1 << min(8, bits)) - 1)
+    c = np.arange(len(wk), dtype=np.uint64) // np.uint64(chunk)
+    h = np.zeros((256, nch), dtype=np.int64)
+    np.add.at(h, (d.astype(np.int64), c.astype(np.int64)), 1)
+    return h.reshape(-1), nch
+
+
+@pytest.mark.parametrize("k,bits,cap,path", [(19, 24, 200_000, 0), (19, 24, 40_000_000, 0), (15, 24, 40_000_000, 0),
+                                             (15, 6, 150_000, 0), (19, 24, 150_000, 1), (19, 16, 40_000_000, 1),
+                                             (19, 24, 60_000, 0)])
+def test_fused_first_pass_histogram(k, bits, cap, path):
+    """mz_extract_ex's fused first-pass histogram (mz_out.hist) equals the digit counts of the
+    oracle's records per radix chunk, and seedtable_build_items_ex started from it equals the
+    oracle table (Fig. 1).  cap = 40e6 takes 131072-entry chunks (a super-tile's
+    records touch <= 2 chunks: the shared-memory path); cap = 200k / 150k takes 4096-entry chunks
+    (records past the second chunk: the global-atomic path); cap = 60k < the count: only the
+    first cap records are counted.  path 1: the generic kernel."""
+    w = 10
+    seq = G.C3(n=700_000).ascii(0, 600_000)
+    st = torch.from_numpy(seq).cuda()
+    items = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    hist = torch.full((P.seedtable_hist_words(cap, bits),), 0xDEAD, dtype=torch.uint32, device="cuda")
+    h, p, c = P.mz_extract_ex(st, k, w, capacity=cap, out_items=items, out_hist=hist, hist_bits=bits, path=path)
+    torch.cuda.synchronize()
+    m = int(c.view(torch.int64).item())
+    wk, wp = O.mz(seq, k, w)
+    assert m == len(wk)
+    mw = min(m, cap)
+    want_h, nch = _hist_oracle(wk[:mw], k, bits, cap)
+    assert hist.numel() == 256 * nch
+    assert np.array_equal(hist.cpu().numpy().astype(np.int64), want_h)
+    if m > cap:
+        return
+    wo, wf, wpos = O.seedtable(wk, wp, k, bits)
+    for pos32 in (False, True):
+        off, po, fp = P.seedtable_build_items_ex(items, h, p, k, bits, m=cap, d_m=c, hist=hist, pos32=pos32)
+        torch.cuda.synchronize()
+        assert np.array_equal(off.cpu().numpy(), wo)
+        assert np.array_equal(fp[:m].cpu().numpy(), wf)
+        gp = po[:m].cpu().numpy()
+        assert np.array_equal(gp, (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32) if pos32 else wpos)

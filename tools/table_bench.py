@@ -23,7 +23,10 @@ P.mz_encode(seq, words, inval)
 del seq
 cap = int(0.25 * (n - k - w + 2)) + 1024
 items = torch.empty(cap, dtype=torch.uint64, device="cuda")
-h, p, c = P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, capacity=cap, out_items=items)
+fused = os.environ.get("MZS_FUSED_HIST", "1") != "0"   # the first pass's counts from the minimizer kernel
+hist = torch.empty(P.seedtable_hist_words(cap, bits), dtype=torch.uint32, device="cuda") if fused else None
+h, p, c = P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval, capacity=cap, out_items=items,
+                          out_hist=hist, hist_bits=bits)
 ws = torch.empty(P.seedtable_workspace_bytes(cap, bits), dtype=torch.uint8, device="cuda")
 off = torch.empty((1 << bits) + 1, dtype=torch.uint64, device="cuda")
 po = torch.empty(cap, dtype=torch.uint64, device="cuda")
@@ -31,7 +34,8 @@ fp = torch.empty(cap, dtype=torch.uint32, device="cuda")
 
 
 def run():
-    P.seedtable_build_items(items, h, p, k, bits, m=cap, d_m=c, offsets=off, pos_out=po, fp_out=fp, ws=ws)
+    P.seedtable_build_items_ex(items, h, p, k, bits, m=cap, d_m=c, hist=hist, offsets=off, pos_out=po, fp_out=fp,
+                               ws=ws)
 
 
 for _ in range(3):
@@ -47,5 +51,5 @@ for _ in range(reps):
     ts.append(a.elapsed_time(b))
 m = int(c.item())
 mix = (po[:m].view(torch.int64) * 0x9E3779B97F4A7C15 + fp[:m].view(torch.int32).to(torch.int64)).sum().item()
-print(f"LB={os.environ.get('MZS_LB', '1')} m={m} table ms: median {sorted(ts)[len(ts) // 2]:.3f} best {min(ts):.3f} "
+print(f"fused_hist={int(fused)} m={m} table ms: median {sorted(ts)[len(ts) // 2]:.3f} best {min(ts):.3f} "
       f"checksum {mix & 0xFFFFFFFFFFFFFFFF:016x} off_last {int(off[-1].item())}", flush=True)
