@@ -750,31 +750,41 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
   // four records per thread per step: their word loads are all in flight before the hashes
   const uint32_t lim = (uint32_t)min((uint64_t)total, a.capacity > base ? a.capacity - base : (uint64_t)0);
   constexpr int U = MZS_MZ_OUT_U;
+  // super_lo is a multiple of 32 (TW = 256 R), so a record's k-mer offset `rel` from the
+  // super-tile start gives its packed word (rel >> 5) and bit offset (rel & 31) relative to
+  // word super_lo / 32: 32-bit index math per record, 64-bit bases once per super-tile
+  static_assert((G::SUBS * G::TW) % 32 == 0, "super-tiles start on a packed word");
+  const uint64_t* wp = a.words + (super_lo >> 5);
+  // the word after an emitted k-mer's first is needed only when the k-mer crosses into it, so
+  // clamping its index to the last word (instead of a bounds test) is safe
+  const uint32_t wlast = (uint32_t)min(a.nwords - 1 - (uint64_t)(super_lo >> 5), (uint64_t)0xffffffffu);
+  uint64_t* const oh = a.out_hash + base;
+  uint64_t* const op = a.out_pos + base;
+  uint64_t* const oi = a.out_items ? a.out_items + base : nullptr;
+  const uint64_t p0 = a.pos_base + (uint64_t)super_lo;
   for (uint32_t i0 = threadIdx.x; i0 < lim; i0 += U * G::TPB) {
-    int64_t q[U];
+    uint32_t rel[U];
     uint64_t A[U], B[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * G::TPB;
-      const uint32_t rel = i < lim ? list[i] : 0u;
-      MZS_DCHECK(rel < (uint32_t)(G::SUBS * G::TW + W));
-      q[u] = super_lo + rel;
-      // an emitted k-mer lies in [0, n), so its first word exists; the next one is needed only
-      // when the k-mer crosses into it, so clamping its index (instead of a bounds test) is safe
-      const uint64_t wq = (uint64_t)max(q[u] >> 5, (int64_t)0);
-      A[u] = i < lim ? __ldg(a.words + wq) : 0ull;
-      B[u] = i < lim ? __ldg(a.words + min(wq + 1, a.nwords - 1)) : 0ull;
+      rel[u] = i < lim ? list[i] : 0u;
+      MZS_DCHECK(rel[u] < (uint32_t)(G::SUBS * G::TW + W));
+      const uint32_t wr = rel[u] >> 5;
+      A[u] = i < lim ? __ldg(wp + wr) : 0ull;
+      B[u] = i < lim ? __ldg(wp + min(wr + 1, wlast)) : 0ull;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t i = i0 + u * G::TPB;
       if (i < lim) {
-        const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, q[u], A[u], B[u]);
-        MZS_DCHECK(base + i < a.capacity && q[u] >= 0 && (uint64_t)q[u] < a.n);
-        a.out_hash[base + i] = h;
-        a.out_pos[base + i] = a.pos_base + (uint64_t)q[u];
-        const uint64_t it = item_of(h, KK ? KK : a.k, a.pos_base + (uint64_t)q[u]);
-        if (a.out_items) a.out_items[base + i] = it;
+        const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, (int64_t)rel[u], A[u], B[u]);
+        MZS_DCHECK(base + i < a.capacity && super_lo + rel[u] < a.n);
+        const uint64_t pos = p0 + rel[u];
+        oh[i] = h;
+        op[i] = pos;
+        const uint64_t it = item_of(h, KK ? KK : a.k, pos);
+        if (oi) oi[i] = it;
         if (a.hist) {
           const uint32_t d = ((uint32_t)(it >> 32) >> a.hist_sh) & a.hist_mask;
           if (!hist_far || i < i1 + a.hist_chunk) atomicAdd(&shist[(i >= i1 ? 256 : 0) + d], 1u);
