@@ -762,36 +762,41 @@ __device__ __forceinline__ void fast_output(const MzArgs& a, uint64_t tile, cons
   uint64_t* const op = a.out_pos + base;
   uint64_t* const oi = a.out_items ? a.out_items + base : nullptr;
   const uint64_t p0 = a.pos_base + (uint64_t)super_lo;
-  for (uint32_t i0 = threadIdx.x; i0 < lim; i0 += U * G::TPB) {
+  auto record = [&](uint32_t i, uint32_t rel, uint64_t A, uint64_t B) {
+    const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, (int64_t)rel, A, B);
+    MZS_DCHECK(base + i < a.capacity && super_lo + rel < a.n);
+    const uint64_t pos = p0 + rel;
+    oh[i] = h;
+    op[i] = pos;
+    const uint64_t it = item_of(h, KK ? KK : a.k, pos);
+    if (oi) oi[i] = it;
+    if (a.hist) {
+      const uint32_t d = ((uint32_t)(it >> 32) >> a.hist_sh) & a.hist_mask;
+      if (!hist_far || i < i1 + a.hist_chunk) atomicAdd(&shist[(i >= i1 ? 256 : 0) + d], 1u);
+      else atomicAdd(&a.hist[d * a.hist_nch + (base + i) / a.hist_chunk], 1u);
+    }
+  };
+  uint32_t i0 = threadIdx.x;
+  // full steps: all U records of the thread exist (no per-record guards), their word loads all
+  // in flight before the hashes
+  for (; i0 + (U - 1) * G::TPB < lim; i0 += U * G::TPB) {
     uint32_t rel[U];
     uint64_t A[U], B[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint32_t i = i0 + u * G::TPB;
-      rel[u] = i < lim ? list[i] : 0u;
+      rel[u] = list[i0 + u * G::TPB];
       MZS_DCHECK(rel[u] < (uint32_t)(G::SUBS * G::TW + W));
       const uint32_t wr = rel[u] >> 5;
-      A[u] = i < lim ? __ldg(wp + wr) : 0ull;
-      B[u] = i < lim ? __ldg(wp + min(wr + 1, wlast)) : 0ull;
+      A[u] = __ldg(wp + wr);
+      B[u] = __ldg(wp + min(wr + 1, wlast));
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = i0 + u * G::TPB;
-      if (i < lim) {
-        const uint64_t h = key_from_words<H64, KK, CN ? 1 : 0>(a, (int64_t)rel[u], A[u], B[u]);
-        MZS_DCHECK(base + i < a.capacity && super_lo + rel[u] < a.n);
-        const uint64_t pos = p0 + rel[u];
-        oh[i] = h;
-        op[i] = pos;
-        const uint64_t it = item_of(h, KK ? KK : a.k, pos);
-        if (oi) oi[i] = it;
-        if (a.hist) {
-          const uint32_t d = ((uint32_t)(it >> 32) >> a.hist_sh) & a.hist_mask;
-          if (!hist_far || i < i1 + a.hist_chunk) atomicAdd(&shist[(i >= i1 ? 256 : 0) + d], 1u);
-          else atomicAdd(&a.hist[d * a.hist_nch + (base + i) / a.hist_chunk], 1u);
-        }
-      }
-    }
+    for (int u = 0; u < U; ++u) record(i0 + u * G::TPB, rel[u], A[u], B[u]);
+  }
+  for (; i0 < lim; i0 += G::TPB) {
+    const uint32_t rel = list[i0];
+    const uint32_t wr = rel >> 5;
+    record(i0, rel, __ldg(wp + wr), __ldg(wp + min(wr + 1, wlast)));
   }
   __syncthreads();  // `list` and `emit` are reused next
   if (a.hist) {
