@@ -93,6 +93,10 @@ inline uint64_t radix_nchunks(uint64_t m) { return (m + radix_chunk_for(m) - 1) 
 // (seedtable.cu) stable sort of (u32 fingerprint, u64 index) pairs by fingerprint bits
 // [lo_bit, 32), used by the sorted seed lookup
 size_t sort_fp_idx_workspace_bytes(uint64_t m, int lo_bit);
+// (seedtable.cu) stable sort of packed u64 items by bits [lo_bit, hi_bit) of their high 32 bits
+size_t sort_items_workspace_bytes(uint64_t m, int lo_bit, int hi_bit);
+int sort_items(const uint64_t* items, uint64_t m, int lo_bit, int hi_bit, uint64_t* out, void* ws, size_t ws_bytes,
+               cudaStream_t st);
 int sort_fp_idx(const uint32_t* fp, const uint64_t* idx, uint64_t m, int lo_bit, uint32_t* fp_out, uint64_t* idx_out,
                 void* ws, size_t ws_bytes, cudaStream_t st);
 

@@ -21,6 +21,9 @@ namespace mzs {
 namespace {
 
 constexpr int kLTPB = 256;
+#ifndef MZS_LOOKUP_EMIT_UNROLL
+#define MZS_LOOKUP_EMIT_UNROLL 1
+#endif
 
 __device__ __forceinline__ uint32_t fp_of(uint64_t key, int k) {
   const int b = 2 * k;
@@ -118,6 +121,7 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
                                                         uint64_t* __restrict__ hit_pos, uint64_t hit_cap,
                                                         uint64_t* __restrict__ first) {
   const uint64_t nq = query_count(d_nq, nq_cap);
+  const uint64_t m_tab = EMIT && MZS_LOOKUP_EMIT_UNROLL ? offsets[(uint64_t)1 << bits] : 0;  // table entries
   for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
     if (EMIT) {
       uint64_t o = hit_off[i];
@@ -129,7 +133,21 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
       if (o < hit_cap) hit_pos[o] = pos_tab[e0];
       if (++o == o_end) continue;
       const uint32_t f = fp_of(q[i], k);
-      for (uint64_t e = e0 + 1; o < o_end; ++e) {
+      uint64_t e = e0 + 1;
+#if MZS_LOOKUP_EMIT_UNROLL
+      // four fingerprints per step with independent loads (bounded by the table's last entry)
+      for (; o < o_end && e + 4 <= m_tab; e += 4) {
+        const uint32_t f0 = fp[e], f1 = fp[e + 1], f2 = fp[e + 2], f3 = fp[e + 3];
+        const uint32_t mm = (uint32_t)(f0 == f) | ((uint32_t)(f1 == f) << 1) | ((uint32_t)(f2 == f) << 2) |
+                            ((uint32_t)(f3 == f) << 3);
+        for (uint32_t b = mm; b && o < o_end; b &= b - 1) {
+          const uint64_t eh = e + (__ffs(b) - 1);
+          if (o < hit_cap) hit_pos[o] = pos_tab[eh];
+          ++o;
+        }
+      }
+#endif
+      for (; o < o_end; ++e) {
         if (fp[e] == f) {
           if (o < hit_cap) hit_pos[o] = pos_tab[e];
           ++o;
@@ -206,6 +224,211 @@ __global__ void __launch_bounds__(kLTPB) lookup_sorted_kernel(const uint32_t* __
   }
 }
 
+// Sorted count (round 2b): thread j scans the slice of the j-th query in bucket order (the
+// neighbouring threads mostly share the bucket, so the slice comes from L1/L2), four
+// fingerprints per step with independent loads, and writes the count and first match to the
+// query's OWN index -- so the emit step can run in query order (lookup1_kernel<true>): the CSR
+// offsets and the hit positions are then read and written coalesced, and the only random
+// accesses left are these two stores, the first hit's position and the scan of multi-hit
+// queries.
+template <bool FIRST_Q>
+__global__ void __launch_bounds__(kLTPB) lookup_sorted_count_kernel(const uint32_t* __restrict__ fps,
+                                                                    const uint64_t* __restrict__ ord, uint64_t nq,
+                                                                    int bits, const uint64_t* __restrict__ offsets,
+                                                                    const uint32_t* __restrict__ fp,
+                                                                    uint64_t* __restrict__ hit_off,
+                                                                    uint64_t* __restrict__ first) {
+  for (uint64_t j = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; j < nq; j += (uint64_t)gridDim.x * kLTPB) {
+    const uint64_t i = ord[j];
+    const uint32_t f = fps[j];
+    const uint64_t b = f >> (32 - bits);
+    const uint64_t lo = offsets[b], hi = offsets[b + 1];
+    uint32_t cnt = 0;
+    uint64_t e0 = hi;
+    uint64_t e = lo;
+    for (; e + 4 <= hi; e += 4) {
+      const uint32_t f0 = fp[e], f1 = fp[e + 1], f2 = fp[e + 2], f3 = fp[e + 3];
+      const uint32_t m = (uint32_t)(f0 == f) | ((uint32_t)(f1 == f) << 1) | ((uint32_t)(f2 == f) << 2) |
+                         ((uint32_t)(f3 == f) << 3);
+      if (m) {
+        if (e0 == hi) e0 = e + (__ffs(m) - 1);
+        cnt += __popc(m);
+      }
+    }
+    for (; e < hi; ++e) {
+      if (fp[e] == f) {
+        if (e0 == hi) e0 = e;
+        ++cnt;
+      }
+    }
+    hit_off[i] = cnt;
+    first[FIRST_Q ? i : j] = cnt ? e0 : lo;
+  }
+}
+
+// Sorted lookup, round 2b (kSortedUnsort): the count step runs in bucket order and writes its
+// result COALESCED as a packed item per query -- (query index << 4 | c) << 32 | first match,
+// c = the hit count, or 15 when it is >= 15 or the first match does not fit 32 bits -- and a
+// stable radix pass over the query index (sort_items) puts the items back into query order.
+// The unpack step then writes the counts and first matches in query order (recounting the
+// rare c = 15 queries), so the CSR scan and the emit (lookup1_kernel<true>) run in query order
+// too: no random 8-byte store per query (which cost ~9 ms per 1.9e8 queries on B200).
+__global__ void __launch_bounds__(kLTPB) lookup_sorted_count_pk_kernel(const uint32_t* __restrict__ fps,
+                                                                       const uint64_t* __restrict__ ord, uint64_t nq,
+                                                                       int bits, const uint64_t* __restrict__ offsets,
+                                                                       const uint32_t* __restrict__ fp,
+                                                                       uint64_t* __restrict__ items) {
+  for (uint64_t j = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; j < nq; j += (uint64_t)gridDim.x * kLTPB) {
+    const uint64_t i = ord[j];
+    const uint32_t f = fps[j];
+    const uint64_t b = f >> (32 - bits);
+    const uint64_t lo = offsets[b], hi = offsets[b + 1];
+    uint32_t cnt = 0;
+    uint64_t e0 = lo;
+    for (uint64_t e = lo; e < hi; ++e) {
+      if (fp[e] == f) {
+        if (cnt == 0) e0 = e;
+        ++cnt;
+      }
+    }
+    const uint32_t c = (cnt >= 15 || (e0 >> 32) != 0) ? 15u : cnt;
+    items[j] = ((uint64_t)(((uint32_t)i << 4) | c) << 32) | (uint32_t)e0;
+  }
+}
+
+// query order: hit_off[i] = count, first[i] = first match (c = 15: counted again here)
+__global__ void __launch_bounds__(kLTPB) lookup_unpack_kernel(const uint64_t* __restrict__ items, uint64_t nq,
+                                                              const uint64_t* __restrict__ q, int k, int bits,
+                                                              const uint64_t* __restrict__ offsets,
+                                                              const uint32_t* __restrict__ fp,
+                                                              uint64_t* __restrict__ hit_off,
+                                                              uint64_t* __restrict__ first) {
+  for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
+    const uint64_t it = items[i];
+    MZS_DCHECK((it >> 36) == i);
+    uint32_t c = (uint32_t)(it >> 32) & 15u;
+    uint64_t e0 = (uint32_t)it;
+    if (c == 15) {
+      const uint32_t f = fp_of(q[i], k);
+      const uint64_t b = f >> (32 - bits);
+      const uint64_t lo = offsets[b], hi = offsets[b + 1];
+      uint64_t cnt = 0;
+      e0 = lo;
+      for (uint64_t e = lo; e < hi; ++e) {
+        if (fp[e] == f) {
+          if (cnt == 0) e0 = e;
+          ++cnt;
+        }
+      }
+      hit_off[i] = cnt;
+    } else {
+      hit_off[i] = c;
+    }
+    first[i] = e0;
+  }
+}
+
+// Unpack + CSR scan in one pass (query order): tiles of kUT queries, claimed in order through
+// an atomic counter, each thread turning kUE consecutive packed items into counts and first
+// matches (c = 15: counted again), a block scan, and the tile's prefix from a decoupled
+// look-back over the tiles before it.  hit_off[i] = exclusive prefix, hit_off[nq] = total.
+constexpr int kUE = 8;
+constexpr int kUT = kLTPB * kUE;
+__device__ __forceinline__ void unpack_one(uint64_t it, uint64_t i, const uint64_t* __restrict__ q, int k, int bits,
+                                           const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ fp,
+                                           uint64_t& cnt, uint64_t& e0) {
+  MZS_DCHECK((it >> 36) == i);
+  const uint32_t c = (uint32_t)(it >> 32) & 15u;
+  e0 = (uint32_t)it;
+  cnt = c;
+  if (c == 15) {
+    const uint32_t f = fp_of(q[i], k);
+    const uint64_t b = f >> (32 - bits);
+    const uint64_t lo = offsets[b], hi = offsets[b + 1];
+    cnt = 0;
+    e0 = lo;
+    for (uint64_t e = lo; e < hi; ++e) {
+      if (fp[e] == f) {
+        if (cnt == 0) e0 = e;
+        ++cnt;
+      }
+    }
+  }
+}
+__global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_t* __restrict__ items, uint64_t nq,
+                                                                   const uint64_t* __restrict__ q, int k, int bits,
+                                                                   const uint64_t* __restrict__ offsets,
+                                                                   const uint32_t* __restrict__ fp,
+                                                                   uint64_t* __restrict__ hit_off,
+                                                                   uint64_t* __restrict__ first, uint64_t* status,
+                                                                   uint32_t* tile_counter, uint64_t* d_total) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t ws[kLTPB / 32];
+  __shared__ uint64_t s_pre;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+  __syncthreads();
+  const uint64_t t = s_tile;
+  const uint64_t ntiles = (nq + kUT - 1) / kUT;
+  const uint64_t i0 = t * kUT + (uint64_t)threadIdx.x * kUE;
+  uint64_t cnt[kUE], e0[kUE];
+  uint64_t sum = 0;
+  if (i0 + kUE <= nq) {
+    uint64_t it[kUE];
+#pragma unroll
+    for (int u = 0; u < kUE; u += 2) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(items + i0 + u);
+      it[u] = v.x;
+      it[u + 1] = v.y;
+    }
+#pragma unroll
+    for (int u = 0; u < kUE; ++u) {
+      unpack_one(it[u], i0 + u, q, k, bits, offsets, fp, cnt[u], e0[u]);
+      sum += cnt[u];
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < kUE; ++u) {
+      cnt[u] = 0;
+      e0[u] = 0;
+      if (i0 + u < nq) unpack_one(items[i0 + u], i0 + u, q, k, bits, offsets, fp, cnt[u], e0[u]);
+      sum += cnt[u];
+    }
+  }
+  uint64_t tot;
+  uint64_t ex = block_exclusive_sum<kLTPB, uint64_t>(sum, ws, &tot);
+  if (warp_id() == 0) {
+    const uint64_t pre = lookback_exclusive(status, t, tot);
+    if (lane_id() == 0) {
+      s_pre = pre;
+      if (t == ntiles - 1) {
+        hit_off[nq] = pre + tot;
+        if (d_total) *d_total = pre + tot;
+      }
+    }
+  }
+  __syncthreads();
+  ex += s_pre;
+  if (i0 + kUE <= nq) {
+#pragma unroll
+    for (int u = 0; u < kUE; u += 2) {
+      const uint64_t a = ex;
+      const uint64_t b = ex + cnt[u];
+      ex = b + cnt[u + 1];
+      *reinterpret_cast<ulonglong2*>(hit_off + i0 + u) = make_ulonglong2(a, b);
+      *reinterpret_cast<ulonglong2*>(first + i0 + u) = make_ulonglong2(e0[u], e0[u + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < kUE; ++u) {
+      if (i0 + u < nq) {
+        hit_off[i0 + u] = ex;
+        first[i0 + u] = e0[u];
+      }
+      ex += cnt[u];
+    }
+  }
+}
+
 // ---- exclusive scan of u64 counts in place (reduce, scan of block sums, add)
 constexpr int kSE = 8;                   // elements per thread
 constexpr int kSB = kLTPB * kSE;         // elements per block
@@ -272,6 +495,20 @@ __global__ void __launch_bounds__(kLTPB) scan_apply_kernel(uint64_t* x, uint64_t
 
 using namespace mzs;
 
+#ifndef MZS_LOOKUP_QEMIT
+#define MZS_LOOKUP_QEMIT 0
+#endif
+// sorted lookup: count in bucket order, emit in query order (1) or both in bucket order (0)
+constexpr bool kSortedQueryOrderEmit = MZS_LOOKUP_QEMIT != 0;
+#ifndef MZS_LOOKUP_UNSORT
+#define MZS_LOOKUP_UNSORT 1
+#endif
+// sorted lookup: per-query results put back into query order by a radix pass (round 2b)
+constexpr bool kSortedUnsort = MZS_LOOKUP_UNSORT != 0;
+#ifndef MZS_LOOKUP_EMIT_LANES
+#define MZS_LOOKUP_EMIT_LANES 1
+#endif
+constexpr int kEmitLanes = MZS_LOOKUP_EMIT_LANES;
 // queries from which the sorted lookup is used (MZS_LOOKUP_SORT=0/1 forces it off/on)
 constexpr uint64_t kSortMin = 1u << 20;
 
@@ -297,7 +534,8 @@ MZS_API size_t seedtable_lookup_workspace_bytes(uint64_t nq) {
   z.take<uint64_t>(nq + 1);
   z.take<uint32_t>(nq + 1);
   z.take<uint64_t>(nq + 1);
-  z.used += sort_fp_idx_workspace_bytes(std::max<uint64_t>(nq, 1), 2) + kAlign;
+  z.used += std::max(sort_fp_idx_workspace_bytes(std::max<uint64_t>(nq, 1), 2),
+                     sort_items_workspace_bytes(std::max<uint64_t>(nq, 1), 4, 32)) + kAlign;
   return z.used;
 }
 
@@ -332,7 +570,8 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
   uint64_t* idx = c.take<uint64_t>(nq + 1);
   uint32_t* fps = c.take<uint32_t>(nq + 1);
   uint64_t* ord = c.take<uint64_t>(nq + 1);
-  const size_t sort_ws = sort_fp_idx_workspace_bytes(std::max<uint64_t>(nq, 1), 2);
+  const size_t sort_ws = std::max(sort_fp_idx_workspace_bytes(std::max<uint64_t>(nq, 1), 2),
+                                  sort_items_workspace_bytes(std::max<uint64_t>(nq, 1), 4, 32));
   void* sws = c.take<unsigned char>(sort_ws);
   if (!c.ok) return SLSUM_ENOMEM;
   if (!d_nq && use_sorted(nq, bucket_bits)) {
@@ -343,8 +582,60 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
     MZS_LAUNCHED();
     int rc = sort_fp_idx(fpq, idx, nq, 32 - bucket_bits, fps, ord, sws, sort_ws, st);
     if (rc) return rc;
-    lookup_sorted_kernel<false><<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pos_tab, hit_off,
-                                                      nullptr, 0, first);
+    int qbits = 1;
+    while (qbits < 28 && (1ull << qbits) < nq) ++qbits;
+    if (kSortedUnsort && nq <= (1ull << 28)) {
+      // count in bucket order -> packed items (into idx, free after the sort) -> back to query
+      // order (into ord, free after the count) -> counts and first matches in query order
+      uint64_t* pk = idx;
+      uint64_t* pq = ord;
+      lookup_sorted_count_pk_kernel<<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pk);
+      MZS_LAUNCHED();
+      rc = sort_items(pk, nq, 4, 4 + qbits, pq, sws, sort_ws, st);
+      if (rc) return rc;
+      // unpack + scan in one pass; its tile status words and counter live in `fpq` (free
+      // after the count: nq + 1 u32 >= 2 * ceil(nq / kUT) + 1 words)
+      const uint64_t nt = (nq + kUT - 1) / kUT;
+      uint64_t* status = reinterpret_cast<uint64_t*>(
+          (reinterpret_cast<uintptr_t>(fpq) + 7) & ~static_cast<uintptr_t>(7));
+      uint32_t* counter = reinterpret_cast<uint32_t*>(status + nt);
+      MZS_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t) * nt + sizeof(uint32_t), st));
+      const bool aligned = ((reinterpret_cast<uintptr_t>(pq) | reinterpret_cast<uintptr_t>(hit_off) |
+                             reinterpret_cast<uintptr_t>(first)) & 15) == 0;
+      if (aligned) {
+        lookup_unpack_scan_kernel<<<(unsigned)nt, kLTPB, 0, st>>>(pq, nq, qkey, k, bucket_bits, offsets, fp, hit_off,
+                                                                  first, status, counter, d_total);
+        MZS_LAUNCHED();
+      } else {
+        lookup_unpack_kernel<<<g, kLTPB, 0, st>>>(pq, nq, qkey, k, bucket_bits, offsets, fp, hit_off, first);
+        MZS_LAUNCHED();
+        scan_reduce_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, nullptr, bsum);
+        MZS_LAUNCHED();
+        scan_blocks_kernel<<<1, kLTPB, 0, st>>>(bsum, nb, hit_off, nq, nullptr, d_total);
+        MZS_LAUNCHED();
+        scan_apply_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, nullptr, bsum);
+        MZS_LAUNCHED();
+      }
+      if (hit_cap) {
+        // the multi-hit queries scan their slice from the first match on: kEmitLanes lanes per
+        // query (ballots) keep the scans short and the warp converged
+        if (kEmitLanes == 1) {
+          lookup1_kernel<true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab, hit_off,
+                                                    hit_pos, hit_cap, first);
+        } else {
+          const unsigned ge = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nq * kEmitLanes + kLTPB - 1) / kLTPB,
+                                                                                 (uint64_t)num_sms() * 8));
+          lookup_kernel<true, kEmitLanes><<<ge, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp,
+                                                               pos_tab, hit_off, hit_pos, hit_cap, first);
+        }
+        MZS_LAUNCHED();
+      }
+      return SLSUM_OK;
+    }
+    if (kSortedQueryOrderEmit)
+      lookup_sorted_count_kernel<true><<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, hit_off, first);
+    else
+      lookup_sorted_count_kernel<false><<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, hit_off, first);
     MZS_LAUNCHED();
     scan_reduce_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, nullptr, bsum);
     MZS_LAUNCHED();
@@ -353,8 +644,12 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
     scan_apply_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, nullptr, bsum);
     MZS_LAUNCHED();
     if (hit_cap) {
-      lookup_sorted_kernel<true><<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pos_tab, hit_off,
-                                                       hit_pos, hit_cap, first);
+      if (kSortedQueryOrderEmit)
+        lookup1_kernel<true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab, hit_off,
+                                                  hit_pos, hit_cap, first);
+      else
+        lookup_sorted_kernel<true><<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pos_tab, hit_off,
+                                                         hit_pos, hit_cap, first);
       MZS_LAUNCHED();
     }
     return SLSUM_OK;

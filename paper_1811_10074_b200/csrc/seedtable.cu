@@ -962,6 +962,58 @@ int sort_fp_idx(const uint32_t* fp, const uint64_t* idx, uint64_t m, int lo_bit,
   return stable_sort(false, fp, idx, nullptr, m, 0, lo_bit, 32, fp_out, idx_out, s, st);
 }
 
+// Stable sort of m packed u64 items by bits [lo_bit, hi_bit) of their HIGH 32 bits (the rest
+// of the item travels unchanged): the narrow passes alone, for other translation units (the
+// sorted seed lookup puts its per-query results back into query order with it).
+size_t sort_items_workspace_bytes(uint64_t m, int lo_bit, int hi_bit) {
+  (void)lo_bit; (void)hi_bit;
+  Sizer z;
+  z.take<uint32_t>(256 * chunks_for(m));
+  z.take<uint64_t>(256 * chunks_for(m));
+  z.take<unsigned long long>(256);
+  z.take<unsigned long long>(256);
+  z.take<uint64_t>(2);
+  z.take<uint64_t>(m + 1);
+  z.take<uint64_t>(m + 1);
+  return z.used;
+}
+int sort_items(const uint64_t* items, uint64_t m, int lo_bit, int hi_bit, uint64_t* out, void* ws, size_t ws_bytes,
+               cudaStream_t st) {
+  if (m == 0) return SLSUM_OK;
+  if (lo_bit < 0 || hi_bit > 32 || hi_bit <= lo_bit) return SLSUM_EINVAL;
+  Carve c(ws, ws_bytes);
+  SortWs s{};
+  s.chunk = chunk_for(m);
+  s.counts = c.take<uint32_t>(256 * chunks_for(m));
+  s.offs = c.take<uint64_t>(256 * chunks_for(m));
+  s.totals = c.take<unsigned long long>(256);
+  s.dbase = c.take<unsigned long long>(256);
+  s.ctl = c.take<uint64_t>(2);
+  uint64_t* A = c.take<uint64_t>(m + 1);
+  uint64_t* B = c.take<uint64_t>(m + 1);
+  if (!c.ok) return SLSUM_ENOMEM;
+  // ctl = {1 (the narrow path), 0}: every kernel runs, no wide fallback (the items are opaque)
+  MZS_CUDA(cudaMemsetAsync(s.ctl, 0, 2 * sizeof(uint64_t), st));
+  MZS_CUDA(cudaMemsetAsync(s.ctl, 1, 1, st));
+  static const int ipt_pk = env_int("MZS_NCFG", 25616);
+  const int npass = (hi_bit - lo_bit + 7) / 8;
+  const uint64_t nch = (m + s.chunk - 1) / s.chunk;
+  const uint64_t* kin = items;
+  int tma = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
+  for (int p = 0; p < npass; ++p) {
+    uint64_t* dst = p == npass - 1 ? out : ((p & 1) ? B : A);
+    const int sh = lo_bit + 8 * p;
+    const int nb = std::min(8, hi_bit - sh);
+    int rc = count_pass<2>(kin, nullptr, m, 0, sh, nb, nch, s, 1, st);
+    if (rc) return rc;
+    rc = launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, kin, nullptr, dst, nullptr, nullptr, m, 0, sh, nb, nch, s, tma, st);
+    if (rc) return rc;
+    kin = dst;
+    tma = 1;
+  }
+  return SLSUM_OK;
+}
+
 }  // namespace mzs
 
 using namespace mzs;

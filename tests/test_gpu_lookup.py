@@ -121,3 +121,26 @@ def test_sorted_lookup_large_batches(k, bits):
         assert np.array_equal(ho[: nq + 1], ho_w)
         c = kw.get("hit_cap", t)
         assert np.array_equal(hp[:c], hp_w[:c])
+
+
+@pytest.mark.parametrize("span", [1000, 20])
+def test_sorted_lookup_heavy_repeats(span):
+    """The sorted lookup's packed per-query result carries hit counts up to 14; queries with 15
+    or more hits (here every key occurs ~400 or ~20000 times) are counted again in query order.
+    The CSR still equals the oracle's (Fig. 1 lookups; R30)."""
+    k, bits = 15, 24
+    rng = np.random.default_rng(span)
+    m, nq = 400_000, (1 << 20) + 7
+    key = rng.integers(0, span, size=m, dtype=np.uint64)
+    pos = np.sort(rng.choice(10 ** 9, size=m, replace=False)).astype(np.uint64)
+    q = np.concatenate([key[rng.integers(0, m, size=nq - 1000)], rng.integers(0, 1 << 30, size=1000, dtype=np.uint64)])
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    npre = 64 if span < 100 else 4096                      # the oracle on a prefix (the hits are many)
+    ho_w, hp_w = O.lookup(q[:npre], k, bits, wo, wf, wp)
+    ho, hp, t = _gpu_lookup(key, pos, q, k, bits, hit_cap=0)
+    assert np.array_equal(ho[: npre + 1], ho_w)
+    # every query's count, by the definition: the entries of the table whose key equals it
+    cnt = np.bincount(key.astype(np.int64), minlength=span)
+    qs = q.astype(np.int64)
+    want = np.where(qs < span, cnt[np.minimum(qs, span - 1)], 0)
+    assert np.array_equal(np.diff(ho[: nq + 1].astype(np.int64)), want)
