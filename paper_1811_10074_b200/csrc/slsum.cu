@@ -791,14 +791,17 @@ __device__ __forceinline__ void shifted_regs(const T (&t)[E], T (&u)[E]) {
     else u[j] = shfl_down(t[src % E], src / E);
   }
 }
-template <class Op, int W>
+// EE: values per lane (default 16 for 4-byte types, 8 for 8-byte ones); EE = 32 for w = 128
+// and 256 on 4-byte types (round 2b): every round in registers, the warp's 1024 inputs give
+// 1024 - 32 * ceil((w-1)/32) outputs (75 % at w = 256) instead of shared-memory rounds.
+template <class Op, int W, int EE = (sizeof(typename Op::T) == 4) ? 16 : 8>
 __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename Op::T* __restrict__ x,
                                                                  typename Op::T* __restrict__ y, uint64_t n,
                                                                  uint64_t nout) {
   using T = typename Op::T;
-  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr int E = EE;
   constexpr uint32_t OV = 16 / sizeof(T);
-  static_assert(W >= 2 && W <= 4 * E, "halo within a warp");
+  static_assert(W >= 2 && W <= 8 * E, "halo within a warp (at most 8 of its 32 lanes)");
   constexpr int M = 31 - __builtin_clz((unsigned)W);  // floor(log2 W)
   constexpr int P2 = 1 << M;
   constexpr int HL = (W - 1 + E - 1) / E;             // halo lanes
@@ -857,7 +860,9 @@ __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename
   level(std::integral_constant<int, 4>{});
   level(std::integral_constant<int, 5>{});
   level(std::integral_constant<int, 6>{});
-  static_assert(M <= 6, "levels unrolled above");
+  level(std::integral_constant<int, 7>{});
+  level(std::integral_constant<int, 8>{});
+  static_assert(M <= 8, "levels unrolled above");
   T* out = t;
   if constexpr (kDigits) {
     out = acc;
@@ -878,15 +883,15 @@ __global__ void __launch_bounds__(256) slsum_doubling_warp_kernel(const typename
   }
 }
 
-template <class Op, int W>
+template <class Op, int W, int EE = (sizeof(typename Op::T) == 4) ? 16 : 8>
 int launch_doubling_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
-  constexpr int E = (sizeof(T) == 4) ? 16 : 8;
+  constexpr int E = EE;
   constexpr int HL = (W - 1 + E - 1) / E;
   const uint64_t nout = n - w + 1;
   const uint64_t kOut = (uint64_t)(32 - HL) * E;
   const uint64_t warps = (nout + kOut - 1) / kOut;
-  slsum_doubling_warp_kernel<Op, W><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
+  slsum_doubling_warp_kernel<Op, W, EE><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
       static_cast<const T*>(xv), static_cast<T*>(yv), n, nout);
   MZS_LAUNCHED();
   return SLSUM_OK;
@@ -1021,6 +1026,11 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
     if (w == 16) return launch_doubling_warp<Op, 16>(xv, yv, n, w, st);
     if (w == 32) return launch_doubling_warp<Op, 32>(xv, yv, n, w, st);
     if (w == 4 * E) return launch_doubling_warp<Op, 4 * E>(xv, yv, n, w, st);
+    // 4-byte types: 32 values per lane keep w = 128 and 256 in registers too
+    if constexpr (sizeof(T) == 4) {
+      if (w == 128 && n >= 4096 && !env_flag("MZS_SLSUM_NO_WARP32")) return launch_doubling_warp<Op, 128, 32>(xv, yv, n, w, st);
+      if (w == 256 && n >= 4096 && !env_flag("MZS_SLSUM_NO_WARP32")) return launch_doubling_warp<Op, 256, 32>(xv, yv, n, w, st);
+    }
     // w = 3..15 outside the powers of two: finishing combine in registers too
     if (w == 3) return launch_doubling_warp<Op, 3>(xv, yv, n, w, st);
     if (w == 5) return launch_doubling_warp<Op, 5>(xv, yv, n, w, st);
