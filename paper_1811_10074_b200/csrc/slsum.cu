@@ -567,17 +567,22 @@ int launch_generic_cta(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStr
 // Operand order is preserved (any associative op).  NWT = 1 needs no shared memory at all.
 constexpr int kTeamEL = 8;
 
-template <class Op, int NWT>
+// RT (round 2b): any block length w with 256 (NWT-1) < w <= 256 NWT -- the block's slots past
+// w hold the identity (they never reach an output: S folds them in as identities, P stops
+// before them), blocks start at b * w (16-byte vector loads only for the blocks that start on
+// a vector), so every w in (256, 2048] streams like the powers of two.
+template <class Op, int NWT, bool RT = false>
 __global__ void __launch_bounds__(256) slsum_generic_team_kernel(const typename Op::T* __restrict__ x,
                                                                 typename Op::T* __restrict__ y, uint64_t n,
-                                                                uint64_t nout, uint64_t blocks_per_team) {
+                                                                uint64_t nout, uint64_t blocks_per_team,
+                                                                uint32_t w_rt = 0) {
   using T = typename Op::T;
   constexpr int EL = kTeamEL;
   constexpr uint32_t OV = 16 / sizeof(T);
   constexpr uint32_t PW = 32 * EL;                          // elements of one warp's part
-  constexpr uint32_t W = PW * NWT;
+  const uint32_t W = RT ? w_rt : PW * NWT;
   constexpr int NTEAM = 8 / NWT;                            // teams per 256-thread CTA
-  static_assert(EL % OV == 0 && 8 % NWT == 0, "team shape");
+  static_assert(EL % OV == 0 && NWT >= 1 && NWT <= 8 && (RT || 8 % NWT == 0), "team shape");
   __shared__ T sT[2][NTEAM][NWT], sR[2][NTEAM][NWT];
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t team = wid / NWT, k = wid % NWT;
@@ -591,14 +596,15 @@ __global__ void __launch_bounds__(256) slsum_generic_team_kernel(const typename 
   auto team_sync = [&]() {
     if (NWT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * NWT) : "memory");
   };
+  const uint32_t loc0 = k * PW + lane * EL;                 // this lane's first slot in a block
   auto load = [&](uint64_t b, T (&v)[EL]) {
-    const uint64_t g = b * W + (uint64_t)k * PW + (uint64_t)lane * EL;
-    if (aligned && b + 1 < nb) {
+    const uint64_t g = b * W + loc0;
+    if (aligned && b + 1 < nb && (!RT || (loc0 + EL <= W && ((b * W) % OV) == 0))) {
 #pragma unroll
       for (int q = 0; q < EL; q += OV) *reinterpret_cast<uint4*>(v + q) = __ldg(reinterpret_cast<const uint4*>(x + g + q));
     } else {
 #pragma unroll
-      for (int j = 0; j < EL; ++j) v[j] = (g + j < n) ? x[g + j] : Op::id();
+      for (int j = 0; j < EL; ++j) v[j] = (g + j < n && (!RT || loc0 + j < W)) ? x[g + j] : Op::id();
     }
   };
   int par = 0;
@@ -668,38 +674,40 @@ __global__ void __launch_bounds__(256) slsum_generic_team_kernel(const typename 
     else o[0] = k == 0 ? Sp[0] : Op::op(Sp[0], C);
 #pragma unroll
     for (int j = 1; j < EL; ++j) o[j] = Op::op(Sp[j], v[j - 1]);
-    const uint64_t g = b * W + (uint64_t)k * PW + (uint64_t)lane * EL;
+    const uint64_t g = b * W + loc0;
     MZS_DCHECK(b < nb);
-    if (aligned && g + EL <= nout) {
+    if (aligned && g + EL <= nout && (!RT || (loc0 + EL <= W && ((b * W) % OV) == 0))) {
 #pragma unroll
       for (int q = 0; q < EL; q += OV) *reinterpret_cast<uint4*>(y + g + q) = *reinterpret_cast<const uint4*>(o + q);
     } else {
 #pragma unroll
       for (int j = 0; j < EL; ++j)
-        if (g + j < nout) y[g + j] = o[j];
+        if (g + j < nout && (!RT || loc0 + j < W)) y[g + j] = o[j];
     }
 #pragma unroll
     for (int j = 0; j < EL; ++j) Sp[j] = Sn[j];
   }
 }
 
-template <class Op, int NWT>
+template <class Op, int NWT, bool RT = false>
 int launch_generic_team(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_t st) {
   using T = typename Op::T;
-  constexpr uint32_t W = 32 * kTeamEL * NWT;
+  const uint32_t W = RT ? w : 32 * kTeamEL * NWT;
   const uint64_t nout = n - w + 1;
   const uint64_t nbo = (nout + W - 1) / W;
   static int occ = 0;
   if (occ == 0) {
-    MZS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slsum_generic_team_kernel<Op, NWT>, 256, 0));
+    MZS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slsum_generic_team_kernel<Op, NWT, RT>,
+                                                           32 * NWT * (8 / NWT), 0));
     occ = std::max(occ, 1);
   }
-  const uint64_t teams = (uint64_t)num_sms() * occ * (8 / NWT);
+  constexpr int NTEAM = 8 / NWT;                 // teams per CTA (CTA = 32 NWT NTEAM <= 256 threads)
+  const uint64_t teams = (uint64_t)num_sms() * occ * NTEAM;
   const uint64_t per = std::max<uint64_t>(4, (nbo + teams - 1) / teams);
   const uint64_t nt = (nbo + per - 1) / per;
-  const uint64_t grid = (nt + (8 / NWT) - 1) / (8 / NWT);
-  slsum_generic_team_kernel<Op, NWT><<<(unsigned)grid, 256, 0, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv),
-                                                                     n, nout, per);
+  const uint64_t grid = (nt + NTEAM - 1) / NTEAM;
+  slsum_generic_team_kernel<Op, NWT, RT><<<(unsigned)grid, 32 * NWT * NTEAM, 0, st>>>(static_cast<const T*>(xv),
+                                                                         static_cast<T*>(yv), n, nout, per, w);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -742,6 +750,20 @@ int launch_generic(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream_
       if (w == 512) return launch_generic_team<Op, 2>(xv, yv, n, w, st);
       if (w == 1024) return launch_generic_team<Op, 4>(xv, yv, n, w, st);
       if (w == 2048) return launch_generic_team<Op, 8>(xv, yv, n, w, st);
+      // any other w in (256, 2048]: the same team kernel with a runtime block length
+      // (NWT = ceil(w / 256) warps per team; taken when at most a quarter of the slots pad)
+      const uint32_t nwt = (w + 255) / 256;
+      if (w > 256 && w <= 2048 && 4 * w >= 3 * 256 * nwt && !env_flag("MZS_SLSUM_NO_TEAM_RT")) {
+        switch (nwt) {
+          case 2: return launch_generic_team<Op, 2, true>(xv, yv, n, w, st);
+          case 3: return launch_generic_team<Op, 3, true>(xv, yv, n, w, st);
+          case 4: return launch_generic_team<Op, 4, true>(xv, yv, n, w, st);
+          case 5: return launch_generic_team<Op, 5, true>(xv, yv, n, w, st);
+          case 6: return launch_generic_team<Op, 6, true>(xv, yv, n, w, st);
+          case 7: return launch_generic_team<Op, 7, true>(xv, yv, n, w, st);
+          default: return launch_generic_team<Op, 8, true>(xv, yv, n, w, st);
+        }
+      }
     }
     if (w == 16 * E) return launch_generic_cta<Op, 256, 16>(xv, yv, n, w, st);  // 256 > 512 lanes (75 vs 68 %)
     if (w == 32 * E) return launch_generic_cta<Op, 512, 32>(xv, yv, n, w, st);

@@ -257,3 +257,21 @@ def test_commutative_register_start(op, w):
     y = P.slsum_run(op, w, xt, path=P.SLSUM_PATH_COMMUTATIVE)
     torch.cuda.synchronize()
     _check(op, w, x, y.cpu().numpy())
+
+
+@pytest.mark.parametrize("op", [P.SLSUM_MIN_U32, P.SLSUM_ADD_F32, P.SLSUM_AFFINE_U32X2, P.SLSUM_MIN_U64])
+@pytest.mark.parametrize("w", [257, 300, 400, 511, 513, 700, 777, 1025, 1500, 1700, 2047])
+def test_generic_team_runtime_w(op, w):
+    """GENERIC for any w in (256, 2048] outside the powers of two: the team kernel with a
+    runtime block length (slots past w hold the identity; blocks start at b*w, so most are not
+    16-byte aligned).  Operand order is kept (AFFINE is not commutative), many blocks per team,
+    a ragged end and a misaligned view; bit-exact vs the oracle (f32 within the BASELINE bound)."""
+    rng = np.random.default_rng(op * 1000 + w)
+    for n in (w, w + 1, 5 * w + 3, 300_001):
+        x = _input(op, n, rng)
+        _check(op, w, x, _run(op, w, x, P.SLSUM_PATH_GENERIC))
+    x = _input(op, 100_003, rng)
+    xt = torch.from_numpy(np.concatenate([x[:1], x])).cuda()[1:]
+    y = P.slsum_run(op, w, xt, path=P.SLSUM_PATH_GENERIC)
+    torch.cuda.synchronize()
+    _check(op, w, x, y.cpu().numpy())
