@@ -628,8 +628,18 @@ __global__ void __launch_bounds__(kTPB) smin_apply_kernel(uint64_t* __restrict__
   __shared__ uint64_t ws[kNW];
   const uint64_t b0 = (uint64_t)blockIdx.x * kSminTile + (uint64_t)threadIdx.x * 16;
   uint64_t x[16];
+  const bool vec = b0 + 16 <= n && (reinterpret_cast<uintptr_t>(v) & 15) == 0;  // 16-byte accesses
+  if (vec) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) x[j] = b0 + j < n ? v[b0 + j] : ~0ull;
+    for (int j = 0; j < 16; j += 2) {
+      const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(v + b0 + j);
+      x[j] = p.x;
+      x[j + 1] = p.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = b0 + j < n ? v[b0 + j] : ~0ull;
+  }
 #pragma unroll
   for (int j = 14; j >= 0; --j) x[j] = min(x[j], x[j + 1]);
   // carry from threads to the right (their chunk minima), nearest first
@@ -647,9 +657,15 @@ __global__ void __launch_bounds__(kTPB) smin_apply_kernel(uint64_t* __restrict__
   uint64_t wr = ~0ull;
   for (int w = wid + 1; w < kNW; ++w) wr = min(wr, ws[w]);
   const uint64_t carry = min(min(right, wr), tile_carry[blockIdx.x]);
+  if (vec) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (b0 + j < n) v[b0 + j] = min(x[j], carry);
+    for (int j = 0; j < 16; j += 2)
+      *reinterpret_cast<ulonglong2*>(v + b0 + j) = make_ulonglong2(min(x[j], carry), min(x[j + 1], carry));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (b0 + j < n) v[b0 + j] = min(x[j], carry);
+  }
 }
 
 // counts[bucket] += 1 (global atomics; the 2^bits counters stay L2-resident)
