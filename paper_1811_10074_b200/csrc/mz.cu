@@ -615,8 +615,9 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
   uint64_t em = 0;  // bit i <-> slot jb + 1 + i
   // FULL unmasked strips mark into a 32-bit mask per block of W windows (their argmins lie in
   // the block's slots + W - 1 more: < 2W <= 32 bits), folded into em once per block
-  constexpr bool kM32 = FULL && !MASKED && MZS_MZ_MARK32;
+  constexpr bool kM32 = FULL && MZS_MZ_MARK32;
   uint32_t m32 = 0, mbase = 0;
+  uint32_t vmb = 0;  // (MASKED) validity of the block's windows: bit c <-> window jblk + c
   auto valid_of = [&](int j) -> bool {
     if (FULL) return true;
     const bool in = (unsigned)(j - vlo) < (unsigned)(vhi - vlo);
@@ -628,8 +629,12 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
       // every window's argmin is marked (argmins never decrease, so a repeat hits the same
       // bit); the carried-in argmin of window jb-1, owned by the strip on the left, is cleared
       // once after the strip (R3)
-      if (MASKED) em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
-      else if (kM32) {
+      if (kM32 && MASKED) {
+        MZS_DCHECK(s - mbase < 32u);
+        m32 |= ((vmb >> (uint32_t)(j - (int)mbase + 1)) & 1u) << (s - mbase);
+      } else if (MASKED) {
+        em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
+      } else if (kM32) {
         MZS_DCHECK(s - mbase < 32u);
         m32 |= 1u << (s - mbase);
       } else {
@@ -664,6 +669,7 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
     if (kM32) {
       m32 = 0;
       mbase = (uint32_t)(jblk + 1);
+      if (MASKED) vmb = (uint32_t)(vm >> (jblk - jb + 1));
     }
     visit(jblk, S[0]);
     const int sb = jb + 1 + b * W;
