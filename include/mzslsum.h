@@ -186,12 +186,9 @@ typedef struct mz_out {
                                 uint32 words; zeroed and filled by mz_extract_ex.  Layout:
                                 hist[d * nchunks + c] = number of records r < min(count,
                                 capacity) with r in chunk c (chunks of the seed table's radix
-                                chunk size for m = capacity) and digit d = the first
-                                radix pass's digit of the bucket b = fp >> (32 - bucket_bits):
-                                for 9 <= bucket_bits <= 24 (the segmented plan: LSD passes
-                                over the bucket's top bucket_bits - 8 bits, then one local
-                                pass per segment) d = bits [8, 8 + min(8, bucket_bits - 8))
-                                of b; otherwise d = bits [0, min(8, bucket_bits)) of b.  */
+                                chunk size for m = capacity) and digit d = bits
+                                [32 - bucket_bits, 40 - bucket_bits) of fp (the least
+                                significant 8 bits of the bucket, as many as it has).  */
   int hist_bucket_bits;      /* bucket_bits of the table the hist is for (1..min(2k,30))  */
 } mz_out_t;
 

@@ -89,19 +89,6 @@ inline uint32_t radix_chunk_for(uint64_t m) {
 }
 inline uint64_t radix_nchunks(uint64_t m) { return (m + radix_chunk_for(m) - 1) / radix_chunk_for(m); }
 
-// Seed-table pass plan from packed items (seedtable.cu, K7).  bucket = fp >> (32 - bits).
-// With 9 <= bits <= 24 ("segmented" plan) the LSD passes sort only the bucket's top bits - 8
-// (its "prefix": one or two 8-bit passes, lowest digit first), and one local pass sorts every
-// prefix segment by the bucket's low 8 bits and writes the pointer table.  Otherwise all bits go
-// through LSD passes from the bucket's low end.  The FIRST pass's digit (the one mz_out.hist
-// counts) is fp bits [radix_first_shift, + radix_first_bits).
-inline bool radix_segmented(int bits) { return bits >= 9 && bits <= 24; }
-inline int radix_first_shift(int bits) { return radix_segmented(bits) ? 40 - bits : 32 - bits; }
-inline int radix_first_bits(int bits) {
-  const int span = radix_segmented(bits) ? bits - 8 : bits;
-  return span < 8 ? span : 8;
-}
-
 // ---------------------------------------------------------------- shared host entry points
 // (seedtable.cu) stable sort of (u32 fingerprint, u64 index) pairs by fingerprint bits
 // [lo_bit, 32), used by the sorted seed lookup

@@ -1225,16 +1225,15 @@ MZS_API int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out
   a.capacity = out->capacity;
   a.d_count = out->d_count;
   if (out->hist) {
-    // the seed table's first radix pass: digit = fp bits [radix_first_shift(bits), +
-    // radix_first_bits(bits)) (common.cuh pass plan), chunks as seedtable_build_items_ex lays
-    // them out for m = capacity
+    // the seed table's first radix pass: digit = the low 8 bits of the bucket (fp bits
+    // [32 - bits, 40 - bits)), chunks as seedtable_build_items_ex lays them out for m = capacity
     const int bits = out->hist_bucket_bits;
     if (bits < 1 || bits > 30 || bits > 2 * k || out->capacity == 0) return SLSUM_EINVAL;
     a.hist = out->hist;
     a.hist_chunk = radix_chunk_for(out->capacity);
     a.hist_nch = radix_nchunks(out->capacity);
-    a.hist_sh = radix_first_shift(bits);
-    a.hist_mask = (1u << radix_first_bits(bits)) - 1u;
+    a.hist_sh = 32 - bits;
+    a.hist_mask = (1u << (bits < 8 ? bits : 8)) - 1u;
     MZS_CUDA(cudaMemsetAsync(out->hist, 0, sizeof(uint32_t) * 256 * a.hist_nch, st));
   }
   return launch_mz(a, path, st);

@@ -533,272 +533,6 @@ __global__ void __launch_bounds__(TPB) nsweep_kernel(const void* a_in, const uin
 template <int IN, int TPB, int IPT>
 size_t nsweep_smem() { return sizeof(NSmem<IN, TPB, TPB * IPT>); }
 
-// ---------------------------------------------------------------- segmented plan (packed items)
-// With 9 <= bits <= 24 (common.cuh radix_segmented) the narrow path sorts the items by the
-// bucket's top bits - 8 (its "prefix") with the LSD passes above, then ONE local pass sorts each
-// prefix segment by the bucket's low 8 bits (segsort_kernel).  A segment's items are contiguous
-// after the prefix passes and its output range is its input range, so the local pass needs no
-// chunk counts (no upsweep, no chunk scan) and it knows every bucket start of its segment: it
-// writes the pointer table directly (no memset, boundary scatter or suffix minimum).
-//
-// Segment starts: the exclusive scan of the prefix counts.  With one prefix pass those are its
-// digit totals; with two, pair[(dB << 8) | dA] is counted by the second pass's upsweep
-// (upsweep_pair_kernel), whose input is sorted by dA, so a chunk holds few dA values.
-constexpr int kPairRows = 4;
-__global__ void __launch_bounds__(kTPB) upsweep_pair_kernel(const uint64_t* __restrict__ items, const uint64_t* d_m,
-                                                            uint64_t m_cap, int shift, int dbits, int sh_a,
-                                                            uint32_t* counts, uint64_t nchunks, const uint64_t* ctl,
-                                                            int want, uint32_t chunk,
-                                                            unsigned long long* __restrict__ pair) {
-  if (gate_off(ctl, want)) return;
-  // rows 0..3: dA = a0 .. a0+3 (a0 = the chunk's first dA); row 4: any other dA, whose pair
-  // counts go to global atomics at once (correct for any order; rare when sorted by dA)
-  __shared__ uint32_t h[kNW][kPairRows + 1][256];
-  __shared__ uint32_t s_a0;
-  const unsigned lane = lane_id(), wid = warp_id();
-  const uint64_t m = block_count(d_m, m_cap);
-  const uint32_t dmask = (1u << dbits) - 1u;
-  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const uint64_t base = c * (uint64_t)chunk;  // chunks past m count zeros (the scan reads them)
-    for (int i = lane; i < (kPairRows + 1) * 256; i += 32) (&h[wid][0][0])[i] = 0;
-    if (threadIdx.x == 0) s_a0 = base < m ? (uint32_t)(items[base] >> (32 + sh_a)) & 255u : 0u;
-    __syncthreads();
-    const uint32_t a0 = s_a0;
-    const uint64_t end = min(m, base + chunk);
-    auto add = [&](uint64_t v) {
-      const uint32_t f = (uint32_t)(v >> 32);
-      const uint32_t d = (f >> shift) & dmask, da = (f >> sh_a) & 255u, r = da - a0;
-      if (r < (uint32_t)kPairRows) {
-        atomicAdd(&h[wid][r][d], 1u);
-      } else {
-        atomicAdd(&h[wid][kPairRows][d], 1u);
-        atomicAdd(&pair[(d << 8) | da], 1ull);
-      }
-    };
-    {
-      uint64_t i = base + threadIdx.x;
-      for (; i + 3 * kTPB < end; i += 4 * kTPB) {
-        uint64_t v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = items[i + u * kTPB];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) add(v[u]);
-      }
-      for (; i < end; i += kTPB) add(items[i]);
-    }
-    __syncthreads();
-    const uint32_t d = threadIdx.x;
-    uint32_t t = 0;
-#pragma unroll
-    for (int r = 0; r <= kPairRows; ++r) {
-      uint32_t tr = 0;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) tr += h[w][r][d];
-      t += tr;
-      if (r < kPairRows && tr && a0 + r < 256u) atomicAdd(&pair[(d << 8) | (a0 + r)], (unsigned long long)tr);
-    }
-    counts[(uint64_t)d * nchunks + c] = t;
-    __syncthreads();
-  }
-}
-
-// seg_start[s] = sum of cnt[0..s) for s <= nseg (one block; nseg <= 65536)
-__global__ void __launch_bounds__(kTPB) seg_scan_kernel(const unsigned long long* __restrict__ cnt, uint64_t nseg,
-                                                        uint64_t* __restrict__ seg_start, const uint64_t* ctl,
-                                                        int want) {
-  if (gate_off(ctl, want)) return;
-  __shared__ unsigned long long ws[kNW];
-  const uint64_t per = (nseg + kTPB - 1) / kTPB;
-  const uint64_t c0 = min(nseg, threadIdx.x * per), c1 = min(nseg, c0 + per);
-  unsigned long long s = 0;
-  for (uint64_t c = c0; c < c1; ++c) s += cnt[c];
-  unsigned long long tot;
-  unsigned long long ex = block_exclusive_sum<kTPB, unsigned long long>(s, ws, &tot);
-  for (uint64_t c = c0; c < c1; ++c) {
-    seg_start[c] = ex;
-    ex += cnt[c];
-  }
-  if (threadIdx.x == 0) seg_start[nseg] = tot;
-}
-
-constexpr int kSegIPT = 16;
-constexpr int kSegT = kTPB * kSegIPT;  // items per tile of a segment
-constexpr int kSegPeer = 4;            // peer tables (items per round of __syncwarp)
-struct SegSmem {
-  uint64_t stage[kSegT];     // a tile in bucket order
-  uint64_t run_off[256];     // next output index of local digit d
-  uint64_t gbase[256];       // staged entry j of digit d goes to gbase[d] + j
-  uint32_t wcnt[kNW][256];   // per-warp digit counters -> staging bases
-  uint32_t dummy[kNW][32];
-  uint32_t pm[kNW][kSegPeer][256];
-  uint32_t ws[kNW];
-  unsigned long long wsl[kNW];
-  uint64_t a, b, p0;
-  int go;
-};
-
-// One CTA per prefix segment s: its items [seg_start[s], seg_start[s+1]) are sorted stably by
-// the local digit d = (fp >> lo) & 255 (bucket = s << 8 | d) into the final fp / position
-// arrays at the same range, and offsets[(s << 8) + d] = the start of bucket (s, d).  A segment
-// of at most kSegT items is one tile: ranked in registers (per-warp peer tables + counters, as
-// in nsweep_kernel), staged in bucket order and written contiguously.  A longer one first
-// counts its digits, then walks its tiles with running digit offsets (runs per tile).
-template <int OUT>
-__global__ void __launch_bounds__(kTPB) segsort_kernel(const uint64_t* __restrict__ items,
-                                                       const uint64_t* __restrict__ seg_start, uint64_t nseg, int lo,
-                                                       uint32_t* __restrict__ fp_out, void* __restrict__ pos_out,
-                                                       uint64_t* __restrict__ offsets, const uint64_t* ctl) {
-  static_assert(OUT == kOutFpPos || OUT == kOutFpPos32, "final outputs");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  SegSmem& S = *reinterpret_cast<SegSmem*>(smem_raw);
-  const uint32_t td = threadIdx.x;
-  const uint64_t sg = blockIdx.x;
-  if (td == 0) {
-    S.go = ctl == nullptr || ld_volatile_u64(ctl) == 1ull;
-    S.a = seg_start[sg];
-    S.b = seg_start[sg + 1];
-    S.p0 = ctl ? ctl[1] : 0;
-    if (sg == 0 && S.go) offsets[nseg << 8] = seg_start[nseg];  // = m
-  }
-  __syncthreads();
-  if (!S.go) return;
-  const uint64_t a = S.a, L = S.b - S.a, p0 = S.p0;
-  uint64_t* const off_s = offsets + (sg << 8);
-  if (L == 0) {
-    off_s[td] = a;  // every bucket of the segment is empty
-    return;
-  }
-  const unsigned lane = lane_id(), wid = warp_id(), lt = (1u << lane) - 1u;
-  const int dsh = 32 + lo;
-  for (uint32_t i = td; i < kNW * 256; i += kTPB) (&S.wcnt[0][0])[i] = 0;
-  for (uint32_t i = td; i < kNW * kSegPeer * 256; i += kTPB) (&S.pm[0][0][0])[i] = 0;
-  __syncthreads();
-  const uint64_t ntiles = (L + kSegT - 1) / kSegT;
-  if (ntiles > 1) {
-    // digit counts of the whole segment -> bucket starts and running offsets
-    for (uint64_t i = td; i < L; i += kTPB) atomicAdd(&S.wcnt[wid][(uint32_t)(items[a + i] >> dsh) & 255u], 1u);
-    __syncthreads();
-    uint32_t tot = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-      tot += S.wcnt[w][td];
-      S.wcnt[w][td] = 0;
-    }
-    uint32_t all;
-    const uint32_t ex = block_exclusive_sum<kTPB, uint32_t>(tot, S.ws, &all);
-    S.run_off[td] = a + ex;
-    off_s[td] = a + ex;
-    __syncthreads();
-  }
-  for (uint64_t t = 0; t < ntiles; ++t) {
-    const uint64_t tb = a + t * kSegT;
-    const uint32_t nvalid = (uint32_t)min((uint64_t)kSegT, L - t * kSegT);
-    uint64_t item[kSegIPT];
-    uint32_t rank[kSegIPT];
-    unsigned peers[kSegIPT];
-#pragma unroll
-    for (int it = 0; it < kSegIPT; ++it) {
-      const uint32_t j = wid * (kSegIPT * 32) + it * 32 + lane;
-      item[it] = j < nvalid ? items[tb + j] : 0ull;
-    }
-    uint32_t (*pm)[256] = S.pm[wid];
-#pragma unroll
-    for (int g = 0; g < kSegIPT; g += kSegPeer) {
-#pragma unroll
-      for (int u = 0; u < kSegPeer; ++u) {
-        const int it = g + u;
-        if (wid * (kSegIPT * 32) + it * 32 + lane < nvalid)
-          atomicOr(&pm[u][(uint32_t)(item[it] >> dsh) & 255u], 1u << lane);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < kSegPeer; ++u) {
-        const int it = g + u;
-        const bool valid = wid * (kSegIPT * 32) + it * 32 + lane < nvalid;
-        peers[it] = valid ? pm[u][(uint32_t)(item[it] >> dsh) & 255u] : (1u << lane);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < kSegPeer; ++u) {
-        const int it = g + u;
-        if (wid * (kSegIPT * 32) + it * 32 + lane < nvalid)
-          atomicXor(&pm[u][(uint32_t)(item[it] >> dsh) & 255u], 1u << lane);
-      }
-    }
-    uint32_t old[kSegIPT];
-#pragma unroll
-    for (int it = 0; it < kSegIPT; ++it) {
-      const bool valid = wid * (kSegIPT * 32) + it * 32 + lane < nvalid;
-      const bool lead = valid && (peers[it] & lt) == 0u;
-      uint32_t* tgt = lead ? &S.wcnt[wid][(uint32_t)(item[it] >> dsh) & 255u] : &S.dummy[wid][lane];
-      old[it] = atomicAdd(tgt, lead ? (uint32_t)__popc(peers[it]) : 0u);
-      if (it + 1 < kSegIPT) __syncwarp();
-    }
-#pragma unroll
-    for (int it = 0; it < kSegIPT; ++it) {
-      const bool valid = wid * (kSegIPT * 32) + it * 32 + lane < nvalid;
-      const uint32_t o = __shfl_sync(0xffffffffu, old[it], __ffs(peers[it]) - 1);
-      rank[it] = valid ? o + __popc(peers[it] & lt) : 0xffffffffu;
-    }
-    __syncthreads();
-    // tile digit totals -> staging bases (digit start in the tile + earlier warps' count)
-    uint32_t cnt[kNW];
-    uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-      cnt[w] = S.wcnt[w][td];
-      run += cnt[w];
-    }
-    uint32_t all;
-    const uint32_t ex = block_exclusive_sum<kTPB, uint32_t>(run, S.ws, &all);
-    uint32_t acc = ex;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) {
-      S.wcnt[w][td] = acc;
-      acc += cnt[w];
-    }
-    if (ntiles == 1) {
-      S.run_off[td] = a + ex;
-      off_s[td] = a + ex;
-    }
-    const uint64_t r0 = S.run_off[td];
-    S.gbase[td] = r0 - ex;
-    S.run_off[td] = r0 + run;
-    __syncthreads();
-    const uint32_t* wrow = S.wcnt[wid];
-#pragma unroll
-    for (int it = 0; it < kSegIPT; ++it) {
-      if (rank[it] != 0xffffffffu) {
-        const uint32_t sl = wrow[(uint32_t)(item[it] >> dsh) & 255u] + rank[it];
-        MZS_DCHECK(sl < nvalid);
-        S.stage[sl] = item[it];
-      }
-    }
-    __syncthreads();
-    for (uint32_t i = lane; i < 256; i += 32) S.wcnt[wid][i] = 0;
-    auto put = [&](uint32_t j) {
-      const uint64_t v = S.stage[j];
-      const uint64_t g = S.gbase[(uint32_t)(v >> dsh) & 255u] + j;
-      MZS_DCHECK(g >= a && g < a + L);
-      fp_out[g] = (uint32_t)(v >> 32);
-      if constexpr (OUT == kOutFpPos32) static_cast<uint32_t*>(pos_out)[g] = (uint32_t)v;
-      else static_cast<uint64_t*>(pos_out)[g] = p0 + (uint32_t)((uint32_t)v - (uint32_t)p0);
-    };
-    if (ntiles == 1) {
-      // one tile: gbase[d] = a for every digit, the output is the staged tile at a
-      for (uint32_t j = td; j < nvalid; j += kTPB) {
-        const uint64_t v = S.stage[j];
-        fp_out[a + j] = (uint32_t)(v >> 32);
-        if constexpr (OUT == kOutFpPos32) static_cast<uint32_t*>(pos_out)[a + j] = (uint32_t)v;
-        else static_cast<uint64_t*>(pos_out)[a + j] = p0 + (uint32_t)((uint32_t)v - (uint32_t)p0);
-      }
-    } else {
-      for (uint32_t j = td; j < nvalid; j += kTPB) put(j);
-    }
-    __syncthreads();
-  }
-}
-
 // Pointer table from the bucket-sorted fingerprints, in three data-parallel steps (bucket
 // sizes are very uneven: minimizer hashes are window minima, so high buckets are mostly
 // empty and a "fill every empty bucket you see" loop serialises on a few threads):
@@ -809,9 +543,7 @@ __global__ void __launch_bounds__(kTPB) segsort_kernel(const uint64_t* __restric
 // bucket(f) = (f >> shift) & bmask.
 __global__ void __launch_bounds__(kTPB) offsets_scatter_kernel(const uint32_t* __restrict__ fp, const uint64_t* d_m,
                                                                uint64_t m_cap, int shift, uint32_t bmask, uint64_t nb,
-                                                               uint64_t* __restrict__ offsets, const uint64_t* ctl,
-                                                               int want) {
-  if (gate_off(ctl, want)) return;
+                                                               uint64_t* __restrict__ offsets) {
   const uint64_t m = block_count(d_m, m_cap);
   const bool aligned = (reinterpret_cast<uintptr_t>(fp) & 15) == 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets[nb] = m;
@@ -844,9 +576,7 @@ constexpr int kSminTile = kTPB * 16;  // 4096 entries per suffix-min tile
 
 // per-tile minimum of offsets[] (tile t covers [t*4096, (t+1)*4096) of [0, n))
 __global__ void __launch_bounds__(kTPB) smin_reduce_kernel(const uint64_t* __restrict__ v, uint64_t n,
-                                                           uint64_t* __restrict__ tile_min, const uint64_t* ctl,
-                                                           int want) {
-  if (gate_off(ctl, want)) return;
+                                                           uint64_t* __restrict__ tile_min) {
   __shared__ uint64_t ws[kNW];
   const uint64_t b0 = (uint64_t)blockIdx.x * kSminTile;
   uint64_t mn = ~0ull;
@@ -863,8 +593,7 @@ __global__ void __launch_bounds__(kTPB) smin_reduce_kernel(const uint64_t* __res
 
 // suffix minimum of the per-tile minima (one block; a few thousand tiles): tile_min[t] <-
 // min over tiles > t (the carry entering tile t from the right)
-__global__ void __launch_bounds__(kTPB) smin_tiles_kernel(uint64_t* tile_min, uint64_t ntiles, const uint64_t* ctl, int want) {
-  if (gate_off(ctl, want)) return;
+__global__ void __launch_bounds__(kTPB) smin_tiles_kernel(uint64_t* tile_min, uint64_t ntiles) {
   __shared__ uint64_t carry_s;
   __shared__ uint64_t buf[kTPB];
   if (threadIdx.x == 0) carry_s = ~0ull;
@@ -895,9 +624,7 @@ __global__ void __launch_bounds__(kTPB) smin_tiles_kernel(uint64_t* tile_min, ui
 // offsets[i] <- min(offsets[i..end of tile], carry of the tile): serial per thread chunk of 16,
 // then a right-to-left warp/block scan
 __global__ void __launch_bounds__(kTPB) smin_apply_kernel(uint64_t* __restrict__ v, uint64_t n,
-                                                          const uint64_t* __restrict__ tile_carry, const uint64_t* ctl,
-                                                          int want) {
-  if (gate_off(ctl, want)) return;
+                                                          const uint64_t* __restrict__ tile_carry) {
   __shared__ uint64_t ws[kNW];
   const uint64_t b0 = (uint64_t)blockIdx.x * kSminTile + (uint64_t)threadIdx.x * 16;
   uint64_t x[16];
@@ -1112,26 +839,12 @@ int launch_nsweep_cfg(int cfg, const void* a_in, const uint64_t* p_in, void* a_o
 // (u64 hashes | u32 fingerprints) + u64 positions.  Both paths are enqueued: the narrow one
 // (packed u64 items, ctl[0] == 1) and the wide one (u32 + u64 entries, ctl[0] == 0); see
 // ctl_kernel.  After the call s.totals holds the digit totals of the LAST pass.
-// The segmented plan's buffers (seedtable_build_impl; see segsort_kernel).
-struct SegPlan {
-  unsigned long long* pair;   // [65536] prefix pair counts (two prefix passes)
-  uint64_t* seg_start;        // [nseg + 1]
-  uint64_t* offsets;          // the pointer table [2^bits + 1]
-};
-
 int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uint64_t* d_m, uint64_t m, int k,
                 int lo_bit, int hi_bit, uint32_t* fp_dst, uint64_t* pos_dst, SortWs& s, cudaStream_t st,
-                const uint64_t* items = nullptr, uint32_t* pos32_dst = nullptr, const uint32_t* hist0 = nullptr,
-                const SegPlan* seg = nullptr) {
+                const uint64_t* items = nullptr, uint32_t* pos32_dst = nullptr, const uint32_t* hist0 = nullptr) {
   // hist0 (with items): the first narrow pass's digit counts, from mz_extract_ex (mz_out.hist)
   // pos32_dst (packed items only): the final positions as u32 (pos mod 2^32) instead of pos_dst
-  // seg (with items): the narrow path sorts bits [lo_bit + 8, hi_bit) by LSD passes into packed
-  // items and finishes with segsort_kernel, which also writes seg->offsets (the wide path is
-  // unchanged: all bits, final outputs; its pointer table is the caller's)
   const int npass = (hi_bit - lo_bit + 7) / 8;
-  if (seg && !items) return SLSUM_EINVAL;
-  const int nlo = seg ? lo_bit + 8 : lo_bit;           // the narrow passes' low bit
-  const int npassN = (hi_bit - nlo + 7) / 8;           // narrow LSD passes
   if (npass > 4 || npass < 1) return SLSUM_EINVAL;
   const uint64_t nch = (m + s.chunk - 1) / s.chunk;
   if (nch == 0) return SLSUM_OK;
@@ -1153,15 +866,14 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
   {
     uint64_t* pk; uint32_t* fo; uint64_t* po;
     pass_out(0, pk, fo, po);
-    const int nb = std::min(8, hi_bit - nlo);
+    const int nb = std::min(8, hi_bit - lo_bit);
     if (items) {
       // pre-packed items (mz_extract_ex's out->items, positions ascending): pass 0 is an
       // ordinary 8-byte item pass; the hash/pos arrays serve only the wide path
-      rc = count_pass<2>(items, d_m, m, k, nlo, nb, nch, s, 1, st, hist0);
+      rc = count_pass<2>(items, d_m, m, k, lo_bit, nb, nch, s, 1, st, hist0);
       if (rc) return rc;
       const int tma_it = (reinterpret_cast<uintptr_t>(items) & 15) == 0;
-      if (seg) pk = s.posA;
-      rc = (npass != 1 || seg) ? launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, nlo, nb, nch, s, tma_it, st)
+      rc = npass != 1 ? launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, items, nullptr, pk, nullptr, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
            : pos32_dst ? launch_nsweep<kInPk, kOutFpPos32, 256, 16>(items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st)
                        : launch_nsweep_cfg<kInPk, kOutFpPos>(ipt_pk, items, nullptr, fo, po, d_m, m, k, lo_bit, nb, nch, s, tma_it, st);
       if (rc) return rc;
@@ -1207,38 +919,7 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
     }
   }
   // ---- narrow passes 1.. (packed items in, packed or final out)
-  if (seg) {
-    // segmented plan: LSD passes over [nlo, hi_bit) from items to items, then the local pass
-    const uint64_t nseg = 1ull << (hi_bit - nlo);
-    const uint64_t* kin = s.posA;
-    if (npassN == 2) {
-      MZS_CUDA(cudaMemsetAsync(seg->pair, 0, sizeof(unsigned long long) * nseg, st));
-      const int sh = nlo + 8, nb = hi_bit - sh;
-      const unsigned grid = (unsigned)std::min<uint64_t>(nch, (uint64_t)num_sms() * 8);
-      upsweep_pair_kernel<<<grid, kTPB, 0, st>>>(kin, d_m, m, sh, nb, nlo, s.counts, nch, s.ctl, 1, s.chunk, seg->pair);
-      MZS_LAUNCHED();
-      rc = count_pass<2>(kin, d_m, m, k, sh, nb, nch, s, 1, st, s.counts);  // counts from the pair upsweep
-      if (rc) return rc;
-      rc = launch_nsweep_cfg<kInPk, kOutPk>(ipt_pk, kin, nullptr, s.posB, nullptr, d_m, m, k, sh, nb, nch, s, 1, st);
-      if (rc) return rc;
-      kin = s.posB;
-    } else if (npassN != 1) {
-      return SLSUM_EINVAL;
-    }
-    seg_scan_kernel<<<1, kTPB, 0, st>>>(npassN == 2 ? seg->pair : s.totals, nseg, seg->seg_start, s.ctl, 1);
-    MZS_LAUNCHED();
-    const size_t sm = sizeof(SegSmem);
-    if (pos32_dst) {
-      MZS_CUDA(cudaFuncSetAttribute(segsort_kernel<kOutFpPos32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      segsort_kernel<kOutFpPos32><<<(unsigned)nseg, kTPB, sm, st>>>(kin, seg->seg_start, nseg, lo_bit, fp_dst, pos32_dst,
-                                                                    seg->offsets, s.ctl);
-    } else {
-      MZS_CUDA(cudaFuncSetAttribute(segsort_kernel<kOutFpPos>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      segsort_kernel<kOutFpPos><<<(unsigned)nseg, kTPB, sm, st>>>(kin, seg->seg_start, nseg, lo_bit, fp_dst, pos_dst,
-                                                                  seg->offsets, s.ctl);
-    }
-    MZS_LAUNCHED();
-  } else {
+  {
     const uint64_t* kin = nullptr;
     { uint64_t* pk; uint32_t* fo; uint64_t* po; pass_out(0, pk, fo, po); kin = pk; }
     for (int p = 1; p < npass; ++p) {
@@ -1259,34 +940,18 @@ int stable_sort(bool from_hash, const void* keys, const uint64_t* pos, const uin
   return SLSUM_OK;
 }
 
-// fill v[0..n) with ~0 (the gated replacement of the memset when the pointer table belongs to
-// one of two enqueued paths)
-__global__ void __launch_bounds__(kTPB) fill_ones_kernel(uint64_t* __restrict__ v, uint64_t n, const uint64_t* ctl,
-                                                         int want) {
-  if (gate_off(ctl, want)) return;
-  for (uint64_t i = (uint64_t)blockIdx.x * kTPB + threadIdx.x; i < n; i += (uint64_t)gridDim.x * kTPB) v[i] = ~0ull;
-}
-
-// ctl != nullptr: every kernel runs only when ctl[0] == want (the wide path's table when the
-// narrow path builds its own pointer table in segsort_kernel)
 int offsets_launch(const uint32_t* fp, const uint64_t* d_m, uint64_t m, int shift, uint32_t bmask, uint64_t nb,
-                   uint64_t* offsets, uint64_t* tile_min, cudaStream_t st, const uint64_t* ctl = nullptr,
-                   int want = 0) {
-  if (ctl) {
-    fill_ones_kernel<<<grid_stride_blocks(nb + 1), kTPB, 0, st>>>(offsets, nb + 1, ctl, want);
-    MZS_LAUNCHED();
-  } else {
-    MZS_CUDA(cudaMemsetAsync(offsets, 0xff, sizeof(uint64_t) * (nb + 1), st));
-  }
+                   uint64_t* offsets, uint64_t* tile_min, cudaStream_t st) {
+  MZS_CUDA(cudaMemsetAsync(offsets, 0xff, sizeof(uint64_t) * (nb + 1), st));
   const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((m / 16 + kTPB) / kTPB, (uint64_t)num_sms() * 8));
-  offsets_scatter_kernel<<<(unsigned)blocks, kTPB, 0, st>>>(fp, d_m, m, shift, bmask, nb, offsets, ctl, want);
+  offsets_scatter_kernel<<<(unsigned)blocks, kTPB, 0, st>>>(fp, d_m, m, shift, bmask, nb, offsets);
   MZS_LAUNCHED();
   const uint64_t n = nb + 1, nt = (n + kSminTile - 1) / kSminTile;
-  smin_reduce_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min, ctl, want);
+  smin_reduce_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min);
   MZS_LAUNCHED();
-  smin_tiles_kernel<<<1, kTPB, 0, st>>>(tile_min, nt, ctl, want);
+  smin_tiles_kernel<<<1, kTPB, 0, st>>>(tile_min, nt);
   MZS_LAUNCHED();
-  smin_apply_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min, ctl, want);
+  smin_apply_kernel<<<(unsigned)nt, kTPB, 0, st>>>(offsets, n, tile_min);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }
@@ -1385,10 +1050,6 @@ MZS_API size_t seedtable_workspace_bytes(uint64_t m, int bucket_bits) {
   const int npass = (bucket_bits + 7) / 8;
   size_sort_ws(z, m, npass, true);
   z.take<uint64_t>(smin_tiles_for(1ull << bucket_bits));
-  if (radix_segmented(bucket_bits)) {  // pair counts + segment starts of the segmented plan
-    z.take<unsigned long long>(65536);
-    z.take<uint64_t>(65537);
-  }
   return z.used;
 }
 
@@ -1418,22 +1079,13 @@ static int seedtable_build_impl(const uint64_t* items, const uint64_t* hash, con
   SortWs s;
   if (!carve_sort_ws(c, m, npass, true, s)) return SLSUM_ENOMEM;
   uint64_t* tile_min = c.take<uint64_t>(smin_tiles_for(nb));
-  SegPlan plan{};
-  const bool segd = items != nullptr && radix_segmented(bucket_bits);
-  if (radix_segmented(bucket_bits)) {
-    plan.pair = c.take<unsigned long long>(65536);
-    plan.seg_start = c.take<uint64_t>(65537);
-    plan.offsets = offsets;
-  }
   if (!c.ok) return SLSUM_ENOMEM;
   uint32_t* fp_final = fp_out ? fp_out : s.fpF;
   const int lo = 32 - bucket_bits;
   int rc = stable_sort(true, hash, pos, d_m, m, k, lo, 32, fp_final, pos_out, s, st, items, pos32_out,
-                       items ? hist0 : nullptr, segd ? &plan : nullptr);
+                       items ? hist0 : nullptr);
   if (rc) return rc;
-  // segmented plan: the narrow path's pointer table comes from segsort_kernel; this one is the
-  // wide path's (gated on ctl[0] == 0)
-  return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st, segd ? s.ctl : nullptr, 0);
+  return offsets_launch(fp_final, d_m, m, lo, (uint32_t)(nb - 1), nb, offsets, tile_min, st);
 }
 
 MZS_API int seedtable_build(const uint64_t* hash, const uint64_t* pos, uint64_t m, const uint64_t* d_m, int k,

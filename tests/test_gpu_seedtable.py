@@ -267,62 +267,6 @@ def test_items_path_vs_oracle(k, pos_base, path):
         assert np.array_equal(fp32[:m].cpu().numpy(), wf)
 
 
-def _items_of(key, pos, k):
-    return _dev((_fp_np(key, k) << np.uint64(32)) | (pos & np.uint64(0xFFFFFFFF)))
-
-
-def _cmp_items(key, pos, k, bits, cap_extra=0):
-    """seedtable_build_items / _items32 (and with a device count below the capacity) vs the oracle"""
-    m = len(key)
-    wo, wf, wpos = O.seedtable(key, pos, k, bits)
-    kpad = np.concatenate([key, np.zeros(cap_extra, np.uint64)])
-    ppad = np.concatenate([pos, np.full(cap_extra, pos[-1] if m else 0, np.uint64)])
-    it, kt, pt = _items_of(kpad, ppad, k), _dev(kpad), _dev(ppad)
-    dm = torch.tensor([m], dtype=torch.int64, device="cuda").view(torch.uint64) if cap_extra else None
-    off, po, fp = P.seedtable_build_items(it, kt, pt, k, bits, m=m + cap_extra, d_m=dm)
-    torch.cuda.synchronize()
-    assert np.array_equal(off.cpu().numpy(), wo)
-    assert np.array_equal(po[:m].cpu().numpy(), wpos)
-    assert np.array_equal(fp[:m].cpu().numpy(), wf)
-    off32, po32, fp32 = P.seedtable_build_items32(it, kt, pt, k, bits, m=m + cap_extra, d_m=dm)
-    torch.cuda.synchronize()
-    assert np.array_equal(off32.cpu().numpy(), wo)
-    assert np.array_equal(po32[:m].cpu().numpy(), (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32))
-    assert np.array_equal(fp32[:m].cpu().numpy(), wf)
-
-
-@pytest.mark.parametrize("bits", [9, 12, 16, 17, 20, 23, 24])
-def test_items_segmented_plan(bits):
-    """The segmented plan of the packed-item path (9 <= bits <= 24: LSD passes over the bucket's
-    top bits - 8, then segsort_kernel per prefix segment, which also writes the pointer table):
-    random keys, heavy repeats, and a device count below the capacity."""
-    rng = np.random.default_rng(bits)
-    k = 19
-    m = 120_000
-    key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
-    pos = np.cumsum(rng.integers(1, 40, size=m, dtype=np.uint64)) + np.uint64(1000)
-    _cmp_items(key, pos, k, bits)
-    heavy = np.where(rng.random(m) < 0.3, np.uint64(0x12345678), key)   # one bucket of ~36k entries
-    _cmp_items(heavy, pos, k, bits, cap_extra=13)
-
-
-def test_items_segments_spanning_tiles():
-    """Prefix segments of exactly one tile (4096 items), one tile + 1, two tiles and three tiles
-    + 1 (segsort_kernel's multi-tile walk with running digit offsets), among random keys; k=16 so
-    the fingerprint is the key and the prefix is its top 16 bits (bits = 24)."""
-    rng = np.random.default_rng(5)
-    k, bits = 16, 24
-    parts = [rng.integers(0, 1 << 32, size=20_000, dtype=np.uint64)]
-    for pre, n in ((5, 4096), (9, 4097), (0xABCD, 8192), (0xFFFF, 12289), (0x8000, 4095)):
-        parts.append((np.uint64(pre) << np.uint64(16)) | rng.integers(0, 1 << 16, size=n, dtype=np.uint64))
-    key = np.concatenate(parts)
-    key = key[rng.permutation(len(key))]
-    pos = np.arange(len(key), dtype=np.uint64) * np.uint64(3)
-    _cmp_items(key, pos, k, bits)
-    # every entry of one bucket (one segment, one local digit)
-    _cmp_items(np.full(9000, 0xABCDEF12, np.uint64), np.arange(9000, dtype=np.uint64), k, bits)
-
-
 @pytest.mark.parametrize("npass_bits", [12, 16, 24, 30])
 def test_items32_wide_spans_and_bit_widths(npass_bits):
     """seedtable_build_items32 when the positions span >= 2^32 (the wide path, narrowed to u32
@@ -347,14 +291,11 @@ def test_items32_wide_spans_and_bit_widths(npass_bits):
 def _hist_oracle(wk, k, bits, cap):
     """The first radix pass's digit counts, from the ORACLE records: chunks of the radix chunk
     size for m = cap (at most 131072 entries, at least 4096, ~cap/296 rounded up to 4096
-    between), digit = the first radix pass's digit of the bucket b = fp >> (32 - bits): bits
-    [8, 8 + min(8, bits - 8)) of b for 9 <= bits <= 24 (the segmented plan, include/mzslsum.h
-    mz_out.hist), else the low min(8, bits) bits of b."""
+    between), digit = the low min(8, bits) bits of the bucket fp >> (32 - bits)."""
     want = (cap + 295) // 296
     chunk = min(131072, max(4096, (want + 4095) // 4096 * 4096))
     nch = (cap + chunk - 1) // chunk
-    lo, nb = (8, min(8, bits - 8)) if 9 <= bits <= 24 else (0, min(8, bits))
-    d = (_fp_np(wk, k) >> np.uint64(32 - bits + lo)) & np.uint64((1 << nb) - 1)
+    d = (_fp_np(wk, k) >> np.uint64(32 - bits)) & np.uint64((1 << min(8, bits)) - 1)
     c = np.arange(len(wk), dtype=np.uint64) // np.uint64(chunk)
     h = np.zeros((256, nch), dtype=np.int64)
     np.add.at(h, (d.astype(np.int64), c.astype(np.int64)), 1)
