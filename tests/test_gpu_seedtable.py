@@ -267,6 +267,61 @@ def test_items_path_vs_oracle(k, pos_base, path):
         assert np.array_equal(fp32[:m].cpu().numpy(), wf)
 
 
+def _items_of(key, pos, k):
+    return _dev((_fp_np(key, k) << np.uint64(32)) | (pos & np.uint64(0xFFFFFFFF)))
+
+
+def _cmp_items(key, pos, k, bits, cap_extra=0):
+    """seedtable_build_items / _items32 (and with a device count below the capacity) vs the oracle"""
+    m = len(key)
+    wo, wf, wpos = O.seedtable(key, pos, k, bits)
+    kpad = np.concatenate([key, np.zeros(cap_extra, np.uint64)])
+    ppad = np.concatenate([pos, np.full(cap_extra, pos[-1] if m else 0, np.uint64)])
+    it, kt, pt = _items_of(kpad, ppad, k), _dev(kpad), _dev(ppad)
+    dm = torch.tensor([m], dtype=torch.int64, device="cuda").view(torch.uint64) if cap_extra else None
+    off, po, fp = P.seedtable_build_items(it, kt, pt, k, bits, m=m + cap_extra, d_m=dm)
+    torch.cuda.synchronize()
+    assert np.array_equal(off.cpu().numpy(), wo)
+    assert np.array_equal(po[:m].cpu().numpy(), wpos)
+    assert np.array_equal(fp[:m].cpu().numpy(), wf)
+    off32, po32, fp32 = P.seedtable_build_items32(it, kt, pt, k, bits, m=m + cap_extra, d_m=dm)
+    torch.cuda.synchronize()
+    assert np.array_equal(off32.cpu().numpy(), wo)
+    assert np.array_equal(po32[:m].cpu().numpy(), (wpos & np.uint64(0xFFFFFFFF)).astype(np.uint32))
+    assert np.array_equal(fp32[:m].cpu().numpy(), wf)
+
+
+@pytest.mark.parametrize("bits", [9, 12, 16, 17, 20, 23, 24])
+def test_items_bit_widths(bits):
+    """The packed-item path at 9..24 bucket bits (2 or 3 radix passes, a last digit of 1..8 bits):
+    random keys, heavy repeats, and a device count below the capacity."""
+    rng = np.random.default_rng(bits)
+    k = 19
+    m = 120_000
+    key = rng.integers(0, 1 << 38, size=m, dtype=np.uint64)
+    pos = np.cumsum(rng.integers(1, 40, size=m, dtype=np.uint64)) + np.uint64(1000)
+    _cmp_items(key, pos, k, bits)
+    heavy = np.where(rng.random(m) < 0.3, np.uint64(0x12345678), key)   # one bucket of ~36k entries
+    _cmp_items(heavy, pos, k, bits, cap_extra=13)
+
+
+def test_items_clustered_prefixes():
+    """Runs of 4095, 4096, 4097, 8192 and 12289 entries sharing the top 16 bits of the key (a
+    downsweep tile holds 4096 items) among random keys, and one bucket holding every entry; k=16
+    so the fingerprint is the key (bits = 24)."""
+    rng = np.random.default_rng(5)
+    k, bits = 16, 24
+    parts = [rng.integers(0, 1 << 32, size=20_000, dtype=np.uint64)]
+    for pre, n in ((5, 4096), (9, 4097), (0xABCD, 8192), (0xFFFF, 12289), (0x8000, 4095)):
+        parts.append((np.uint64(pre) << np.uint64(16)) | rng.integers(0, 1 << 16, size=n, dtype=np.uint64))
+    key = np.concatenate(parts)
+    key = key[rng.permutation(len(key))]
+    pos = np.arange(len(key), dtype=np.uint64) * np.uint64(3)
+    _cmp_items(key, pos, k, bits)
+    # every entry of one bucket (one segment, one local digit)
+    _cmp_items(np.full(9000, 0xABCDEF12, np.uint64), np.arange(9000, dtype=np.uint64), k, bits)
+
+
 @pytest.mark.parametrize("npass_bits", [12, 16, 24, 30])
 def test_items32_wide_spans_and_bit_widths(npass_bits):
     """seedtable_build_items32 when the positions span >= 2^32 (the wide path, narrowed to u32
