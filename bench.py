@@ -761,7 +761,7 @@ def main():
                     ev_d2h[b].record(s_d2h)
                 return 8 * ((1 << bits) + 1) + esz * m
 
-            ke = max(3, min(args.steps, 6))
+            ke = max(3, args.steps)                      # the K timed steps (fill and drain amortised over K)
             enqueue(0)                                   # warm-up step (untimed)
             readback(0)
             torch.cuda.synchronize()
@@ -797,13 +797,16 @@ def main():
         seq2 = torch.empty_like(seq)
         torch.cuda.synchronize()
 
+        hbuf = {}   # pinned read-back buffers, allocated in the untimed first call and reused
+
         def e2e_step_mg():
             seq2.copy_(host_in, non_blocking=True)
             off, pl, fl, base = step(seq2)
-            ho = torch.empty(off.numel(), dtype=off.dtype, pin_memory=True)
-            hp = torch.empty(pl.numel(), dtype=pl.dtype, pin_memory=True)
-            ho.copy_(off, non_blocking=True)
-            hp.copy_(pl, non_blocking=True)
+            for key, t in (("off", off), ("pos", pl)):
+                if key not in hbuf or hbuf[key].numel() < t.numel() or hbuf[key].dtype != t.dtype:
+                    hbuf[key] = torch.empty(max(1, t.numel() + t.numel() // 8), dtype=t.dtype, pin_memory=True)
+            hbuf["off"][:off.numel()].copy_(off, non_blocking=True)
+            hbuf["pos"][:pl.numel()].copy_(pl, non_blocking=True)
             torch.cuda.synchronize()
             return 8 * (off.numel() + pl.numel())
 
@@ -811,7 +814,7 @@ def main():
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         bev = torch.cuda.Event(enable_timing=True)
-        ke = max(1, min(args.steps, 3))
+        ke = max(1, args.steps)
         a.record(stream)
         d2h = 0
         for _ in range(ke):
