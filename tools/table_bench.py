@@ -29,13 +29,14 @@ h, p, c = P.mz_extract_ex(words, k, w, n=n, kind=P.MZ_IN_PACKED2, invalid=inval,
                           out_hist=hist, hist_bits=bits)
 ws = torch.empty(P.seedtable_workspace_bytes(cap, bits), dtype=torch.uint8, device="cuda")
 off = torch.empty((1 << bits) + 1, dtype=torch.uint64, device="cuda")
-po = torch.empty(cap, dtype=torch.uint64, device="cuda")
+pos32 = os.environ.get("MZS_TB_POS32", "0") == "1"   # bench.py's table: 32-bit positions
+po = torch.empty(cap, dtype=torch.uint32 if pos32 else torch.uint64, device="cuda")
 fp = torch.empty(cap, dtype=torch.uint32, device="cuda")
 
 
 def run():
     P.seedtable_build_items_ex(items, h, p, k, bits, m=cap, d_m=c, hist=hist, offsets=off, pos_out=po, fp_out=fp,
-                               ws=ws)
+                               ws=ws, pos32=pos32)
 
 
 for _ in range(3):
@@ -50,6 +51,7 @@ for _ in range(reps):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
 m = int(c.item())
-mix = (po[:m].view(torch.int64) * 0x9E3779B97F4A7C15 + fp[:m].view(torch.int32).to(torch.int64)).sum().item()
-print(f"fused_hist={int(fused)} m={m} table ms: median {sorted(ts)[len(ts) // 2]:.3f} best {min(ts):.3f} "
+pv = po[:m].view(torch.int32).to(torch.int64) if pos32 else po[:m].view(torch.int64)
+mix = (pv * 0x9E3779B97F4A7C15 + fp[:m].view(torch.int32).to(torch.int64)).sum().item()
+print(f"fused_hist={int(fused)} pos32={int(pos32)} ncfg={os.environ.get('MZS_NCFG', '-')}/{os.environ.get('MZS_NCFG_LAST', '-')} m={m} table ms: median {sorted(ts)[len(ts) // 2]:.3f} best {min(ts):.3f} "
       f"checksum {mix & 0xFFFFFFFFFFFFFFFF:016x} off_last {int(off[-1].item())}", flush=True)
