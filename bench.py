@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--canonical", action="store_true",
                     help="c3/c4: canonical (strand-symmetric) minimizers, MZ_KEY_CANON (NEXT f4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pos64", action="store_true", help="c3: skip the u64-position-table step timed beside the line")
     ap.add_argument("--cpu-sample-bases", type=int, default=32_000_000)
     return ap.parse_args()
 
@@ -626,7 +627,7 @@ def main():
 
     # encode + mz + seed table: path-select kernel, 3 narrow passes x (upsweep, chunk scan, digit
     # scan, downsweep), 3 wide passes (enqueued, gated off at entry), 4 pointer-table kernels
-    table_launches = 1 + 12 + 12 + 4 - (1 if FUSED_HIST else 0)
+    table_launches = 1 + 12 + 12 + 4 - (1 if FUSED_HIST else 0) + (1 if (world == 1 and c3 is not None and n_total < (1 << 32)) else 0)  # + the gated wide-path u32 narrowing
     # N>1: count, partition (NCCL: ctl + 4 narrow + 4 wide; p2p: ctl + 3 scan kernels + the fused
     # nsweep writing into the peers), finalize (ctl + 2 passes x 12 + 4)
     part = 5 if EXCHANGE == "p2p" else 1 + 4 + 4
@@ -637,8 +638,11 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # positions below 2^32 (C3 at one GPU): the table stores them as u32, exactly (R34,
+    # seedtable_build_items32) -- the table the e2e line reads back; the u64 table is timed beside it
+    tab32 = world == 1 and c3 is not None and n_total < (1 << 32)
     for _ in range(max(3, args.warmup)):
-        step(seq)
+        step(seq, pos32=tab32)
     torch.cuda.synchronize()
     m_local = int(d_count.view(torch.int64).item())
     if m_local > cap:
@@ -651,7 +655,7 @@ def main():
     with Clocks(local) as clk:
         t0.record(stream)
         for _ in range(args.steps):
-            step(seq, record=True)
+            step(seq, record=True, pos32=tab32)
         t1.record(stream)
         barrier()
     ms = t0.elapsed_time(t1)
@@ -663,6 +667,21 @@ def main():
     gbases = n_total / (ms_step * 1e-3) / 1e9
 
     phase_ms = {kk: statistics.mean(a.elapsed_time(b) for a, b in v) for kk, v in ev.items()}
+    pos64_line = None
+    if tab32 and not args.no_pos64:
+        # the same step with the u64 position table (seedtable_build_items_ex, pos_out)
+        for _ in range(max(3, args.warmup)):
+            step(seq)
+        barrier()
+        a64, b64 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a64.record(stream)
+        for _ in range(args.steps):
+            step(seq)
+        b64.record(stream)
+        barrier()
+        ms64 = a64.elapsed_time(b64) / args.steps
+        pos64_line = {"value": n_total / (ms64 * 1e-3) / 1e9, "unit": "Gbases/s", "ms_per_step": ms64,
+                      "steps": args.steps, "table_positions": "u64 (seedtable_build_items_ex, pos_out)"}
     # per-step device times (encode start -> table end of each timed step): median and best
     per_step = [a.elapsed_time(d) for (a, _), (_, d) in zip(ev["encode"], ev["table"])]
     step_stats = {"median_ms": statistics.median(per_step), "best_ms": min(per_step), "steps": len(per_step)}
@@ -835,7 +854,8 @@ def main():
         "encode": n * (1 + 0.25 + 0.125),
         # records: hash + pos (16 B), plus the 8-byte packed item at N=1 (seedtable_build_items)
         "extract": n * (0.25 + 0.125) + m_rec * (24 if world == 1 else 16),
-        "table": m_rec * SEEDTABLE_BYTES_PER_REC + 8 * ((1 << bits) + 1),
+        # the last pass writes u32 positions with the 32-bit table (4 B less per entry)
+        "table": m_rec * (SEEDTABLE_BYTES_PER_REC - (4 if tab32 else 0)) + 8 * ((1 << bits) + 1),
     }
     clk = clk_sum = clk.summary()
     sm_mhz = clk.get("sm_mhz") or sm_max
@@ -865,8 +885,8 @@ def main():
                   "traffic": tab_traffic,
                   "traffic_note": "DRAM bytes of the radix passes' upsweeps + downsweeps (ncu; the first "
                                   "pass's counts come from the minimizer kernel, so 2 upsweeps); the "
-                                  "SURVEY's algorithmic model is 32 B/entry, the 3-pass LSD on 8-byte "
-                                  "items moves 68 B/entry",
+                                  f"SURVEY's algorithmic model is {SEEDTABLE_BYTES_PER_REC - (4 if tab32 else 0)} "
+                                  f"B/entry, the 3-pass LSD on 8-byte items moves {64 if tab32 else 68} B/entry",
                   "peak_kind": peak_kind, "frac_vs_nominal_8tbs": tab_ach / 8000.0, "ms": phase_ms["table"]}
     step_bytes = sum(per_phase_bytes.values())
     step_hbm = {"achieved": step_bytes / (ms_step * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -913,12 +933,15 @@ def main():
                        "l2": ("inputs (3.1 GB) >> L2 (126 MB); no flush needed" if c3 is not None else
                               "eager loop on L2-resident inputs (1 MB); cuda_graph has the L2-flushed time"),
                        "parallelism": f"shards{world}",
-                       "exchange": EXCHANGE if world > 1 else None},
+                       "exchange": EXCHANGE if world > 1 else None,
+                       "table_positions": ("u32 (seedtable_build_items_ex, pos32; exact: C3 has < 2^32 bases)"
+                                           if tab32 else "u64")},
             "roofline": roof,
             "roofline_table": roof_table,
             "hbm_step": step_hbm,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "table_pos64": pos64_line,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk_sum,
         }

@@ -10,13 +10,13 @@ mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
 # launch list of one timed C3 step (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c3.csv \
-  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/launches_c3.log 2>&1
+  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-pos64 > $O/launches_c3.log 2>&1
 # full sections of the step's kernels: encode, mz, 3 x (upsweep, nsweep) of the narrow path
 # (the 3 x 2 gated wide-path launches also match and are captured as no-ops); the 3 warm-up
 # steps are skipped (13 matching launches per step since the first pass takes its counts from the
 # minimizer kernel)
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mz_fast|^nsweep|encode_kernel|upsweep" \
-  -s 39 -c 13 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/full_c3.log 2>&1
+  -s 39 -c 13 -o $O/full_c3 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-pos64 > $O/full_c3.log 2>&1
 for cfg in "min 256 generic" "min 1024 generic" "min 1024 commutative" "min 256 commutative"; do
   set -- $cfg
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"slsum" -s 3 -c 1 \
