@@ -930,8 +930,13 @@ int launch_doubling_warp(const void* xv, void* yv, uint64_t n, uint32_t w, cudaS
 template <class Op, int TPB, int XR = 0>
 __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename Op::T* __restrict__ x,
                                                                typename Op::T* __restrict__ y, uint64_t n,
-                                                               uint32_t w, uint64_t nout, uint32_t tout) {
+                                                               uint32_t w, uint64_t nout, uint32_t tout,
+                                                               int four) {
   // XR extra register rounds: shifts up to 2E << XR, spans overlapping by 4E << XR
+  // four (w = 2^m, m - 2 >= RR): the shared-memory rounds stop at t_{m-2} and the output takes
+  // y[i] = t_{m-2}[i] (+) t_{m-2}[i+d] (+) t_{m-2}[i+2d] (+) t_{m-2}[i+3d], d = w/4: two
+  // rounds' stores and barriers fewer for one more (+) per output (the four windows of d
+  // partition the window of w, so any commutative op is exact)
   using T = typename Op::T;
   constexpr int E = (sizeof(T) == 4) ? 16 : 8;
   constexpr uint32_t OV = 16 / sizeof(T);
@@ -982,7 +987,8 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename O
   T* cur = B;
   T* nxt = A;
   const int m = 31 - __clz(w);
-  for (int r = RR; r < m; ++r) {
+  const int mend = four ? m - 2 : m;
+  for (int r = RR; r < mend; ++r) {
     const uint32_t d = 1u << r;               // a multiple of OV
     for (uint32_t e = t * OV; e + d < Lv; e += TPB * OV) {
       T a[OV], c[OV], o[OV];
@@ -998,7 +1004,25 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename O
   const uint32_t dd = w - (1u << m);          // 0 unless an idempotent op with w not a power of two
   const uint32_t e_end = (uint32_t)min((uint64_t)tout, nout - g0);
   const bool vout = ((reinterpret_cast<uintptr_t>(y + g0) & 15) == 0) && e_end == tout;
-  if (vout) {
+  if (four) {
+    const uint32_t d = 1u << (m - 2);           // a multiple of OV
+    for (uint32_t e = t * OV; e < e_end; e += TPB * OV) {
+      T a[OV], b[OV], c[OV], f[OV], o[OV];
+      *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(cur + e);
+      *reinterpret_cast<uint4*>(b) = *reinterpret_cast<const uint4*>(cur + e + d);
+      *reinterpret_cast<uint4*>(c) = *reinterpret_cast<const uint4*>(cur + e + 2 * d);
+      *reinterpret_cast<uint4*>(f) = *reinterpret_cast<const uint4*>(cur + e + 3 * d);
+#pragma unroll
+      for (uint32_t q = 0; q < OV; ++q) o[q] = Op::op(Op::op(a[q], b[q]), Op::op(c[q], f[q]));
+      if (vout) {
+        *reinterpret_cast<uint4*>(y + g0 + e) = *reinterpret_cast<const uint4*>(o);
+      } else {
+#pragma unroll
+        for (uint32_t q = 0; q < OV; ++q)
+          if (e + q < e_end) y[g0 + e + q] = o[q];
+      }
+    }
+  } else if (vout) {
     for (uint32_t e = t * OV; e < tout; e += TPB * OV) {
       T a[OV], c[OV], o[OV];
       *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(cur + e);
@@ -1031,7 +1055,11 @@ int launch_doubling_rs(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStr
   const size_t smem = 2 * sizeof(T) * ((size_t)L + 2 * OV);
   auto k = slsum_doubling_rs_kernel<Op, TPB, XR>;
   MZS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, w, nout, tout);
+  constexpr int RR = ((E == 16) ? 6 : 5) + XR;
+  int m = 0;
+  while ((2u << m) <= w) ++m;                   // 2^m <= w < 2^(m+1)
+  const int four = (w & (w - 1)) == 0 && m - 2 >= RR && !env_flag("MZS_SLSUM_NO_RS4");
+  k<<<(unsigned)grid, TPB, smem, st>>>(static_cast<const T*>(xv), static_cast<T*>(yv), n, w, nout, tout, four);
   MZS_LAUNCHED();
   return SLSUM_OK;
 }

@@ -243,11 +243,14 @@ def test_generic_large_blocks(op, m_lanes):
 
 @pytest.mark.parametrize("op,w", [(P.SLSUM_MIN_U32, 128), (P.SLSUM_MIN_U32, 1024), (P.SLSUM_ADD_U32, 256),
                                   (P.SLSUM_ADD_U32, 4096), (P.SLSUM_ADD_F32, 512), (P.SLSUM_MAX_U32, 300),
-                                  (P.SLSUM_MAX_U32, 2049), (P.SLSUM_MIN_U64, 64), (P.SLSUM_MIN_U64, 777)])
+                                  (P.SLSUM_MAX_U32, 2049), (P.SLSUM_MIN_U64, 64), (P.SLSUM_MIN_U64, 777),
+                                  (P.SLSUM_MIN_U64, 256), (P.SLSUM_ADD_F32, 2048), (P.SLSUM_ADD_U32, 1024)])
 def test_commutative_register_start(op, w):
     """The COMMUTATIVE kernel for w >= 8E (first rounds in registers on overlapping warp spans,
     the rest in shared memory): power-of-two w for any commutative op, other w for idempotent
-    ones; several tiles, a ragged end, and a misaligned view."""
+    ones; several tiles, a ragged end, and a misaligned view.  Power-of-two w with log2(w) - 2
+    register-or-more rounds finish with the 4-way combine of t_{m-2} (MIN_U32 1024, ADD_U32
+    1024 / 4096, ADD_F32 512 / 2048, MIN_U64 256)."""
     rng = np.random.default_rng(op * 31 + w)
     for n in (w + 16 * 1024, 200_003, 1 << 20):
         x = _input(op, n, rng)
