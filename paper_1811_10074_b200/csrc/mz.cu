@@ -27,6 +27,9 @@ constexpr int kSlotBits = 14;  // slot index inside a tile (< 16384)
 #ifndef MZS_MZ_MARK32
 #define MZS_MZ_MARK32 1
 #endif
+#ifndef MZS_MZ_MARKW
+#define MZS_MZ_MARKW 1   // FULL-strip argmin marks from the key's low word (see fast_phase2)
+#endif
 #ifndef MZS_MZ_OUT_U
 #define MZS_MZ_OUT_U 4   // records per thread per step of the fast path's output loop
 #endif
@@ -631,12 +634,23 @@ __device__ __forceinline__ void fast_phase2(const Key* keys, const uint32_t* wvb
       // once after the strip (R3)
       if (kM32 && MASKED) {
         MZS_DCHECK(s - mbase < 32u);
+#if MZS_MZ_MARKW
+        m32 |= __funnelshift_l(0u, (vmb >> (uint32_t)(j - (int)mbase + 1)) & 1u, (uint32_t)y.v - mbase);
+#else
         m32 |= ((vmb >> (uint32_t)(j - (int)mbase + 1)) & 1u) << (s - mbase);
+#endif
       } else if (MASKED) {
         em |= (uint64_t)((vm >> (j - jb + 1)) & 1u) << (s - (uint32_t)(jb + 1));
       } else if (kM32) {
         MZS_DCHECK(s - mbase < 32u);
+#if MZS_MZ_MARKW
+        // (low key word - mbase) mod 32 = s - mbase: the slot is the key's low 14 bits and
+        // s >= mbase, so the subtraction borrows nothing from above them; the wrapping funnel
+        // shift uses only those 5 bits (no slot mask)
+        m32 |= __funnelshift_l(0u, 1u, (uint32_t)y.v - mbase);
+#else
         m32 |= 1u << (s - mbase);
+#endif
       } else {
         MZS_DCHECK(s - (uint32_t)(jb + 1) < 64u);
         em |= 1ull << (s - (uint32_t)(jb + 1));
