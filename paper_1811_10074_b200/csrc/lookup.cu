@@ -112,7 +112,10 @@ __global__ void __launch_bounds__(kLTPB) lookup_kernel(const uint64_t* __restric
 // The count step also records each query's first matching entry (first[i]); the emit step
 // then skips the queries without hits and starts at that entry -- no second pointer-table
 // read and no second scan of the leading entries (one dependent random access fewer).
-template <bool EMIT>
+// POS1 (sorted lookup with the packed-item unsort): first[i] already holds the POSITION of a
+// query's only hit (count 1; the count step read it while it walked the buckets in order), and
+// the first match's table index otherwise.
+template <bool EMIT, bool POS1 = false>
 __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restrict__ q, uint64_t nq_cap,
                                                         const uint64_t* d_nq, int k, int bits,
                                                         const uint64_t* __restrict__ offsets,
@@ -130,6 +133,10 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
       // the hits are the first o_end - o entries from first[i] on whose fingerprint is f;
       // first[i] itself is one (no need to read its fingerprint again)
       const uint64_t e0 = first[i];
+      if (POS1 && o + 1 == o_end) {
+        if (o < hit_cap) hit_pos[o] = e0;  // the position itself
+        continue;
+      }
       if (o < hit_cap) hit_pos[o] = pos_tab[e0];
       if (++o == o_end) continue;
       const uint32_t f = fp_of(q[i], k);
@@ -277,7 +284,12 @@ __global__ void __launch_bounds__(kLTPB) lookup_sorted_count_pk_kernel(const uin
                                                                        const uint64_t* __restrict__ ord, uint64_t nq,
                                                                        int bits, const uint64_t* __restrict__ offsets,
                                                                        const uint32_t* __restrict__ fp,
-                                                                       uint64_t* __restrict__ items) {
+                                                                       uint64_t* __restrict__ items,
+                                                                       const uint64_t* __restrict__ pos1_tab) {
+  // pos1_tab (the POS1 emit): a query with one hit carries that hit's POSITION in the item's low
+  // word -- read here, where the slices are walked in bucket order and the reads nearly in order,
+  // instead of by a random 8-byte read (~128 B of DRAM traffic) per hit in the query-order emit;
+  // a position >= 2^32 forces c = 15 (recounted by the unpack)
   for (uint64_t j = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; j < nq; j += (uint64_t)gridDim.x * kLTPB) {
     const uint64_t i = ord[j];
     const uint32_t f = fps[j];
@@ -291,8 +303,13 @@ __global__ void __launch_bounds__(kLTPB) lookup_sorted_count_pk_kernel(const uin
         ++cnt;
       }
     }
-    const uint32_t c = (cnt >= 15 || (e0 >> 32) != 0) ? 15u : cnt;
-    items[j] = ((uint64_t)(((uint32_t)i << 4) | c) << 32) | (uint32_t)e0;
+    uint32_t c = (cnt >= 15 || (e0 >> 32) != 0) ? 15u : cnt;
+    uint64_t lo32 = e0;
+    if (pos1_tab && c == 1) {
+      lo32 = pos1_tab[e0];
+      if (lo32 >> 32) c = 15;
+    }
+    items[j] = ((uint64_t)(((uint32_t)i << 4) | c) << 32) | (uint32_t)lo32;
   }
 }
 
@@ -302,7 +319,8 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_kernel(const uint64_t* __
                                                               const uint64_t* __restrict__ offsets,
                                                               const uint32_t* __restrict__ fp,
                                                               uint64_t* __restrict__ hit_off,
-                                                              uint64_t* __restrict__ first) {
+                                                              uint64_t* __restrict__ first,
+                                                              const uint64_t* __restrict__ pos1_tab) {
   for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
     const uint64_t it = items[i];
     MZS_DCHECK((it >> 36) == i);
@@ -320,6 +338,7 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_kernel(const uint64_t* __
           ++cnt;
         }
       }
+      if (pos1_tab && cnt == 1) e0 = pos1_tab[e0];  // (POS1) the only hit's position
       hit_off[i] = cnt;
     } else {
       hit_off[i] = c;
@@ -336,7 +355,9 @@ constexpr int kUE = 8;
 constexpr int kUT = kLTPB * kUE;
 __device__ __forceinline__ void unpack_one(uint64_t it, uint64_t i, const uint64_t* __restrict__ q, int k, int bits,
                                            const uint64_t* __restrict__ offsets, const uint32_t* __restrict__ fp,
-                                           uint64_t& cnt, uint64_t& e0) {
+                                           const uint64_t* __restrict__ pos1_tab, uint64_t& cnt, uint64_t& e0) {
+  // pos1_tab: e0 of a count-1 query is its hit's position (from the item, or read here after a
+  // recount); otherwise the first match's table index
   MZS_DCHECK((it >> 36) == i);
   const uint32_t c = (uint32_t)(it >> 32) & 15u;
   e0 = (uint32_t)it;
@@ -353,6 +374,7 @@ __device__ __forceinline__ void unpack_one(uint64_t it, uint64_t i, const uint64
         ++cnt;
       }
     }
+    if (pos1_tab && cnt == 1) e0 = pos1_tab[e0];
   }
 }
 __global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_t* __restrict__ items, uint64_t nq,
@@ -361,7 +383,8 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_
                                                                    const uint32_t* __restrict__ fp,
                                                                    uint64_t* __restrict__ hit_off,
                                                                    uint64_t* __restrict__ first, uint64_t* status,
-                                                                   uint32_t* tile_counter, uint64_t* d_total) {
+                                                                   uint32_t* tile_counter, uint64_t* d_total,
+                                                                   const uint64_t* __restrict__ pos1_tab) {
   __shared__ uint32_t s_tile;
   __shared__ uint64_t ws[kLTPB / 32];
   __shared__ uint64_t s_pre;
@@ -382,7 +405,7 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_
     }
 #pragma unroll
     for (int u = 0; u < kUE; ++u) {
-      unpack_one(it[u], i0 + u, q, k, bits, offsets, fp, cnt[u], e0[u]);
+      unpack_one(it[u], i0 + u, q, k, bits, offsets, fp, pos1_tab, cnt[u], e0[u]);
       sum += cnt[u];
     }
   } else {
@@ -390,7 +413,7 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_
     for (int u = 0; u < kUE; ++u) {
       cnt[u] = 0;
       e0[u] = 0;
-      if (i0 + u < nq) unpack_one(items[i0 + u], i0 + u, q, k, bits, offsets, fp, cnt[u], e0[u]);
+      if (i0 + u < nq) unpack_one(items[i0 + u], i0 + u, q, k, bits, offsets, fp, pos1_tab, cnt[u], e0[u]);
       sum += cnt[u];
     }
   }
@@ -589,7 +612,11 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
       // order (into ord, free after the count) -> counts and first matches in query order
       uint64_t* pk = idx;
       uint64_t* pq = ord;
-      lookup_sorted_count_pk_kernel<<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pk);
+      // POS1: the count step carries a count-1 query's hit POSITION (read in bucket order) to the
+      // emit, which then reads pos_tab only for multi-hit queries (MZS_LOOKUP_NO_POS1: off)
+      static const bool pos1_env = getenv("MZS_LOOKUP_NO_POS1") == nullptr;
+      const uint64_t* pos1_tab = (pos1_env && hit_cap && kEmitLanes == 1) ? pos_tab : nullptr;
+      lookup_sorted_count_pk_kernel<<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pk, pos1_tab);
       MZS_LAUNCHED();
       rc = sort_items(pk, nq, 4, 4 + qbits, pq, sws, sort_ws, st);
       if (rc) return rc;
@@ -604,10 +631,11 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
                              reinterpret_cast<uintptr_t>(first)) & 15) == 0;
       if (aligned) {
         lookup_unpack_scan_kernel<<<(unsigned)nt, kLTPB, 0, st>>>(pq, nq, qkey, k, bucket_bits, offsets, fp, hit_off,
-                                                                  first, status, counter, d_total);
+                                                                  first, status, counter, d_total, pos1_tab);
         MZS_LAUNCHED();
       } else {
-        lookup_unpack_kernel<<<g, kLTPB, 0, st>>>(pq, nq, qkey, k, bucket_bits, offsets, fp, hit_off, first);
+        lookup_unpack_kernel<<<g, kLTPB, 0, st>>>(pq, nq, qkey, k, bucket_bits, offsets, fp, hit_off, first,
+                                                  pos1_tab);
         MZS_LAUNCHED();
         scan_reduce_kernel<<<(unsigned)nb, kLTPB, 0, st>>>(hit_off, nq, nullptr, bsum);
         MZS_LAUNCHED();
@@ -619,7 +647,10 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
       if (hit_cap) {
         // the multi-hit queries scan their slice from the first match on: kEmitLanes lanes per
         // query (ballots) keep the scans short and the warp converged
-        if (kEmitLanes == 1) {
+        if (kEmitLanes == 1 && pos1_tab) {
+          lookup1_kernel<true, true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab,
+                                                          hit_off, hit_pos, hit_cap, first);
+        } else if (kEmitLanes == 1) {
           lookup1_kernel<true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab, hit_off,
                                                     hit_pos, hit_cap, first);
         } else {

@@ -123,6 +123,26 @@ def test_sorted_lookup_large_batches(k, bits):
         assert np.array_equal(hp[:c], hp_w[:c])
 
 
+@pytest.mark.parametrize("pos_hi", [0, 1 << 33])
+def test_sorted_lookup_single_hit_positions(pos_hi):
+    """The sorted lookup's count step carries a single-hit query's POSITION to the emit (read in
+    bucket order); a position >= 2^32 does not fit the packed item, so such queries are counted
+    again in query order and their position read there.  Hits equal the oracle's either way."""
+    k, bits = 15, 24
+    rng = np.random.default_rng(3 + pos_hi % 7)
+    m, nq = 300_000, (1 << 20) + 99
+    key = rng.integers(0, 1 << 30, size=m, dtype=np.uint64)          # mostly distinct: single hits
+    key[: m // 10] = key[m // 10: 2 * (m // 10)]                     # and some doubles
+    pos = np.sort(rng.choice(10 ** 9, size=m, replace=False)).astype(np.uint64) + np.uint64(pos_hi)
+    q = np.concatenate([key[rng.integers(0, m, size=nq - 5000)], rng.integers(0, 1 << 30, size=5000, dtype=np.uint64)])
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    ho_w, hp_w = O.lookup(q, k, bits, wo, wf, wp)
+    ho, hp, t = _gpu_lookup(key, pos, q, k, bits)
+    assert t == len(hp_w)
+    assert np.array_equal(ho[: nq + 1], ho_w)
+    assert np.array_equal(hp[:t], hp_w)
+
+
 @pytest.mark.parametrize("span", [1000, 20])
 def test_sorted_lookup_heavy_repeats(span):
     """The sorted lookup's packed per-query result carries hit counts up to 14; queries with 15
