@@ -1007,6 +1007,7 @@ __global__ void __launch_bounds__(TPB) slsum_doubling_rs_kernel(const typename O
   if (four) {
     const uint32_t d = 1u << (m - 2);           // a multiple of OV
     for (uint32_t e = t * OV; e < e_end; e += TPB * OV) {
+      MZS_DCHECK(e + 3 * d + OV <= L + 2 * OV);  // t_{m-2} reads stay inside the ping-pong buffer
       T a[OV], b[OV], c[OV], f[OV], o[OV];
       *reinterpret_cast<uint4*>(a) = *reinterpret_cast<const uint4*>(cur + e);
       *reinterpret_cast<uint4*>(b) = *reinterpret_cast<const uint4*>(cur + e + d);
