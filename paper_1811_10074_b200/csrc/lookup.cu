@@ -25,6 +25,10 @@ constexpr int kLTPB = 256;
 #define MZS_LOOKUP_EMIT_UNROLL 1
 #endif
 
+// POS1 paths: first[i] with this bit set is a table index to scan from (recounted queries with
+// two or more hits); without it, a position (one hit) or a side-array index (2..14 hits)
+constexpr uint64_t kScanFlag = 1ull << 63;
+
 __device__ __forceinline__ uint32_t fp_of(uint64_t key, int k) {
   const int b = 2 * k;
   return b >= 32 ? (uint32_t)(key >> (b - 32)) : (uint32_t)(key << (32 - b));
@@ -122,7 +126,9 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
                                                         const uint32_t* __restrict__ fp,
                                                         const uint64_t* __restrict__ pos_tab, uint64_t* hit_off,
                                                         uint64_t* __restrict__ hit_pos, uint64_t hit_cap,
-                                                        uint64_t* __restrict__ first) {
+                                                        uint64_t* __restrict__ first,
+                                                        const uint64_t* __restrict__ side = nullptr) {
+  // side (POS1): first[i] of a query with 2..14 hits indexes its positions in side (count step)
   const uint64_t nq = query_count(d_nq, nq_cap);
   const uint64_t m_tab = EMIT && MZS_LOOKUP_EMIT_UNROLL ? offsets[(uint64_t)1 << bits] : 0;  // table entries
   for (uint64_t i = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; i < nq; i += (uint64_t)gridDim.x * kLTPB) {
@@ -132,11 +138,19 @@ __global__ void __launch_bounds__(kLTPB) lookup1_kernel(const uint64_t* __restri
       if (o == o_end) continue;
       // the hits are the first o_end - o entries from first[i] on whose fingerprint is f;
       // first[i] itself is one (no need to read its fingerprint again)
-      const uint64_t e0 = first[i];
-      if (POS1 && o + 1 == o_end) {
-        if (o < hit_cap) hit_pos[o] = e0;  // the position itself
-        continue;
+      uint64_t e0 = first[i];
+      if (POS1 && !(e0 & kScanFlag)) {
+        if (o + 1 == o_end) {
+          if (o < hit_cap) hit_pos[o] = e0;  // the position itself
+          continue;
+        }
+        if (side) {  // 2..14 hits: their positions, copied from the count step's side array
+          for (uint64_t r = 0; o + r < o_end; ++r)
+            if (o + r < hit_cap) hit_pos[o + r] = side[e0 + r];
+          continue;
+        }
       }
+      if (POS1) e0 &= ~kScanFlag;
       if (o < hit_cap) hit_pos[o] = pos_tab[e0];
       if (++o == o_end) continue;
       const uint32_t f = fp_of(q[i], k);
@@ -285,31 +299,98 @@ __global__ void __launch_bounds__(kLTPB) lookup_sorted_count_pk_kernel(const uin
                                                                        int bits, const uint64_t* __restrict__ offsets,
                                                                        const uint32_t* __restrict__ fp,
                                                                        uint64_t* __restrict__ items,
-                                                                       const uint64_t* __restrict__ pos1_tab) {
+                                                                       const uint64_t* __restrict__ pos1_tab,
+                                                                       uint64_t* __restrict__ side = nullptr) {
   // pos1_tab (the POS1 emit): a query with one hit carries that hit's POSITION in the item's low
   // word -- read here, where the slices are walked in bucket order and the reads nearly in order,
   // instead of by a random 8-byte read (~128 B of DRAM traffic) per hit in the query-order emit;
-  // a position >= 2^32 forces c = 15 (recounted by the unpack)
-  for (uint64_t j = (uint64_t)blockIdx.x * kLTPB + threadIdx.x; j < nq; j += (uint64_t)gridDim.x * kLTPB) {
-    const uint64_t i = ord[j];
-    const uint32_t f = fps[j];
-    const uint64_t b = f >> (32 - bits);
-    const uint64_t lo = offsets[b], hi = offsets[b + 1];
-    uint32_t cnt = 0;
-    uint64_t e0 = lo;
-    for (uint64_t e = lo; e < hi; ++e) {
-      if (fp[e] == f) {
-        if (cnt == 0) e0 = e;
+  // a position >= 2^32 forces c = 15 (recounted by the unpack).
+  // side (with pos1_tab): a query with 2..14 hits writes their positions, in table order, to
+  // side[s .. s + cnt) and carries s instead of its first match, so the emit copies them
+  // instead of scanning the slice again in query order.  Every warp owns a private region of
+  // qw = (its share of the queries, rounded up to 32) slots and a private fill counter (no
+  // atomics: one global counter serialised the kernel at ~2x its time); a query that does not
+  // fit its warp's region takes c = 15 (recount + scan).  The loop is warp-uniform (the slot
+  // scan is a warp collective).  side holds nwarps * qw <= nq + 32 * nwarps entries.
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (kLTPB / 32);
+  const uint64_t qw = (nq + 32 * nwarps - 1) / (32 * nwarps) * 32;
+  const uint64_t region = ((uint64_t)blockIdx.x * (kLTPB / 32) + (threadIdx.x >> 5)) * qw;
+  uint64_t used = 0;  // warp-uniform
+  for (uint64_t j0 = (uint64_t)blockIdx.x * kLTPB + (threadIdx.x & ~31u); j0 < nq; j0 += (uint64_t)gridDim.x * kLTPB) {
+    const uint64_t j = j0 + lane;
+    const bool valid = j < nq;
+    uint64_t i = 0, lo = 0, e0 = 0, e1 = 0, e2 = 0, e3 = 0;  // the first four matches
+    uint32_t f = 0, cnt = 0;
+    if (valid) {
+      i = ord[j];
+      f = fps[j];
+      const uint64_t b = f >> (32 - bits);
+      lo = offsets[b];
+      const uint64_t hi = offsets[b + 1];
+      e0 = lo;
+      auto record = [&](uint64_t eh) {
+        if (cnt == 0) e0 = eh;
+        else if (cnt == 1) e1 = eh;
+        else if (cnt == 2) e2 = eh;
+        else if (cnt == 3) e3 = eh;
         ++cnt;
+      };
+      // four independent fingerprint loads per step; the (rare) matches are recorded off the
+      // main path, so the loop stays short and several loads stay in flight
+      uint64_t e = lo;
+      for (; e + 4 <= hi; e += 4) {
+        const uint32_t f0 = fp[e], f1 = fp[e + 1], f2 = fp[e + 2], f3 = fp[e + 3];
+        uint32_t mm = (uint32_t)(f0 == f) | ((uint32_t)(f1 == f) << 1) | ((uint32_t)(f2 == f) << 2) |
+                      ((uint32_t)(f3 == f) << 3);
+        while (mm) {
+          record(e + (uint32_t)(__ffs(mm) - 1));
+          mm &= mm - 1;
+        }
       }
+      for (; e < hi; ++e)
+        if (fp[e] == f) record(e);
     }
     uint32_t c = (cnt >= 15 || (e0 >> 32) != 0) ? 15u : cnt;
     uint64_t lo32 = e0;
-    if (pos1_tab && c == 1) {
+    if (pos1_tab && valid && c == 1) {
       lo32 = pos1_tab[e0];
       if (lo32 >> 32) c = 15;
     }
-    items[j] = ((uint64_t)(((uint32_t)i << 4) | c) << 32) | (uint32_t)lo32;
+    if (side) {
+      const uint32_t need = (valid && cnt >= 2 && cnt <= 14) ? cnt : 0u;  // (c may be 15 from e0 >= 2^32)
+      uint32_t incl = need;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      const uint64_t base = used;
+      used += tot;
+      if (need) {
+        const uint64_t my = base + incl - need;
+        if (my + need <= qw) {
+          uint64_t* const sd = side + region + my;
+          if (need <= 4) {  // the matches the scan kept (the common case: no second scan)
+            sd[0] = pos1_tab[e0];
+            sd[1] = pos1_tab[e1];
+            if (need > 2) sd[2] = pos1_tab[e2];
+            if (need > 3) sd[3] = pos1_tab[e3];
+          } else {
+            uint32_t r = 0;
+            for (uint64_t e = e0; r < need; ++e) {
+              if (fp[e] == f) sd[r++] = pos1_tab[e];
+            }
+          }
+          c = cnt;
+          lo32 = region + my;
+        } else {
+          c = 15;  // no room: recounted and scanned in query order
+        }
+      }
+    }
+    if (valid) items[j] = ((uint64_t)(((uint32_t)i << 4) | c) << 32) | (uint32_t)lo32;
   }
 }
 
@@ -339,6 +420,7 @@ __global__ void __launch_bounds__(kLTPB) lookup_unpack_kernel(const uint64_t* __
         }
       }
       if (pos1_tab && cnt == 1) e0 = pos1_tab[e0];  // (POS1) the only hit's position
+      else if (pos1_tab && cnt >= 2) e0 |= kScanFlag;  // a table index: the emit scans from it
       hit_off[i] = cnt;
     } else {
       hit_off[i] = c;
@@ -375,6 +457,7 @@ __device__ __forceinline__ void unpack_one(uint64_t it, uint64_t i, const uint64
       }
     }
     if (pos1_tab && cnt == 1) e0 = pos1_tab[e0];
+    else if (pos1_tab && cnt >= 2) e0 |= kScanFlag;  // a table index: the emit scans from it
   }
 }
 __global__ void __launch_bounds__(kLTPB) lookup_unpack_scan_kernel(const uint64_t* __restrict__ items, uint64_t nq,
@@ -551,6 +634,7 @@ MZS_API size_t seedtable_lookup_workspace_bytes(uint64_t nq) {
   z.take<uint64_t>((nq + kSB - 1) / kSB + 1);
   z.take<uint64_t>(1);
   z.take<uint64_t>(nq);  // first matching entry per query
+  z.take<uint64_t>(nq + (1u << 19));  // (sorted lookup) multi-hit positions from the count step (per-warp regions)
   // (sorted lookup) query fingerprints and indices, the sorted copies and the sort's scratch
   // (sized for the 4 passes of bucket_bits 25..30, enough for any bits)
   z.take<uint32_t>(nq + 1);
@@ -589,6 +673,7 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
   uint64_t* bsum = c.take<uint64_t>(nb + 1);
   c.take<uint64_t>(1);
   uint64_t* first = c.take<uint64_t>(nq);
+  uint64_t* side = c.take<uint64_t>(nq + (1u << 19));
   uint32_t* fpq = c.take<uint32_t>(nq + 1);
   uint64_t* idx = c.take<uint64_t>(nq + 1);
   uint32_t* fps = c.take<uint32_t>(nq + 1);
@@ -616,7 +701,13 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
       // emit, which then reads pos_tab only for multi-hit queries (MZS_LOOKUP_NO_POS1: off)
       static const bool pos1_env = getenv("MZS_LOOKUP_NO_POS1") == nullptr;
       const uint64_t* pos1_tab = (pos1_env && hit_cap && kEmitLanes == 1) ? pos_tab : nullptr;
-      lookup_sorted_count_pk_kernel<<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pk, pos1_tab);
+      static const bool side_env = getenv("MZS_LOOKUP_NO_SIDE") == nullptr;
+      const bool use_side = pos1_tab != nullptr && side_env;
+      // per-warp side regions: g * 8 warps of qw slots <= nq + 32 * g * 8 <= nq + 2^19 (g <= 2048)
+      const bool side_fits = (uint64_t)g * (kLTPB / 32) * 32 <= (1u << 19) && nq + (1u << 19) < (1ull << 32);
+      const bool use_side2 = use_side && side_fits;
+      lookup_sorted_count_pk_kernel<<<g, kLTPB, 0, st>>>(fps, ord, nq, bucket_bits, offsets, fp, pk, pos1_tab,
+                                                         use_side2 ? side : nullptr);
       MZS_LAUNCHED();
       rc = sort_items(pk, nq, 4, 4 + qbits, pq, sws, sort_ws, st);
       if (rc) return rc;
@@ -649,7 +740,7 @@ MZS_API int seedtable_lookup(const uint64_t* qkey, uint64_t nq, const uint64_t* 
         // query (ballots) keep the scans short and the warp converged
         if (kEmitLanes == 1 && pos1_tab) {
           lookup1_kernel<true, true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab,
-                                                          hit_off, hit_pos, hit_cap, first);
+                                                          hit_off, hit_pos, hit_cap, first, use_side2 ? side : nullptr);
         } else if (kEmitLanes == 1) {
           lookup1_kernel<true><<<g, kLTPB, 0, st>>>(qkey, nq, nullptr, k, bucket_bits, offsets, fp, pos_tab, hit_off,
                                                     hit_pos, hit_cap, first);

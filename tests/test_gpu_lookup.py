@@ -143,6 +143,24 @@ def test_sorted_lookup_single_hit_positions(pos_hi):
     assert np.array_equal(hp[:t], hp_w)
 
 
+def test_sorted_lookup_multi_hit_side_overflow():
+    """The sorted lookup's count step copies the positions of 2..14-hit queries to a side array
+    of nq entries; here every query has ~10 hits, so the array fills after ~nq/10 queries and the
+    rest are recounted and scanned in query order.  Hits equal the oracle's either way."""
+    k, bits = 15, 24
+    rng = np.random.default_rng(77)
+    m, nq = 400_000, (1 << 20) + 3
+    key = rng.integers(0, 40_000, size=m, dtype=np.uint64)      # each key ~10 times
+    pos = np.sort(rng.choice(10 ** 9, size=m, replace=False)).astype(np.uint64)
+    q = key[rng.integers(0, m, size=nq)]
+    wo, wf, wp = O.seedtable(key, pos, k, bits)
+    ho_w, hp_w = O.lookup(q, k, bits, wo, wf, wp)
+    ho, hp, t = _gpu_lookup(key, pos, q, k, bits)
+    assert t == len(hp_w)
+    assert np.array_equal(ho[: nq + 1], ho_w)
+    assert np.array_equal(hp[:t], hp_w)
+
+
 @pytest.mark.parametrize("span", [1000, 20])
 def test_sorted_lookup_heavy_repeats(span):
     """The sorted lookup's packed per-query result carries hit counts up to 14; queries with 15
