@@ -1080,7 +1080,9 @@ int launch_doubling(const void* xv, void* yv, uint64_t n, uint32_t w, cudaStream
     // 4-byte types: 32 values per lane keep w = 128 and 256 in registers too
     if constexpr (sizeof(T) == 4) {
       if (w == 128 && n >= 4096 && !env_flag("MZS_SLSUM_NO_WARP32")) return launch_doubling_warp<Op, 128, 32>(xv, yv, n, w, st);
-      if (w == 256 && n >= 4096 && !env_flag("MZS_SLSUM_NO_WARP32")) return launch_doubling_warp<Op, 256, 32>(xv, yv, n, w, st);
+      // (w = 256 takes the register-start kernel below: its 4-way finish needs no shared-memory
+      // round there, 393 against 353 Gelem/s)
+      if (w == 256 && n >= 4096 && env_flag("MZS_SLSUM_WARP32_256")) return launch_doubling_warp<Op, 256, 32>(xv, yv, n, w, st);
     }
     // w = 3..15 outside the powers of two: finishing combine in registers too
     if (w == 3) return launch_doubling_warp<Op, 3>(xv, yv, n, w, st);
