@@ -21,6 +21,8 @@ Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
   * orc_mz      Fig. 2 caption facts on a constructed
                 instance, SPEC.md examples, numpy argmin brute force, exhaustive
                 4^L strings, density band (L85), invariants.
+  * orc_mz_ties hand examples, a pure-Python brute force from the reading (R35), equality
+                with orc_mz when no window repeats a key, containment of orc_mz's set.
   * orc_seedtable  sort-based construction (Python sorted), partition property.
   * orc_kmer_rc / canonical keys: hand-computed reverse complements, involution, the
                 canonical code of a k-mer equals that of its reverse complement, and strand
@@ -71,6 +73,8 @@ def lib():
         L.orc_hash_array.argtypes = [vp, vp, u64, i32]
         L.orc_mz.argtypes = [vp, u64, i32, i32, vp, u64, i32, u64, u64, u64, vp, vp, u64]
         L.orc_mz.restype = i64
+        L.orc_mz_ties.argtypes = [vp, u64, i32, i32, vp, u64, i32, u64, vp, vp, u64]
+        L.orc_mz_ties.restype = i64
         L.orc_fingerprint.argtypes = [u64, i32]
         L.orc_fingerprint.restype = u32
         L.orc_seedtable.argtypes = [vp, vp, u64, i32, i32, vp, vp, vp]
@@ -199,6 +203,23 @@ def mz(seq, k: int, w: int, read_off=None, keymode: int = KEY_HASH, pos_base: in
     pos = np.zeros(cnt, np.uint64)
     if cnt:
         L.orc_mz(_p(s), len(s), k, w, _p(ro), nreads, keymode, pos_base, win_lo, win_hi, _p(key), _p(pos), cnt)
+    return key, pos
+
+
+def mz_ties(seq, k: int, w: int, read_off=None, keymode: int = KEY_HASH, pos_base: int = 0):
+    """minimap2-compatible minimizers (R35: all tied minima, run-end windows,
+    symmetric k-mers skipped): returns (key uint64[M], pos uint64[M]) by ascending pos."""
+    s = as_bytes(seq)
+    ro = None if read_off is None else np.ascontiguousarray(read_off, dtype=np.uint64)
+    nreads = 0 if ro is None else len(ro) - 1
+    L = lib()
+    cnt = L.orc_mz_ties(_p(s), len(s), k, w, _p(ro), nreads, keymode, pos_base, None, None, 0)
+    if cnt < 0:
+        raise ValueError(f"orc_mz_ties: error {cnt}")
+    key = np.zeros(cnt, np.uint64)
+    pos = np.zeros(cnt, np.uint64)
+    if cnt:
+        L.orc_mz_ties(_p(s), len(s), k, w, _p(ro), nreads, keymode, pos_base, _p(key), _p(pos), cnt)
     return key, pos
 
 

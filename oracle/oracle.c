@@ -26,6 +26,8 @@
  *               (leftmost on ties, R2); a pair shared by adjacent
  *               windows is stored once -> the SET of (s, p') over valid windows,
  *               listed by ascending p'.
+ *   orc_mz_ties the minimap2-compatible variant (R35): every tied
+ *               minimum of every window, run-end windows, symmetric k-mers skipped.
  *   orc_seedtable  the seed pointer table + seed position table of Fig. 1
  *               (L63-65), bucketed on the top `bits` bits of the hash (R21).
  *
@@ -377,6 +379,94 @@ int64_t orc_mz(const uint8_t* s, uint64_t n, int k, int w,
         }
     }
     free(code); free(valid); free(seg); free(key); free(best); free(wvalid); free(first);
+    return cnt;
+}
+
+/*
+ * orc_mz_ties -- the minimap2-compatible variant of the minimizers (PAPER.md L87
+ * names minimap2 but fixes neither rule; the reading is DESIGN.md R35):
+ *   present k-mer  q: bases q..q+k-1 all A/C/G/T and inside one segment (read);
+ *   run            a maximal stretch of consecutive present k-mer positions (an N or a read
+ *                  start ends it);
+ *   symmetric      (canonical key modes only) forward code == reverse-complement code: the
+ *                  k-mer keeps its place in the run but is never selected;
+ *   windows        in a run of L k-mers: the L-w+1 windows of w consecutive k-mers if L >= w,
+ *                  else ONE window, the whole run (the end rule);
+ *   selection      in every window, EVERY non-symmetric k-mer whose key equals the window's
+ *                  minimum over its non-symmetric k-mers (all tied minima);
+ *   output         the selected positions, each once, ascending, with their keys.
+ * Same arguments as orc_mz, without the shard range.  Returns the record count.
+ */
+int64_t orc_mz_ties(const uint8_t* s, uint64_t n, int k, int w,
+                    const uint64_t* read_off, uint64_t nreads, int keymode, uint64_t pos_base,
+                    uint64_t* out_key, uint64_t* out_pos, uint64_t cap) {
+    if (k < 1 || k > 31 || w < 1 || keymode < ORC_KEY_HASH || keymode > ORC_KEY_CANON_RAW)
+        return ORC_EINVAL;
+    if (n < (uint64_t)k) return 0;
+    const uint64_t nk = n - (uint64_t)k + 1;
+    const int canon = keymode == ORC_KEY_CANON || keymode == ORC_KEY_CANON_RAW;
+    uint8_t* code = malloc(n), *valid = malloc(n);
+    uint64_t* seg = malloc(n * sizeof(uint64_t));
+    uint64_t* key = malloc(nk * sizeof(uint64_t));
+    uint8_t* present = malloc(nk), *sym = malloc(nk), *sel = malloc(nk);
+    if (!code || !valid || !seg || !key || !present || !sym || !sel) {
+        free(code); free(valid); free(seg); free(key); free(present); free(sym); free(sel);
+        return ORC_ENOMEM;
+    }
+    orc_encode(s, n, code, valid);
+    {
+        uint64_t r = 0;
+        for (uint64_t j = 0; j < n; j++) {
+            if (read_off) while (r + 1 < nreads && read_off[r + 1] <= j) r++;
+            seg[j] = read_off ? r : 0;
+        }
+    }
+    for (uint64_t q = 0; q < nk; q++) {
+        int ok = 1;
+        for (uint64_t j = q; j < q + (uint64_t)k; j++)
+            if (!valid[j] || seg[j] != seg[q]) { ok = 0; break; }
+        present[q] = (uint8_t)ok;
+        sym[q] = 0;
+        sel[q] = 0;
+        key[q] = 0;
+        if (!ok) continue;
+        uint64_t c = orc_kmer(code, q, k);
+        if (canon) {
+            uint64_t r = orc_kmer_rc(code, q, k);
+            if (r == c) sym[q] = 1;
+            if (r < c) c = r;
+        }
+        key[q] = (keymode == ORC_KEY_HASH || keymode == ORC_KEY_CANON) ? orc_hash(c, 2 * k) : c;
+    }
+    /* runs [a, b) of present k-mers, then their windows */
+    uint64_t a = 0;
+    while (a < nk) {
+        if (!present[a]) { a++; continue; }
+        uint64_t b = a;
+        while (b < nk && present[b]) b++;
+        const uint64_t L = b - a;
+        const uint64_t ww = L >= (uint64_t)w ? (uint64_t)w : L;     /* window length */
+        for (uint64_t i = a; i + ww <= b; i++) {                       /* window [i, i+ww) */
+            int have = 0;
+            uint64_t mn = 0;
+            for (uint64_t q = i; q < i + ww; q++)
+                if (!sym[q] && (!have || key[q] < mn)) { mn = key[q]; have = 1; }
+            if (!have) continue;
+            for (uint64_t q = i; q < i + ww; q++)
+                if (!sym[q] && key[q] == mn) sel[q] = 1;
+        }
+        a = b;
+    }
+    int64_t cnt = 0;
+    for (uint64_t q = 0; q < nk; q++) {
+        if (!sel[q]) continue;
+        if ((uint64_t)cnt < cap) {
+            if (out_key) out_key[cnt] = key[q];
+            if (out_pos) out_pos[cnt] = pos_base + q;
+        }
+        cnt++;
+    }
+    free(code); free(valid); free(seg); free(key); free(present); free(sym); free(sel);
     return cnt;
 }
 
