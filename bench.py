@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4", "lookup"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c1", "c2", "c4", "lookup", "ties"])
     ap.add_argument("--graph-reps", type=int, default=1000, help="c1: CUDA-graph replays timed (0: off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--canonical", action="store_true",
@@ -408,6 +408,59 @@ def bench_c4(args, rank=0, world=1):
     return 0
 
 
+TIES_N = 400_000_000
+# bytes per base the ties composition moves (K10): encode 1 + 0.28, keys 0.28 + 8,
+# first min sum 8 + 8, pad 8 + 8, second min sum 8 + 8, mark 16 + 0.03 (+ the output, per record)
+TIES_BYTES_PER_BASE = 1.28 + 8.28 + 16 + 16 + 16 + 16.03
+TIES_BYTES_PER_RECORD = 8 + 16 + 0.125
+
+
+def bench_ties(args):
+    """f4: minimap2-compatible minimizers (mz_extract_ties: all tied minima, run-end windows) on a
+    400 Mbp C3-shaped prefix (GC 41 %, 1 % N in runs), k=19, w=10, ASCII input resident in HBM."""
+    import torch
+    import paper_1811_10074_b200 as P
+    from synthgen import device as SD
+    from synthgen import host as H
+    hbm_peak, peak_kind, sm_max = load_peaks()
+    k, w, n = K_MER, W_WIN, TIES_N
+    c3 = H.C3()
+    seq = SD.c3_ascii(c3, lo=0, n=n, device="cuda")
+    cap = int(0.25 * n) + 1024
+    out_h = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    out_p = torch.empty(cap, dtype=torch.uint64, device="cuda")
+    d_count = torch.zeros(1, dtype=torch.uint64, device="cuda")
+    ws = torch.empty(P.mz_ties_workspace_bytes(n, k, w, P.MZ_IN_ASCII), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.mz_extract_ties(seq, k, w, capacity=cap, out_hash=out_h, out_pos=out_p, d_count=d_count, ws=ws)
+
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        ms = _timed(step, args.steps, args.warmup, stream)
+    m = int(d_count.view(torch.int64).item())
+    if m > cap:
+        raise RuntimeError(f"capacity {cap} < {m} records")
+    byts = TIES_BYTES_PER_BASE * n + TIES_BYTES_PER_RECORD * m
+    ach = byts / (ms * 1e-3) / 1e9
+    line = {
+        "metric": "minimap2-compatible minimizer extraction, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
+        "unit": "Gbases/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "f4: mz_extract_ties on a 400 Mbp C3-shaped prefix (GC 41 %, 1 % N in runs)",
+                   "k": k, "w": w, "bases": n, "records": m, "density": m / n,
+                   "l2": f"inputs and intermediates ({n * 33 / 1e9:.0f} GB) >> L2; no flush needed"},
+        "roofline": {"bound": "hbm", "kernel": "the whole composition (encode, keys, 2 x slsum MIN_U64, pad, mark, "
+                                               "scan, write)",
+                     "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                     "bytes_per_base": TIES_BYTES_PER_BASE, "peak_kind": peak_kind},
+        "clocks": clk.summary(),
+        "gpu_launches": 8 * args.steps,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def bench_lookup(args):
     """NEXT f1: batch seed lookup (Fig. 1 lookups) of read minimizers against a template table."""
     import torch
@@ -517,6 +570,10 @@ def main():
         if world > 1 and rank != 0:
             return 0          # the lookup line is a single-GPU measurement
         return bench_lookup(args)
+    if args.config == "ties":
+        if world > 1 and rank != 0:
+            return 0          # the f4 variant's line is a single-GPU measurement
+        return bench_ties(args)
     if args.config in ("c2", "c4"):
         if world > 1:
             _nccl_log_env()

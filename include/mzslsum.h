@@ -208,6 +208,26 @@ int mz_extract_path(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out,
  * (*out->d_count then holds the required count). */
 int mz_extract(const uint8_t* seq, uint64_t n, int k, int w, mz_out_t* out);
 
+/* minimap2-compatible minimizers (PAPER.md L87 names minimap2 but fixes neither
+ * rule; the reading is DESIGN.md R35).  Same inputs, key modes and outputs as mz_extract_ex,
+ * with three rules changed:
+ *   run      a maximal stretch of consecutive PRESENT k-mers (all k bases A/C/G/T, one read);
+ *            windows never leave a run, and a run of L < w k-mers is ONE window (end rule);
+ *   ties     EVERY k-mer whose key equals its window's minimum is a record (not only the
+ *            leftmost one);
+ *   strand   (MZ_KEY_CANON*) a symmetric k-mer (code = its reverse complement; even k only)
+ *            keeps its place in the run but is never selected.
+ * Output: the distinct selected (key, pos_base + q), ascending q; at most one per k-mer, so
+ * capacity = n - k + 1 always suffices.  out->items is written if non-NULL; out->hist must be
+ * NULL (SLSUM_EINVAL).  The shard range is not supported: win_lo must be 0 and win_hi
+ * UINT64_MAX (else SLSUM_EUNSUPPORTED).  Computed with two sliding window sums (Eq. 2,
+ * (+) = min, L38-41) of the keys: the window minima m_j, then M_q = max of the m_j over the
+ * windows holding q; q is a record iff key_q = M_q.  Asynchronous on `stream`; workspace
+ * mz_ties_workspace_bytes(n, k, w, kind) (about 32 B per base), or NULL to allocate. */
+size_t mz_ties_workspace_bytes(uint64_t n, int k, int w, int kind);
+int mz_extract_ties(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out,
+                    void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ seed table
  * Fig. 1 (L63-65): a pointer table over seeds + a position table.  Seeds are bucketed
  * on the top `bucket_bits` bits of the 2k-bit key (R21):

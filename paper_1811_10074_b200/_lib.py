@@ -71,6 +71,9 @@ _mz_extract_ex = _sig("mz_extract_ex", _i32, ctypes.POINTER(MzIn), _i32, _i32, _
 _mz_extract_path = _sig("mz_extract_path", _i32, ctypes.POINTER(MzIn), _i32, _i32, _i32, ctypes.POINTER(MzOut), _vp,
                         _sz, _vp, _i32)
 _mz_extract = _sig("mz_extract", _i32, _vp, _u64, _i32, _i32, ctypes.POINTER(MzOut))
+_mz_ties_ws = _sig("mz_ties_workspace_bytes", _sz, _u64, _i32, _i32, _i32)
+_mz_extract_ties = _sig("mz_extract_ties", _i32, ctypes.POINTER(MzIn), _i32, _i32, _i32, ctypes.POINTER(MzOut), _vp,
+                        _sz, _vp)
 _st_ws = _sig("seedtable_workspace_bytes", _sz, _u64, _i32)
 _st_build = _sig("seedtable_build", _i32, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 _st_build_items = _sig("seedtable_build_items", _i32, _vp, _vp, _vp, _u64, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
@@ -97,7 +100,7 @@ EXPORTS = ["slsum_strerror", "slsum_version", "slsum_run", "slsum_run_ex", "mz_e
            "seedtable_partition_workspace_bytes", "seedtable_partition", "seedtable_finalize_workspace_bytes",
            "seedtable_finalize", "seedtable_lookup_workspace_bytes", "seedtable_lookup",
            "seedtable_partition_p2p_workspace_bytes", "seedtable_partition_p2p", "seedtable_partition_p2p_items",
-           "mz_extract_path"]
+           "mz_extract_path", "mz_ties_workspace_bytes", "mz_extract_ties"]
 
 
 def strerror(rc: int) -> str:
@@ -255,6 +258,51 @@ def mz_extract(seq: torch.Tensor, k: int, w: int, **kw):
 
 
 # ---------------------------------------------------------------- seed table (Fig. 1)
+def mz_ties_workspace_bytes(n: int, k: int, w: int, kind: int = MZ_IN_ASCII) -> int:
+    return int(_mz_ties_ws(n, k, w, kind))
+
+
+def mz_extract_ties(seq: torch.Tensor, k: int, w: int, *, n: int | None = None, kind: int = MZ_IN_ASCII,
+                    invalid: torch.Tensor | None = None, read_off: torch.Tensor | None = None, pos_base: int = 0,
+                    keymode: int = MZ_KEY_HASH, capacity: int | None = None,
+                    out_hash: torch.Tensor | None = None, out_pos: torch.Tensor | None = None,
+                    d_count: torch.Tensor | None = None, out_items: torch.Tensor | None = None,
+                    ws: torch.Tensor | None = None, stream=None):
+    """minimap2-compatible minimizers (include/mzslsum.h mz_extract_ties; R35), asynchronous:
+    returns (hash, pos, d_count) device tensors, count on the device."""
+    if n is None:
+        n = seq.numel() if kind == MZ_IN_ASCII else seq.numel() * 32
+    nk = max(0, n - k + 1)
+    if capacity is None:
+        capacity = out_hash.numel() if out_hash is not None else nk
+    dev = seq.device
+    if out_hash is None:
+        out_hash = torch.empty(max(1, capacity), dtype=torch.uint64, device=dev)
+    if out_pos is None:
+        out_pos = torch.empty(max(1, capacity), dtype=torch.uint64, device=dev)
+    if d_count is None:
+        d_count = torch.zeros(1, dtype=torch.uint64, device=dev)
+    if ws is None:
+        ws = _ws(mz_ties_workspace_bytes(n, k, w, kind), dev)
+    nreads = 0 if read_off is None else read_off.numel() - 1
+    if kind == MZ_IN_ASCII:
+        _need(seq, "seq", torch.uint8, n)
+    else:
+        _need(seq, "seq (packed words)", torch.uint64, (n + 31) // 32)
+        _need(invalid, "invalid", torch.uint32, (n + 31) // 32, allow_none=True)
+    for name, t in (("out_hash", out_hash), ("out_pos", out_pos), ("out_items", out_items)):
+        _need(t, name, torch.uint64, capacity, allow_none=name == "out_items")
+    _need(d_count, "d_count", torch.uint64, 1)
+    _need(read_off, "read_off", torch.uint64, 2, allow_none=True)
+    if ws.numel() < mz_ties_workspace_bytes(n, k, w, kind):
+        raise ValueError("ws smaller than mz_ties_workspace_bytes")
+    mi = MzIn(kind, _ptr(seq), _ptr(invalid), n, _ptr(read_off), nreads, pos_base, 0, U64_MAX)
+    mo = MzOut(_ptr(out_hash), _ptr(out_pos), capacity, _ptr(d_count), _ptr(out_items), None, 0)
+    _check(_mz_extract_ties(ctypes.byref(mi), k, w, keymode, ctypes.byref(mo), _ptr(ws), ws.numel(),
+                            _stream(stream)), "mz_extract_ties")
+    return out_hash, out_pos, d_count
+
+
 def seedtable_workspace_bytes(m: int, bits: int) -> int:
     return int(_st_ws(m, bits))
 

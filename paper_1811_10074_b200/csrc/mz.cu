@@ -1272,3 +1272,318 @@ MZS_API int mz_extract(const uint8_t* seq, uint64_t n, int k, int w, mz_out_t* o
   MZS_CUDA(cudaMemcpy(&cnt, out->d_count, sizeof(cnt), cudaMemcpyDeviceToHost));
   return cnt > out->capacity ? SLSUM_ECAPACITY : SLSUM_OK;
 }
+
+// ------------------------------------------------------------------ minimap2-compatible variant
+// mz_extract_ties (R35): every tied minimum of every window, windows kept
+// inside runs of present k-mers (a run shorter than w is one window), symmetric k-mers never
+// selected.  Built from two sliding window sums of the paper (Eq. 2 with (+) = min, PAPER.md
+// L38-41): with K_q = key+1 for a present k-mer (0 if absent, ~0 if symmetric),
+//   m_j = min(K_j .. K_{j+w-1})            (0 iff window j leaves its run)
+//   M_q = max(m_j : j in [q-w+1, q])        (= ~min(~m_j), the same min sum on a padded copy)
+// k-mer q is selected iff K_q = M_q: the windows of its run containing q all have m_j <= K_q,
+// and one has m_j = K_q iff q is a tied minimum of it.  M_q = 0 iff q's run is shorter than w;
+// there the run's minimum is found by a scan of the (< w) run.
+namespace mzs {
+namespace {
+constexpr uint64_t kTieSym = ~0ull;
+constexpr int kTieTPB = 256;
+constexpr int kTieBlk = kTieTPB * 32;  // positions per mark/write block (one bitmap word per thread)
+
+template <int KK>
+__global__ void __launch_bounds__(256) ties_key_kernel(MzArgs a, uint64_t nk, uint64_t* __restrict__ K) {
+  const int k = KK ? KK : a.k;  // KK != 0: compile-time k (the C1/C3/C4 values), masks and shifts fold
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nk; q += (uint64_t)gridDim.x * blockDim.x) {
+    bool ok = (inv_window64(a, (int64_t)q) & ((1ull << k) - 1ull)) == 0;
+    if (ok && a.read_off) {
+      const uint64_t r = upper_read(a, (int64_t)q);  // first read starting after q
+      ok = !(r <= a.nreads && __ldg(a.read_off + r) <= q + (uint64_t)k - 1);
+    }
+    uint64_t v = 0;
+    if (ok) {
+      const uint64_t A = ldw(a, (int64_t)(q >> 5)), B = ldw(a, (int64_t)(q >> 5) + 1);
+      const uint32_t off = (uint32_t)(q & 31) * 2;
+      const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
+      const uint64_t code = X >> (64 - 2 * k);
+      if (a.canon && revcomp64(code, k) == code) {
+        v = kTieSym;
+      } else {
+        v = 1 + (2 * k > 32 ? key_from_words<true, (2 * KK > 32 ? KK : 0)>(a, (int64_t)q, A, B)
+                            : key_from_words<false, (2 * KK > 32 ? 0 : KK)>(a, (int64_t)q, A, B));
+      }
+    }
+    K[q] = v;
+  }
+}
+
+// c[t] = ~m[t - (w-1)] inside, ~0 (m = 0: no window) in the w-1 pads on each side
+__global__ void __launch_bounds__(256) ties_pad_kernel(const uint64_t* __restrict__ m, uint64_t nw, uint32_t w,
+                                                       uint64_t* __restrict__ c, uint64_t nc) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nc; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = t - (uint64_t)(w - 1);
+    c[t] = (t >= (uint64_t)(w - 1) && j < nw) ? ~__ldg(m + j) : ~0ull;
+  }
+}
+
+// selection bitmap (bit q & 31 of word q >> 5) and per-block counts.
+// INLINE = false: z = ~M from the second sliding sum.  INLINE = true (w <= kTieInlineW): z = m,
+// the window minima themselves; the block stages m_{base-w+1 .. base+kTieBlk-1} (0 outside
+// [0, nw)) in shared memory and takes M_q = max(m_{q-w+1} .. m_q) there (w - 1 compares per
+// k-mer, no padded copy and no second sum in HBM).
+constexpr int kTieInlineW = 32;
+template <bool INLINE>
+__global__ void __launch_bounds__(kTieTPB) ties_mark_kernel(const uint64_t* __restrict__ K, const uint64_t* __restrict__ z,
+                                                            uint64_t nk, uint64_t nw, int w, uint32_t* __restrict__ bits,
+                                                            uint64_t* __restrict__ blkcnt) {
+  extern __shared__ uint64_t s_m[];
+  const uint64_t base = (uint64_t)blockIdx.x * kTieBlk;
+  if (INLINE) {
+    for (int t = threadIdx.x; t < kTieBlk + w - 1; t += kTieTPB) {
+      const uint64_t j = base + (uint64_t)t - (uint64_t)(w - 1);  // wraps below 0: >= nw
+      s_m[t] = j < nw ? __ldg(z + j) : 0ull;
+    }
+    __syncthreads();
+  }
+  uint32_t cnt = 0;
+  for (int r = 0; r < 32; ++r) {
+    const uint64_t q = base + (uint64_t)r * kTieTPB + threadIdx.x;
+    bool f = false;
+    if (q < nk) {
+      const uint64_t kq = __ldg(K + q);
+      if (kq != 0 && kq != kTieSym) {
+        uint64_t M;
+        if (INLINE) {
+          const int t0 = r * kTieTPB + threadIdx.x;
+          M = s_m[t0];
+          for (int d = 1; d < w; ++d) M = max(M, s_m[t0 + d]);
+        } else {
+          M = ~__ldg(z + q);
+        }
+        if (M != 0) {
+          f = kq == M;
+        } else {  // run shorter than w: the whole run is the window
+          uint64_t mn = kq;
+          for (uint64_t j = q; j > 0;) {
+            const uint64_t v = __ldg(K + --j);
+            if (v == 0) break;
+            mn = min(mn, v);
+          }
+          for (uint64_t j = q + 1; j < nk; ++j) {
+            const uint64_t v = __ldg(K + j);
+            if (v == 0) break;
+            mn = min(mn, v);
+          }
+          f = kq == mn;
+        }
+      }
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0 && base + (uint64_t)r * kTieTPB + threadIdx.x < nk)
+      bits[(base + (uint64_t)r * kTieTPB + threadIdx.x) >> 5] = b;
+    cnt += (threadIdx.x & 31) == 0 ? __popc(b) : 0u;
+  }
+  __shared__ uint32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) blkcnt[blockIdx.x] = s_cnt;
+}
+
+// exclusive scan of the block counts (one CTA); d_count = the total
+__global__ void __launch_bounds__(1024) ties_scan_kernel(const uint64_t* __restrict__ blkcnt, uint64_t nblk,
+                                                         uint64_t* __restrict__ blkoff, uint64_t* __restrict__ d_count) {
+  __shared__ uint64_t s_warp[32];
+  __shared__ uint64_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (uint64_t b0 = 0; b0 < nblk; b0 += 1024) {
+    const uint64_t b = b0 + threadIdx.x;
+    const uint64_t v = b < nblk ? blkcnt[b] : 0;
+    uint64_t x = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t t = s_warp[lane];
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, t, d);
+        if (lane >= d) t += y;
+      }
+      s_warp[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint64_t incl = x + (wid ? s_warp[wid - 1] : 0) + s_carry;
+    if (b < nblk) blkoff[b] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *d_count = s_carry;
+}
+
+// ordered output: thread t of block b owns bitmap word b * 256 + t
+__global__ void __launch_bounds__(kTieTPB) ties_write_kernel(MzArgs a, const uint64_t* __restrict__ K, uint64_t nk,
+                                                             const uint32_t* __restrict__ bits,
+                                                             const uint64_t* __restrict__ blkoff) {
+  __shared__ uint32_t s_warp[kTieTPB / 32];
+  const uint64_t wi = (uint64_t)blockIdx.x * kTieTPB + threadIdx.x;
+  const uint64_t nwords = (nk + 31) / 32;
+  uint32_t word = wi < nwords ? bits[wi] : 0u;
+  const uint32_t c = __popc(word);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = c;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) s_warp[wid] = x;
+  __syncthreads();
+  uint32_t pre = 0;
+  for (int i = 0; i < wid; ++i) pre += s_warp[i];
+  uint64_t o = blkoff[blockIdx.x] + pre + x - c;
+  const int k = a.k;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1;
+    const uint64_t q = wi * 32 + (uint64_t)b;
+    if (o < a.capacity) {
+      const uint64_t h = __ldg(K + q) - 1;
+      a.out_hash[o] = h;
+      a.out_pos[o] = a.pos_base + q;
+      if (a.out_items) a.out_items[o] = item_of(h, k, a.pos_base + q);
+    }
+    ++o;
+  }
+}
+
+uint64_t ties_grid(uint64_t n) { return std::min<uint64_t>((n + 255) / 256, 148ull * 16); }
+}  // namespace
+}  // namespace mzs
+
+MZS_API size_t mz_ties_workspace_bytes(uint64_t n, int k, int w, int kind) {
+  Sizer z;
+  z.take<uint64_t>(ridx_entries(n));
+  if (kind == MZ_IN_ASCII) {
+    z.take<uint64_t>((n + 31) / 32 + 1);
+    z.take<uint32_t>((n + 31) / 32 + 1);
+  }
+  const uint64_t nk = (k >= 1 && n >= (uint64_t)k) ? n - (uint64_t)k + 1 : 0;
+  const uint64_t ww = w >= 1 ? (uint64_t)w : 1;
+  const uint64_t nw = nk >= ww ? nk - ww + 1 : 0;
+  const uint64_t nblk = (nk + kTieBlk - 1) / kTieBlk + 1;
+  z.take<uint64_t>(nk + 1);           // K
+  z.take<uint64_t>(nw + 1);           // m
+  z.take<uint64_t>(nw + 2 * (ww - 1) + 1);  // padded ~m
+  z.take<uint64_t>(nk + 1);           // z = ~M
+  z.take<uint32_t>((nk + 31) / 32 + 1);
+  z.take<uint64_t>(nblk);
+  z.take<uint64_t>(nblk);
+  return z.used;
+}
+
+MZS_API int mz_extract_ties(const mz_in_t* in, int k, int w, int keymode, mz_out_t* out, void* ws,
+                            size_t ws_bytes, void* stream) {
+  if (!in || !out || !out->d_count || k < 1 || k > 31 || w < 1) return SLSUM_EINVAL;
+  if (in->kind != MZ_IN_ASCII && in->kind != MZ_IN_PACKED2) return SLSUM_EINVAL;
+  if (keymode < MZ_KEY_HASH || keymode > MZ_KEY_CANON_RAW) return SLSUM_EINVAL;
+  if (in->read_off && in->nreads == 0) return SLSUM_EINVAL;
+  if (out->capacity && (!out->hash || !out->pos)) return SLSUM_EINVAL;
+  if (out->hist) return SLSUM_EINVAL;
+  if (in->win_lo != 0 || in->win_hi != UINT64_MAX) return SLSUM_EUNSUPPORTED;
+  cudaStream_t st = as_stream(stream);
+  const uint64_t n = in->n;
+  if (n < (uint64_t)k) {
+    MZS_CUDA(cudaMemsetAsync(out->d_count, 0, sizeof(uint64_t), st));
+    return SLSUM_OK;
+  }
+  if (!in->seq) return SLSUM_EINVAL;
+  TempWs tmp;
+  const size_t need = mz_ties_workspace_bytes(n, k, w, in->kind);
+  if (!ws) {
+    MZS_CUDA(cudaMallocAsync(&tmp.p, need, st));
+    tmp.s = st;
+    ws = tmp.p;
+    ws_bytes = need;
+  }
+  if (ws_bytes < need) return SLSUM_ENOMEM;
+  Carve c(ws, ws_bytes);
+  MzArgs a{};
+  uint64_t* ridx = c.take<uint64_t>(ridx_entries(n));
+  a.nwords = (n + 31) / 32;
+  if (in->kind == MZ_IN_ASCII) {
+    uint64_t* words = c.take<uint64_t>(a.nwords + 1);
+    uint32_t* inval = c.take<uint32_t>(a.nwords + 1);
+    int rc = encode_launch(static_cast<const uint8_t*>(in->seq), n, words, inval, st);
+    if (rc) return rc;
+    a.words = words;
+    a.invalid = inval;
+  } else {
+    a.words = static_cast<const uint64_t*>(in->seq);
+    a.invalid = in->invalid;
+  }
+  a.n = n;
+  a.read_off = in->read_off;
+  a.nreads = in->read_off ? in->nreads : 0;
+  if (in->read_off) {
+    const uint64_t nb = ridx_entries(n);
+    ridx_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(in->read_off, a.nreads, ridx, nb);
+    MZS_LAUNCHED();
+    a.ridx = ridx;
+  }
+  a.pos_base = in->pos_base;
+  a.k = k;
+  a.w = w;
+  a.raw = keymode == MZ_KEY_RAW || keymode == MZ_KEY_CANON_RAW;
+  a.canon = keymode == MZ_KEY_CANON || keymode == MZ_KEY_CANON_RAW;
+  a.out_hash = out->hash;
+  a.out_pos = out->pos;
+  a.out_items = out->items;
+  a.capacity = out->capacity;
+  a.d_count = out->d_count;
+  const uint64_t nk = n - (uint64_t)k + 1, ww = (uint64_t)w;
+  const uint64_t nw = nk >= ww ? nk - ww + 1 : 0;
+  const uint64_t nblk = (nk + kTieBlk - 1) / kTieBlk;
+  uint64_t* K = c.take<uint64_t>(nk + 1);
+  uint64_t* m = c.take<uint64_t>(nw + 1);
+  uint64_t* cp = c.take<uint64_t>(nw + 2 * (ww - 1) + 1);
+  uint64_t* z = c.take<uint64_t>(nk + 1);
+  uint32_t* bits = c.take<uint32_t>((nk + 31) / 32 + 1);
+  uint64_t* blkcnt = c.take<uint64_t>(nblk + 1);
+  uint64_t* blkoff = c.take<uint64_t>(nblk + 1);
+  if (!c.ok) return SLSUM_ENOMEM;
+  if (k == 19) ties_key_kernel<19><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
+  else if (k == 15) ties_key_kernel<15><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
+  else ties_key_kernel<0><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
+  MZS_LAUNCHED();
+  if (nw > 0 && w <= kTieInlineW) {
+    int rc = slsum_run_ex(SLSUM_MIN_U64, (uint32_t)w, K, m, nk, SLSUM_PATH_GENERIC, st);
+    if (rc) return rc;
+    const size_t smem = sizeof(uint64_t) * (kTieBlk + kTieInlineW - 1);
+    MZS_CUDA(cudaFuncSetAttribute(ties_mark_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ties_mark_kernel<true><<<(unsigned)nblk, kTieTPB, smem, st>>>(K, m, nk, nw, w, bits, blkcnt);
+    MZS_LAUNCHED();
+  } else if (nw > 0) {
+    int rc = slsum_run_ex(SLSUM_MIN_U64, (uint32_t)w, K, m, nk, SLSUM_PATH_GENERIC, st);
+    if (rc) return rc;
+    const uint64_t nc = nw + 2 * (ww - 1);
+    ties_pad_kernel<<<(unsigned)ties_grid(nc), 256, 0, st>>>(m, nw, (uint32_t)w, cp, nc);
+    MZS_LAUNCHED();
+    rc = slsum_run_ex(SLSUM_MIN_U64, (uint32_t)w, cp, z, nc, SLSUM_PATH_GENERIC, st);  // nc-w+1 = nk outputs
+    if (rc) return rc;
+    ties_mark_kernel<false><<<(unsigned)nblk, kTieTPB, 0, st>>>(K, z, nk, nw, w, bits, blkcnt);
+    MZS_LAUNCHED();
+  } else {
+    MZS_CUDA(cudaMemsetAsync(z, 0xff, sizeof(uint64_t) * nk, st));  // no full window: M = 0
+    ties_mark_kernel<false><<<(unsigned)nblk, kTieTPB, 0, st>>>(K, z, nk, nw, w, bits, blkcnt);
+    MZS_LAUNCHED();
+  }
+  ties_scan_kernel<<<1, 1024, 0, st>>>(blkcnt, nblk, blkoff, out->d_count);
+  MZS_LAUNCHED();
+  ties_write_kernel<<<(unsigned)nblk, kTieTPB, 0, st>>>(a, K, nk, bits, blkoff);
+  MZS_LAUNCHED();
+  return SLSUM_OK;
+}
