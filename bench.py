@@ -409,10 +409,11 @@ def bench_c4(args, rank=0, world=1):
 
 
 TIES_N = 400_000_000
-# bytes per base the ties composition moves (K10): encode 1 + 0.28, keys 0.28 + 8,
-# first min sum 8 + 8, pad 8 + 8, second min sum 8 + 8, mark 16 + 0.03 (+ the output, per record)
-TIES_BYTES_PER_BASE = 1.28 + 8.28 + 16 + 16 + 16 + 16.03
-TIES_BYTES_PER_RECORD = 8 + 16 + 0.125
+# bytes per base the ties composition moves at w <= 32 (K10): encode 1 + 0.28, keys
+# 0.28 + 8, the min sum 8 + 8, mark (K and m read, bitmap written) 16 + 0.125; per record the
+# write kernel reads K (8) and writes hash + pos (16)
+TIES_BYTES_PER_BASE = 1.28 + 8.28 + 16 + 16.125
+TIES_BYTES_PER_RECORD = 8 + 16
 
 
 def bench_ties(args):
@@ -450,12 +451,12 @@ def bench_ties(args):
         "config": {"workload": "f4: mz_extract_ties on a 400 Mbp C3-shaped prefix (GC 41 %, 1 % N in runs)",
                    "k": k, "w": w, "bases": n, "records": m, "density": m / n,
                    "l2": f"inputs and intermediates ({n * 33 / 1e9:.0f} GB) >> L2; no flush needed"},
-        "roofline": {"bound": "hbm", "kernel": "the whole composition (encode, keys, 2 x slsum MIN_U64, pad, mark, "
-                                               "scan, write)",
+        "roofline": {"bound": "hbm", "kernel": "the whole composition (encode, keys, slsum MIN_U64, mark with the "
+                                               "shared-memory max, scan, write)",
                      "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
                      "bytes_per_base": TIES_BYTES_PER_BASE, "peak_kind": peak_kind},
         "clocks": clk.summary(),
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": 6 * args.steps,
     }
     print(json.dumps(line), flush=True)
     return 0
