@@ -1289,19 +1289,31 @@ constexpr uint64_t kTieSym = ~0ull;
 constexpr int kTieTPB = 256;
 constexpr int kTieBlk = kTieTPB * 32;  // positions per mark/write block (one bitmap word per thread)
 
+// K_q = key + 1 for a present k-mer, 0 for an absent one (an N or a read start inside it),
+// kTieSym for a symmetric one.  One packed word (32 k-mers) per thread: the word pair and the
+// 64 validity bits are loaded once, the 32 keys are staged in shared memory (row t*33:
+// conflict-free both ways) and written out coalesced.  8192 k-mers per CTA; KK != 0: the
+// compile-time k (C1/C3/C4 values), masks and shifts fold.
 template <int KK>
-__global__ void __launch_bounds__(256) ties_key_kernel(MzArgs a, uint64_t nk, uint64_t* __restrict__ K) {
-  const int k = KK ? KK : a.k;  // KK != 0: compile-time k (the C1/C3/C4 values), masks and shifts fold
-  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nk; q += (uint64_t)gridDim.x * blockDim.x) {
-    bool ok = (inv_window64(a, (int64_t)q) & ((1ull << k) - 1ull)) == 0;
+__global__ void __launch_bounds__(256) ties_key_tile_kernel(MzArgs a, uint64_t nk, uint64_t* __restrict__ K) {
+  extern __shared__ uint64_t s_k[];
+  const int k = KK ? KK : a.k;
+  const uint64_t base = (uint64_t)blockIdx.x * kTieBlk;
+  const int64_t wi = (int64_t)(base >> 5) + threadIdx.x;
+  const uint64_t A = ldw(a, wi), B = ldw(a, wi + 1);
+  const uint64_t inv = (uint64_t)ldi(a, wi) | ((uint64_t)ldi(a, wi + 1) << 32);
+  const uint64_t kmask = (1ull << k) - 1ull;
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) {
+    const uint64_t q = (uint64_t)wi * 32 + (uint64_t)r;
+    bool ok = q < nk && ((inv >> r) & kmask) == 0;
     if (ok && a.read_off) {
-      const uint64_t r = upper_read(a, (int64_t)q);  // first read starting after q
-      ok = !(r <= a.nreads && __ldg(a.read_off + r) <= q + (uint64_t)k - 1);
+      const uint64_t rr = upper_read(a, (int64_t)q);
+      ok = !(rr <= a.nreads && __ldg(a.read_off + rr) <= q + (uint64_t)k - 1);
     }
     uint64_t v = 0;
     if (ok) {
-      const uint64_t A = ldw(a, (int64_t)(q >> 5)), B = ldw(a, (int64_t)(q >> 5) + 1);
-      const uint32_t off = (uint32_t)(q & 31) * 2;
+      const uint32_t off = (uint32_t)r * 2;
       const uint64_t X = off ? (A << off) | (B >> (64 - off)) : A;
       const uint64_t code = X >> (64 - 2 * k);
       if (a.canon && revcomp64(code, k) == code) {
@@ -1311,7 +1323,12 @@ __global__ void __launch_bounds__(256) ties_key_kernel(MzArgs a, uint64_t nk, ui
                             : key_from_words<false, (2 * KK > 32 ? 0 : KK)>(a, (int64_t)q, A, B));
       }
     }
-    K[q] = v;
+    s_k[threadIdx.x * 33 + r] = v;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < kTieBlk; j += 256) {
+    const uint64_t q = base + (uint64_t)j;
+    if (q < nk) K[q] = s_k[(j >> 5) * 33 + (j & 31)];
   }
 }
 
@@ -1555,10 +1572,13 @@ MZS_API int mz_extract_ties(const mz_in_t* in, int k, int w, int keymode, mz_out
   uint64_t* blkcnt = c.take<uint64_t>(nblk + 1);
   uint64_t* blkoff = c.take<uint64_t>(nblk + 1);
   if (!c.ok) return SLSUM_ENOMEM;
-  if (k == 19) ties_key_kernel<19><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
-  else if (k == 15) ties_key_kernel<15><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
-  else ties_key_kernel<0><<<(unsigned)ties_grid(nk), 256, 0, st>>>(a, nk, K);
-  MZS_LAUNCHED();
+  {
+    const size_t ksm = sizeof(uint64_t) * 256 * 33;
+    auto kfn = k == 19 ? ties_key_tile_kernel<19> : k == 15 ? ties_key_tile_kernel<15> : ties_key_tile_kernel<0>;
+    MZS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm));
+    kfn<<<(unsigned)nblk, 256, ksm, st>>>(a, nk, K);
+    MZS_LAUNCHED();
+  }
   if (nw > 0 && w <= kTieInlineW) {
     int rc = slsum_run_ex(SLSUM_MIN_U64, (uint32_t)w, K, m, nk, SLSUM_PATH_GENERIC, st);
     if (rc) return rc;
