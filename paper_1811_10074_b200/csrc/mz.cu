@@ -1343,53 +1343,64 @@ __global__ void __launch_bounds__(256) ties_pad_kernel(const uint64_t* __restric
 
 // selection bitmap (bit q & 31 of word q >> 5) and per-block counts.
 // INLINE = false: z = ~M from the second sliding sum.  INLINE = true (w <= kTieInlineW): z = m,
-// the window minima themselves; the block stages m_{base-w+1 .. base+kTieBlk-1} (0 outside
-// [0, nw)) in shared memory and takes M_q = max(m_{q-w+1} .. m_q) there (w - 1 compares per
-// k-mer, no padded copy and no second sum in HBM).
+// the window minima themselves; the block stages them in shared memory a quarter of its k-mers
+// at a time (16.6 KB, so 8 CTAs fit per SM) and tests K_q against m_{q-w+1} .. m_q there (w
+// equality tests per k-mer, no padded copy and no second sum in HBM).
 constexpr int kTieInlineW = 32;
+// k-mer q of a run shorter than w (no full window holds it): the whole run is the window
+__device__ __forceinline__ bool tie_short_run(const uint64_t* __restrict__ K, uint64_t nk, uint64_t q, uint64_t kq) {
+  uint64_t mn = kq;
+  for (uint64_t j = q; j > 0;) {
+    const uint64_t v = __ldg(K + --j);
+    if (v == 0) break;
+    mn = min(mn, v);
+  }
+  for (uint64_t j = q + 1; j < nk; ++j) {
+    const uint64_t v = __ldg(K + j);
+    if (v == 0) break;
+    mn = min(mn, v);
+  }
+  return kq == mn;
+}
+constexpr int kTieQuarter = kTieBlk / 4;  // INLINE: the block stages m a quarter at a time
 template <bool INLINE>
 __global__ void __launch_bounds__(kTieTPB) ties_mark_kernel(const uint64_t* __restrict__ K, const uint64_t* __restrict__ z,
                                                             uint64_t nk, uint64_t nw, int w, uint32_t* __restrict__ bits,
                                                             uint64_t* __restrict__ blkcnt) {
   extern __shared__ uint64_t s_m[];
   const uint64_t base = (uint64_t)blockIdx.x * kTieBlk;
-  if (INLINE) {
-    for (int t = threadIdx.x; t < kTieBlk + w - 1; t += kTieTPB) {
-      const uint64_t j = base + (uint64_t)t - (uint64_t)(w - 1);  // wraps below 0: >= nw
-      s_m[t] = j < nw ? __ldg(z + j) : 0ull;
-    }
-    __syncthreads();
-  }
   uint32_t cnt = 0;
   for (int r = 0; r < 32; ++r) {
+    if (INLINE && r % (kTieQuarter / kTieTPB) == 0) {
+      // stage m_{qb-w+1 .. qb+kTieQuarter-1} (0 outside [0, nw)) for this quarter's k-mers
+      const uint64_t qb = base + (uint64_t)r * kTieTPB;
+      __syncthreads();
+      for (int t = threadIdx.x; t < kTieQuarter + w - 1; t += kTieTPB) {
+        const uint64_t j = qb + (uint64_t)t - (uint64_t)(w - 1);  // wraps below 0: >= nw
+        s_m[t] = j < nw ? __ldg(z + j) : 0ull;
+      }
+      __syncthreads();
+    }
     const uint64_t q = base + (uint64_t)r * kTieTPB + threadIdx.x;
     bool f = false;
     if (q < nk) {
       const uint64_t kq = __ldg(K + q);
       if (kq != 0 && kq != kTieSym) {
-        uint64_t M;
         if (INLINE) {
-          const int t0 = r * kTieTPB + threadIdx.x;
-          M = s_m[t0];
-          for (int d = 1; d < w; ++d) M = max(M, s_m[t0 + d]);
+          // every m_j of a window holding q is <= K_q, so K_q = max_j m_j iff some m_j = K_q;
+          // all m_j = 0 iff q's run is shorter than w
+          const int t0 = (r % (kTieQuarter / kTieTPB)) * kTieTPB + threadIdx.x;
+          bool eq = false;
+          uint64_t nz = 0;
+          for (int d = 0; d < w; ++d) {
+            const uint64_t v = s_m[t0 + d];
+            eq |= v == kq;
+            nz |= v;
+          }
+          f = nz ? eq : tie_short_run(K, nk, q, kq);
         } else {
-          M = ~__ldg(z + q);
-        }
-        if (M != 0) {
-          f = kq == M;
-        } else {  // run shorter than w: the whole run is the window
-          uint64_t mn = kq;
-          for (uint64_t j = q; j > 0;) {
-            const uint64_t v = __ldg(K + --j);
-            if (v == 0) break;
-            mn = min(mn, v);
-          }
-          for (uint64_t j = q + 1; j < nk; ++j) {
-            const uint64_t v = __ldg(K + j);
-            if (v == 0) break;
-            mn = min(mn, v);
-          }
-          f = kq == mn;
+          const uint64_t M = ~__ldg(z + q);
+          f = M ? kq == M : tie_short_run(K, nk, q, kq);
         }
       }
     }
@@ -1582,7 +1593,7 @@ MZS_API int mz_extract_ties(const mz_in_t* in, int k, int w, int keymode, mz_out
   if (nw > 0 && w <= kTieInlineW) {
     int rc = slsum_run_ex(SLSUM_MIN_U64, (uint32_t)w, K, m, nk, SLSUM_PATH_GENERIC, st);
     if (rc) return rc;
-    const size_t smem = sizeof(uint64_t) * (kTieBlk + kTieInlineW - 1);
+    const size_t smem = sizeof(uint64_t) * (kTieQuarter + kTieInlineW - 1);
     MZS_CUDA(cudaFuncSetAttribute(ties_mark_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ties_mark_kernel<true><<<(unsigned)nblk, kTieTPB, smem, st>>>(K, m, nk, nw, w, bits, blkcnt);
     MZS_LAUNCHED();
