@@ -1453,11 +1453,14 @@ __global__ void __launch_bounds__(1024) ties_scan_kernel(const uint64_t* __restr
   if (threadIdx.x == 0) *d_count = s_carry;
 }
 
-// ordered output: thread t of block b owns bitmap word b * 256 + t
+// ordered output: thread t of block b owns bitmap word b * 256 + t.  The block's records are
+// first listed in order in shared memory (13-bit k-mer offsets within the block), then written
+// by consecutive threads to consecutive outputs (coalesced stores, K read in order).
 __global__ void __launch_bounds__(kTieTPB) ties_write_kernel(MzArgs a, const uint64_t* __restrict__ K, uint64_t nk,
                                                              const uint32_t* __restrict__ bits,
                                                              const uint64_t* __restrict__ blkoff) {
   __shared__ uint32_t s_warp[kTieTPB / 32];
+  __shared__ uint16_t s_list[kTieBlk];
   const uint64_t wi = (uint64_t)blockIdx.x * kTieTPB + threadIdx.x;
   const uint64_t nwords = (nk + 31) / 32;
   uint32_t word = wi < nwords ? bits[wi] : 0u;
@@ -1470,21 +1473,29 @@ __global__ void __launch_bounds__(kTieTPB) ties_write_kernel(MzArgs a, const uin
   }
   if (lane == 31) s_warp[wid] = x;
   __syncthreads();
-  uint32_t pre = 0;
-  for (int i = 0; i < wid; ++i) pre += s_warp[i];
-  uint64_t o = blkoff[blockIdx.x] + pre + x - c;
-  const int k = a.k;
+  uint32_t pre = 0, total = 0;
+  for (int i = 0; i < kTieTPB / 32; ++i) {
+    if (i < wid) pre += s_warp[i];
+    total += s_warp[i];
+  }
+  uint32_t lo = pre + x - c;  // block-local index of this word's first record
   while (word) {
     const int b = __ffs(word) - 1;
     word &= word - 1;
-    const uint64_t q = wi * 32 + (uint64_t)b;
-    if (o < a.capacity) {
-      const uint64_t h = __ldg(K + q) - 1;
-      a.out_hash[o] = h;
-      a.out_pos[o] = a.pos_base + q;
-      if (a.out_items) a.out_items[o] = item_of(h, k, a.pos_base + q);
-    }
-    ++o;
+    s_list[lo++] = (uint16_t)(threadIdx.x * 32 + b);
+  }
+  __syncthreads();
+  const uint64_t o0 = blkoff[blockIdx.x];
+  const uint64_t qb = (uint64_t)blockIdx.x * kTieBlk;
+  const int k = a.k;
+  for (uint32_t i = threadIdx.x; i < total; i += kTieTPB) {
+    const uint64_t o = o0 + i;
+    if (o >= a.capacity) break;
+    const uint64_t q = qb + s_list[i];
+    const uint64_t h = __ldg(K + q) - 1;
+    a.out_hash[o] = h;
+    a.out_pos[o] = a.pos_base + q;
+    if (a.out_items) a.out_items[o] = item_of(h, k, a.pos_base + q);
   }
 }
 
