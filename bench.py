@@ -444,6 +444,19 @@ def bench_ties(args):
         raise RuntimeError(f"capacity {cap} < {m} records")
     byts = TIES_BYTES_PER_BASE * n + TIES_BYTES_PER_RECORD * m
     ach = byts / (ms * 1e-3) / 1e9
+    # DRAM bytes of one step's six kernels from the committed ncu --set full capture, if any
+    tr = load_traffic("traffic_ties.json")
+    traffic = sum(v["dram_bytes"] / max(1, v.get("launches", 1)) for v in tr.values()) if tr else None
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        ns = min(n, args.cpu_sample_bases)
+        s = seq[:ns].cpu().numpy()
+        t0 = time.perf_counter()
+        O.mz_ties(s, k, w)
+        dt = time.perf_counter() - t0
+        cpu = {"value": ns / dt / 1e9, "unit": "Gbases/s", "cores": O.num_threads(), "cpu_model": cpu_model(),
+               "kind": "oracle", "sample": f"orc_mz_ties on the first {ns} bases of the prefix ({dt:.1f} s)"}
     line = {
         "metric": "minimap2-compatible minimizer extraction, Gbases/s", "value": n / (ms * 1e-3) / 1e9,
         "unit": "Gbases/s", "n_gpus": 1, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
@@ -453,9 +466,11 @@ def bench_ties(args):
                    "l2": f"inputs and intermediates ({n * 33 / 1e9:.0f} GB) >> L2; no flush needed"},
         "roofline": {"bound": "hbm", "kernel": "the whole composition (encode, keys, slsum MIN_U64, mark with the "
                                                "shared-memory max, scan, write)",
-                     "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                     "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
+                     "traffic_note": "DRAM bytes of one step's kernels, ncu --set full "
+                                     f"(profiles/r0x/traffic_ties.json); algorithmic {byts:.4g} B",
                      "bytes_per_base": TIES_BYTES_PER_BASE, "peak_kind": peak_kind},
-        "clocks": clk.summary(),
+        "cpu_baseline": cpu, "clocks": clk.summary(),
         "gpu_launches": 6 * args.steps,
     }
     print(json.dumps(line), flush=True)
