@@ -1363,6 +1363,18 @@ __device__ __forceinline__ bool tie_short_run(const uint64_t* __restrict__ K, ui
   return kq == mn;
 }
 constexpr int kTieQuarter = kTieBlk / 4;  // INLINE: the block stages m a quarter at a time
+// the w equality tests of k-mer q against s[0 .. w-1] = m_{q-w+1} .. m_q.  W > 0: w = W at compile
+// time (unrolled, immediate shared-memory offsets); W = 0: any w
+template <int W>
+__device__ __forceinline__ void tie_window_tests(const uint64_t* s, int w, uint64_t kq, bool& eq, uint32_t& nz) {
+  const int ww = W ? W : w;
+#pragma unroll
+  for (int d = 0; d < ww; ++d) {
+    const uint64_t v = s[d];
+    eq |= v == kq;
+    nz |= (uint32_t)v | (uint32_t)(v >> 32);
+  }
+}
 template <bool INLINE>
 __global__ void __launch_bounds__(kTieTPB) ties_mark_kernel(const uint64_t* __restrict__ K, const uint64_t* __restrict__ z,
                                                             uint64_t nk, uint64_t nw, int w, uint32_t* __restrict__ bits,
@@ -1391,11 +1403,13 @@ __global__ void __launch_bounds__(kTieTPB) ties_mark_kernel(const uint64_t* __re
           // all m_j = 0 iff q's run is shorter than w
           const int t0 = (r % (kTieQuarter / kTieTPB)) * kTieTPB + threadIdx.x;
           bool eq = false;
-          uint64_t nz = 0;
-          for (int d = 0; d < w; ++d) {
-            const uint64_t v = s_m[t0 + d];
-            eq |= v == kq;
-            nz |= v;
+          uint32_t nz = 0;
+          switch (w) {  // the usual window lengths unrolled (minimap2 presets: 5, 10, 11, 19)
+            case 5: tie_window_tests<5>(s_m + t0, w, kq, eq, nz); break;
+            case 10: tie_window_tests<10>(s_m + t0, w, kq, eq, nz); break;
+            case 11: tie_window_tests<11>(s_m + t0, w, kq, eq, nz); break;
+            case 19: tie_window_tests<19>(s_m + t0, w, kq, eq, nz); break;
+            default: tie_window_tests<0>(s_m + t0, w, kq, eq, nz); break;
           }
           f = nz ? eq : tie_short_run(K, nk, q, kq);
         } else {
